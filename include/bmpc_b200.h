@@ -1,0 +1,210 @@
+/* bmpc_b200 — C ABI of the B200-native branch-MPC solver.
+ *
+ * Drop-in boundary for the reference solve path (bmpc::solve,
+ * /root/reference/proj/include/bmpc/solver.hpp:595-596). Every entry point
+ * takes plain pointers and sizes; no exceptions cross it (int status +
+ * bmpc_last_error()). Reference interfaces each entry replaces are cited.
+ *
+ * Ownership: the library owns everything it returns through a `**out`
+ * argument; free it with the matching *_free / *_destroy call. Input arrays
+ * are borrowed for the duration of the call only. A bmpc_ctx is bound to one
+ * device and one CUDA stream and is not thread-safe (one host thread per ctx,
+ * like the reference's single-owner solver).
+ */
+#ifndef BMPC_B200_H
+#define BMPC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. */
+#define BMPC_OK 0
+#define BMPC_ERR_INVALID (-1)     /* bad argument (reference: std::invalid_argument) */
+#define BMPC_ERR_CUDA (-2)        /* CUDA runtime failure / no device */
+#define BMPC_ERR_UNSUPPORTED (-3) /* model kind or dimensions not compiled in */
+#define BMPC_ERR_ROLLOUT (-4)     /* nonlinear_rollout non-finite state (problem.hpp:160-162 throws) */
+#define BMPC_ERR_OUT_OF_RANGE (-5)
+
+/* Solve status (SolveStatus, solver.hpp:536). */
+#define BMPC_CONVERGED 0
+#define BMPC_MAX_ITERATIONS 1
+#define BMPC_ERROR 2
+
+/* Model families (the reference's per-node callbacks, problem.hpp:15-40,
+ * restated as device functions). */
+#define BMPC_MODEL_UNICYCLE 1          /* unicycle RK4 + tracking + ego constraints (scenarios.hpp) */
+#define BMPC_MODEL_AFFINE_QUADRATIC 2  /* affine dynamics + quadratic cost (oracles.hpp:316 random_lq_problem) */
+
+const char* bmpc_last_error(void);
+const char* bmpc_version(void);
+
+/* ------------------------------------------------------------------ tree */
+/* TreeTopology (tree.hpp:28-44) as flat arrays, bit-identical to build_tree
+ * (tree.hpp:61-128). Children of a node are contiguous in BFS order, so they
+ * are given as [first_child, first_child + child_count). */
+typedef struct bmpc_tree {
+  int node_count;
+  int horizon;
+  int last_branch_step; /* -1 for a path graph */
+  int leaf_count;
+  int* parent;      /* [node_count], -1 at the root */
+  int* time_step;   /* [node_count] */
+  double* weight;   /* [node_count] path probability */
+  int* first_child; /* [node_count], -1 at leaves */
+  int* child_count; /* [node_count] */
+  int* step_begin;  /* [horizon + 2] */
+  int* leaves;      /* [leaf_count] ascending */
+} bmpc_tree;
+
+/* build_tree(horizon, branchings) (tree.hpp:61). weights is n_branchings
+ * rows of max_arity entries (row b holds arities[b] weights). */
+int bmpc_tree_build(int horizon, int n_branchings, const int* steps, const int* arities, const double* weights,
+                    int max_arity, bmpc_tree** out);
+void bmpc_tree_free(bmpc_tree* tree);
+
+/* -------------------------------------------------------------- problem */
+/* Device model descriptor: what the reference captures inside its
+ * std::function callbacks, as plain per-node arrays. */
+typedef struct bmpc_model_desc {
+  int kind;
+  int state_dim;
+  int input_dim;
+  const double* initial_state; /* [state_dim] (BmpcProblem::initial_state) */
+  /* BMPC_MODEL_UNICYCLE (state_dim 4, input_dim 2) */
+  double dt;
+  double state_weights[16];    /* Wx, column-major 4x4 (tracking_cost, problem.hpp:194) */
+  double input_weights[4];     /* Wu, 2x2 */
+  double terminal_weights[16]; /* Wf, 4x4 (tracking_terminal_cost, problem.hpp:211) */
+  double accel_limit, yaw_rate_limit, safety_radius; /* ego_constraints (scenarios.hpp:206) */
+  int num_vehicles;                                  /* <= 4 */
+  const double* reference;        /* [node][4] tracking reference */
+  const double* vehicle_position; /* [node][num_vehicles][2] */
+  /* BMPC_MODEL_AFFINE_QUADRATIC: column-major blocks per node
+   *   non-leaf: A[nx*nx] B[nx*nu] c[nx] Q[nx*nx] R[nu*nu] M[nu*nx] q[nx] r[nu]
+   *   leaf:     P[nx*nx] p[nx]                                               */
+  const double* lq_stage; /* [node][stage record] */
+  const double* lq_leaf;  /* [node][nx*nx + nx] */
+} bmpc_model_desc;
+
+/* Host-side scenario builders (scenarios.hpp), producing a tree + model
+ * descriptor whose arrays the returned object owns. */
+#define BMPC_SCENARIO_INTERSECTION 0 /* build_intersection_case (scenarios.hpp:296) */
+#define BMPC_SCENARIO_LATENCY 1      /* build_latency_case (scenarios.hpp:398) */
+#define BMPC_SCENARIO_MULTISTAGE 2   /* multi-stage intersection (cfg2/cfg3) */
+typedef struct bmpc_scenario {
+  int family;
+  int horizon;
+  double total_time;
+  double shared_time[2]; /* intersection: [0]; latency: T_sh0, T_sh1 */
+  int v1, v2;            /* intersection vehicle option counts */
+  int n_branchings;      /* multistage: explicit uniform branchings */
+  int branch_step[8];
+  int branch_arity[8];
+  int perturb;           /* perturb the measured initial state ... */
+  unsigned long long perturb_seed; /* ... with std::mt19937_64(perturb_seed) */
+} bmpc_scenario;
+
+typedef struct bmpc_problem_data {
+  bmpc_tree* tree;
+  bmpc_model_desc model;
+} bmpc_problem_data;
+
+int bmpc_scenario_build(const bmpc_scenario* spec, bmpc_problem_data** out);
+void bmpc_problem_data_free(bmpc_problem_data* data);
+
+/* -------------------------------------------------------- options/report */
+/* SolverOptions (solver.hpp:28-58); the strategy enums are fixed to the
+ * north-star path (pmsilqr: scan backward, linear rollout, parallel LS). */
+typedef struct bmpc_options {
+  int max_inner_iterations, max_outer_iterations, alpha_levels;
+  double armijo_beta, merit_gamma, merit_mu0, merit_mu_init, defect_epsilon;
+  double tol_defect, tol_cost, tol_feedforward, tol_constraint;
+  double penalty_init, penalty_growth, penalty_max;
+  double reg_init, reg_min, reg_growth, reg_decay, reg_max;
+} bmpc_options;
+void bmpc_options_default(bmpc_options* opts);
+
+/* IterationRecord (solver.hpp:547-561). */
+typedef struct bmpc_record {
+  int outer, accepted;
+  double cost, cost_al, merit_before, merit_after, model_decrease, defect_l1, violation, alpha, mu,
+      max_feedforward, regularization;
+} bmpc_record;
+
+/* SolveReport (solver.hpp:572-582); `times` = PhaseTimes (setup,
+ * backward_p1 [= whole tree-scan backward pass], backward_p2 [= 0],
+ * forward, line_search, total) in seconds of device time. */
+typedef struct bmpc_report {
+  int status, error_code, error_node, inner_iterations, outer_iterations, n_records;
+  double final_cost, final_violation, final_defect_l1;
+  double times[6];
+  double final_penalty, final_mu, final_reg;
+  char message[160];
+} bmpc_report;
+
+/* ------------------------------------------------------------- context */
+typedef struct bmpc_ctx bmpc_ctx;
+int bmpc_ctx_create(int device, bmpc_ctx** out);
+void bmpc_ctx_destroy(bmpc_ctx* ctx);
+int bmpc_ctx_set_stream(bmpc_ctx* ctx, void* cuda_stream); /* cudaStream_t; NULL = ctx-owned stream */
+int bmpc_ctx_synchronize(bmpc_ctx* ctx);
+/* Number of kernels this ctx launched since creation (evidence counter). */
+long long bmpc_ctx_launch_count(const bmpc_ctx* ctx);
+
+/* ------------------------------------------------------ single solve */
+/* solve(problem, opts, initial_inputs) (solver.hpp:595). initial_inputs:
+ * [node][input_dim] or NULL (zeros). Outputs: x_out [node][state_dim],
+ * u_out [node][input_dim] (leaf rows 0), report, up to max_records records.
+ * Large trees run on the whole GPU (cooperative launch); small ones on one
+ * thread block. Host buffers; synchronous. */
+int bmpc_solve(bmpc_ctx* ctx, const bmpc_tree* tree, const bmpc_model_desc* model, const bmpc_options* opts,
+               const double* initial_inputs, double* x_out, double* u_out, bmpc_report* report,
+               bmpc_record* records, int max_records);
+
+/* ------------------------------------------------------ batched solves */
+/* A batch holds `count` independent instances sharing one tree shape and
+ * model family, device-resident (one thread block per instance). */
+typedef struct bmpc_batch bmpc_batch;
+int bmpc_batch_create(bmpc_ctx* ctx, const bmpc_tree* tree, int count, const bmpc_model_desc* model_template,
+                      int max_records, bmpc_batch** out);
+void bmpc_batch_destroy(bmpc_batch* batch);
+/* Host -> device copy of every instance's per-node data and initial state
+ * (models[count], same kind/dims/num_vehicles as the template). Async on the
+ * ctx stream. Returns the bytes copied in *h2d_bytes (may be NULL). */
+int bmpc_batch_set_models(bmpc_batch* batch, const bmpc_model_desc* models, size_t* h2d_bytes);
+/* Device-to-device replication of instance 0's data into all instances. */
+int bmpc_batch_replicate(bmpc_batch* batch);
+/* Launch the solve of every instance (async on the ctx stream). */
+int bmpc_batch_solve(bmpc_batch* batch, const bmpc_options* opts);
+/* Device -> host copy of results and synchronize. Any pointer may be NULL.
+ * x_out [count][node][nx], u_out [count][node][nu], reports [count]. */
+int bmpc_batch_results(bmpc_batch* batch, double* x_out, double* u_out, bmpc_report* reports,
+                       size_t* d2h_bytes);
+/* Device pointers of the result trajectories (for an NVLink gather). */
+int bmpc_batch_device_results(bmpc_batch* batch, double** d_x, double** d_u, size_t* bytes_x, size_t* bytes_u);
+/* Records of one instance (device -> host copy). */
+int bmpc_batch_records(bmpc_batch* batch, int instance, bmpc_record* records, int max_records, int* n_records);
+/* Kernel launches the batch solve issues (1) and the launch configuration. */
+int bmpc_batch_info(const bmpc_batch* batch, int* threads_per_block, int* blocks, int* regs_per_thread);
+
+/* ---------------------------------------------- kernel-level LQR tree */
+/* backward_pass + linear_rollout + expected_change_coefficients
+ * (solver.hpp:203-430) on explicit TreeStageModels (riccati.hpp:77-84):
+ * stage [node][A B c Q R M q r] (c ignored), defect [node][nx], leaf
+ * [node][P p]. Outputs K [node][nu*nx], k [node][nu], P [node][nx*nx],
+ * p [node][nx], dx [node][nx], du [node][nu]; scalars = {max_feedforward,
+ * a1, a2, error (0 ok, 1 IndefiniteHessian, 2 Factorization)}.
+ * grid != 0 runs on the whole GPU (cooperative), else one thread block. */
+int bmpc_lqr_tree(bmpc_ctx* ctx, const bmpc_tree* tree, int nx, int nu, const double* stage, const double* defect,
+                  const double* leaf, double reg, const double* dx0, int grid, double* K, double* k, double* P,
+                  double* p, double* dx, double* du, double* scalars);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BMPC_B200_H */

@@ -1,0 +1,501 @@
+"""bmpc_b200 — B200-native branch MPC (parallel tree iLQR + augmented Lagrangian).
+
+Python mirror of the reference's solve-path interface
+(/root/reference/proj/include/bmpc: build_tree tree.hpp:61, the scenario
+builders scenarios.hpp:178-402, SolverOptions / solve solver.hpp:28-58,
+595-780) over the C ABI in include/bmpc_b200.h. The compute runs in the
+in-tree sm_100a library _lib/libbmpc_b200.so; there is no CPU fallback — if the
+library is missing every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libbmpc_b200.so")
+
+CONVERGED, MAX_ITERATIONS, ERROR = 0, 1, 2
+STATUS_NAMES = {CONVERGED: "converged", MAX_ITERATIONS: "max-iter", ERROR: "error"}  # solver.hpp:538-545
+MODEL_UNICYCLE, MODEL_AFFINE_QUADRATIC = 1, 2
+SCENARIO_INTERSECTION, SCENARIO_LATENCY, SCENARIO_MULTISTAGE = 0, 1, 2
+
+
+class BmpcError(RuntimeError):
+    """A C-ABI call failed (carries the library's status code)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+# ----------------------------------------------------------------- C structs
+class _Tree(C.Structure):
+    _fields_ = [("node_count", C.c_int), ("horizon", C.c_int), ("last_branch_step", C.c_int),
+                ("leaf_count", C.c_int), ("parent", C.POINTER(C.c_int)), ("time_step", C.POINTER(C.c_int)),
+                ("weight", C.POINTER(C.c_double)), ("first_child", C.POINTER(C.c_int)),
+                ("child_count", C.POINTER(C.c_int)), ("step_begin", C.POINTER(C.c_int)),
+                ("leaves", C.POINTER(C.c_int))]
+
+
+class _Model(C.Structure):
+    _fields_ = [("kind", C.c_int), ("state_dim", C.c_int), ("input_dim", C.c_int),
+                ("initial_state", C.c_void_p), ("dt", C.c_double), ("state_weights", C.c_double * 16),
+                ("input_weights", C.c_double * 4), ("terminal_weights", C.c_double * 16),
+                ("accel_limit", C.c_double), ("yaw_rate_limit", C.c_double), ("safety_radius", C.c_double),
+                ("num_vehicles", C.c_int), ("reference", C.c_void_p), ("vehicle_position", C.c_void_p),
+                ("lq_stage", C.c_void_p), ("lq_leaf", C.c_void_p)]
+
+
+class _Scenario(C.Structure):
+    _fields_ = [("family", C.c_int), ("horizon", C.c_int), ("total_time", C.c_double),
+                ("shared_time", C.c_double * 2), ("v1", C.c_int), ("v2", C.c_int), ("n_branchings", C.c_int),
+                ("branch_step", C.c_int * 8), ("branch_arity", C.c_int * 8), ("perturb", C.c_int),
+                ("perturb_seed", C.c_ulonglong)]
+
+
+class _ProblemData(C.Structure):
+    _fields_ = [("tree", C.POINTER(_Tree)), ("model", _Model)]
+
+
+_OPT_INT = ("max_inner_iterations", "max_outer_iterations", "alpha_levels")
+_OPT_DBL = ("armijo_beta", "merit_gamma", "merit_mu0", "merit_mu_init", "defect_epsilon", "tol_defect",
+            "tol_cost", "tol_feedforward", "tol_constraint", "penalty_init", "penalty_growth", "penalty_max",
+            "reg_init", "reg_min", "reg_growth", "reg_decay", "reg_max")
+
+
+class _Options(C.Structure):
+    _fields_ = [(n, C.c_int) for n in _OPT_INT] + [(n, C.c_double) for n in _OPT_DBL]
+
+
+RECORD_FIELDS = ("outer", "accepted", "cost", "cost_al", "merit_before", "merit_after", "model_decrease",
+                 "defect_l1", "violation", "alpha", "mu", "max_feedforward", "regularization")
+
+
+class _Record(C.Structure):
+    _fields_ = [("outer", C.c_int), ("accepted", C.c_int)] + [(n, C.c_double) for n in RECORD_FIELDS[2:]]
+
+
+class _Report(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("status", "error_code", "error_node", "inner_iterations",
+                                       "outer_iterations", "n_records")] + \
+               [(n, C.c_double) for n in ("final_cost", "final_violation", "final_defect_l1")] + \
+               [("times", C.c_double * 6)] + \
+               [(n, C.c_double) for n in ("final_penalty", "final_mu", "final_reg")] + \
+               [("message", C.c_char * 160)]
+
+
+_lib_handle = None
+
+
+def lib():
+    """The loaded sm_100a library (raises if it was not built)."""
+    global _lib_handle
+    if _lib_handle is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                              f"g.build()'` (make -C paper_2506_13624_b200)")
+        L = C.CDLL(LIB_PATH)
+        L.bmpc_last_error.restype = C.c_char_p
+        L.bmpc_version.restype = C.c_char_p
+        L.bmpc_ctx_launch_count.restype = C.c_longlong
+        _lib_handle = L
+    return _lib_handle
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise BmpcError(rc, lib().bmpc_last_error().decode())
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# ---------------------------------------------------------------- topology
+class TreeTopology:
+    """TreeTopology (tree.hpp:28-44) owned by the library; numpy copies of
+    the index arrays are exposed with the reference's field names."""
+
+    def __init__(self, handle: C.POINTER(_Tree), owner=None):
+        self._h = handle
+        self._owner = owner  # keeps a parent object (problem data) alive
+        t = handle.contents
+        n = t.node_count
+        self.node_count = n
+        self.horizon = t.horizon
+        self.last_branch_step = t.last_branch_step
+        self.parent = np.ctypeslib.as_array(t.parent, (n,)).copy()
+        self.time_step = np.ctypeslib.as_array(t.time_step, (n,)).copy()
+        self.weight = np.ctypeslib.as_array(t.weight, (n,)).copy()
+        self.first_child = np.ctypeslib.as_array(t.first_child, (n,)).copy()
+        self.child_count = np.ctypeslib.as_array(t.child_count, (n,)).copy()
+        self.step_begin = np.ctypeslib.as_array(t.step_begin, (t.horizon + 2,)).copy()
+        self.leaves = np.ctypeslib.as_array(t.leaves, (t.leaf_count,)).copy()
+
+    @property
+    def children(self):
+        return [list(range(f, f + c)) if c else [] for f, c in zip(self.first_child, self.child_count)]
+
+    def is_leaf(self, i: int) -> bool:
+        return self.child_count[i] == 0
+
+    def leaf_count(self) -> int:
+        return len(self.leaves)
+
+    def __del__(self):
+        if self._owner is None and getattr(self, "_h", None) is not None and _lib_handle is not None:
+            _lib_handle.bmpc_tree_free(self._h)
+            self._h = None
+
+
+def build_tree(horizon: int, branchings: Sequence[tuple] = ()) -> TreeTopology:
+    """build_tree(horizon, branchings) (tree.hpp:61). Each branching is
+    (step, arity, weights) or (step, arity) for uniform weights. Raises
+    ValueError on invalid specs, as the reference throws invalid_argument."""
+    nb = len(branchings)
+    max_a = max([b[1] for b in branchings] + [1])
+    steps = np.array([b[0] for b in branchings], np.int32)
+    ar = np.array([b[1] for b in branchings], np.int32)
+    w = np.zeros((max(nb, 1), max_a))
+    for i, b in enumerate(branchings):
+        ws = b[2] if len(b) > 2 else [1.0 / b[1]] * b[1]
+        if len(ws) != b[1]:
+            raise ValueError("build_tree: branching needs arity >= 2 and one weight per child")
+        w[i, :b[1]] = ws
+    out = C.POINTER(_Tree)()
+    rc = lib().bmpc_tree_build(int(horizon), nb, _ptr(steps), _ptr(ar), _ptr(w), int(max_a), C.byref(out))
+    if rc == -1:
+        raise ValueError(lib().bmpc_last_error().decode())
+    _check(rc)
+    return TreeTopology(out)
+
+
+# ----------------------------------------------------------------- problems
+@dataclasses.dataclass
+class ScenarioSpec:
+    """Subset of ScenarioSpec (scenarios.hpp:25-47) the builders consume."""
+    family: int
+    horizon: int = 63
+    total_time: float = 10.0
+    shared_times: tuple = (0.1,)
+    branchings: tuple = ()  # multistage: ((step, arity), ...)
+
+    def dt(self) -> float:
+        return self.total_time / self.horizon
+
+
+def intersection_spec(horizon: int = 63, total_time: float = 10.0, shared_time: float = 0.1) -> ScenarioSpec:
+    return ScenarioSpec(SCENARIO_INTERSECTION, horizon, total_time, (shared_time,))
+
+
+def latency_spec(shared_time_1: float, horizon: int = 255, total_time: float = 5.0,
+                 shared_time_0: float = 0.05) -> ScenarioSpec:
+    return ScenarioSpec(SCENARIO_LATENCY, horizon, total_time, (shared_time_0, shared_time_1))
+
+
+def multistage_spec(horizon: int, branchings: Sequence[tuple], total_time: float = 10.0) -> ScenarioSpec:
+    """cfg2/cfg3 trees: one uniform branching (step, arity) per stage; at stage
+    j vehicle j mod 2 reveals its speed target."""
+    return ScenarioSpec(SCENARIO_MULTISTAGE, horizon, total_time, (0.1,), tuple(tuple(b) for b in branchings))
+
+
+class BmpcProblem:
+    """BmpcProblem (problem.hpp:44-63) as a tree + device model descriptor."""
+
+    def __init__(self, tree: TreeTopology, model: _Model, keep=(), data_handle=None):
+        self.tree = tree
+        self.model = model
+        self._keep = keep
+        self._data = data_handle
+        self.state_dim = model.state_dim
+        self.input_dim = model.input_dim
+
+    @property
+    def initial_state(self) -> np.ndarray:
+        return np.ctypeslib.as_array(C.cast(self.model.initial_state, C.POINTER(C.c_double)),
+                                     (self.state_dim,)).copy()
+
+    def arrays(self) -> dict:
+        """Per-node scenario data (reference / vehicle predictions)."""
+        n = self.tree.node_count
+        out = {"initial_state": self.initial_state}
+        if self.model.kind == MODEL_UNICYCLE:
+            out["reference"] = np.ctypeslib.as_array(C.cast(self.model.reference, C.POINTER(C.c_double)),
+                                                     (n, 4)).copy()
+            nv = self.model.num_vehicles
+            if nv:
+                out["vehicles"] = np.ctypeslib.as_array(
+                    C.cast(self.model.vehicle_position, C.POINTER(C.c_double)), (n, nv, 2)).copy()
+            out["dt"] = self.model.dt
+        return out
+
+    def __del__(self):
+        if getattr(self, "_data", None) is not None and _lib_handle is not None:
+            _lib_handle.bmpc_problem_data_free(self._data)
+            self._data = None
+
+
+def _build_scenario(spec: ScenarioSpec, v1=2, v2=2, perturb_seed=None) -> BmpcProblem:
+    s = _Scenario()
+    s.family = spec.family
+    s.horizon = spec.horizon
+    s.total_time = spec.total_time
+    st = list(spec.shared_times) + [0.0, 0.0]
+    s.shared_time[0], s.shared_time[1] = st[0], st[1]
+    s.v1, s.v2 = v1, v2
+    s.n_branchings = len(spec.branchings)
+    for i, b in enumerate(spec.branchings):
+        s.branch_step[i], s.branch_arity[i] = b[0], b[1]
+    s.perturb = 0 if perturb_seed is None else 1
+    s.perturb_seed = 0 if perturb_seed is None else int(perturb_seed)
+    out = C.POINTER(_ProblemData)()
+    rc = lib().bmpc_scenario_build(C.byref(s), C.byref(out))
+    if rc == -1:
+        raise ValueError(lib().bmpc_last_error().decode())
+    _check(rc)
+    d = out.contents
+    tree = TreeTopology(d.tree, owner=out)
+    return BmpcProblem(tree, d.model, data_handle=out)
+
+
+def build_intersection_case(spec: ScenarioSpec, v1_count: int, v2_count: int, perturb_seed=None) -> BmpcProblem:
+    """build_intersection_case (scenarios.hpp:296-372)."""
+    return _build_scenario(spec, v1_count, v2_count, perturb_seed)
+
+
+def build_latency_case(spec: ScenarioSpec, perturb_seed=None) -> BmpcProblem:
+    """build_latency_case (scenarios.hpp:398-479)."""
+    return _build_scenario(spec, perturb_seed=perturb_seed)
+
+
+def build_multistage_case(spec: ScenarioSpec, perturb_seed=None) -> BmpcProblem:
+    return _build_scenario(spec, perturb_seed=perturb_seed)
+
+
+def lq_problem(tree: TreeTopology, nx: int, nu: int, x0: np.ndarray, stage: np.ndarray,
+               leaf: np.ndarray) -> BmpcProblem:
+    """Affine-quadratic problem (the data random_lq_problem captures,
+    oracles.hpp:316-365): stage [node][A B c Q R M q r], leaf [node][P p],
+    all blocks column-major."""
+    x0 = np.ascontiguousarray(x0, np.float64)
+    stage = np.ascontiguousarray(stage, np.float64)
+    leaf = np.ascontiguousarray(leaf, np.float64)
+    m = _Model()
+    m.kind = MODEL_AFFINE_QUADRATIC
+    m.state_dim, m.input_dim = nx, nu
+    m.initial_state = x0.ctypes.data
+    m.lq_stage = stage.ctypes.data
+    m.lq_leaf = leaf.ctypes.data
+    return BmpcProblem(tree, m, keep=(x0, stage, leaf))
+
+
+# ------------------------------------------------------------------ options
+@dataclasses.dataclass
+class SolverOptions:
+    """SolverOptions (solver.hpp:28-58) — pmsilqr defaults."""
+    max_inner_iterations: int = 100
+    max_outer_iterations: int = 10
+    alpha_levels: int = 11
+    armijo_beta: float = 1e-4
+    merit_gamma: float = 0.5
+    merit_mu0: float = 1.0
+    merit_mu_init: float = 1.0
+    defect_epsilon: float = 1e-8
+    tol_defect: float = 1e-8
+    tol_cost: float = 1e-8
+    tol_feedforward: float = 1e-6
+    tol_constraint: float = 1e-4
+    penalty_init: float = 10.0
+    penalty_growth: float = 10.0
+    penalty_max: float = 1e8
+    reg_init: float = 0.0
+    reg_min: float = 1e-6
+    reg_growth: float = 10.0
+    reg_decay: float = 10.0
+    reg_max: float = 1e10
+
+    def _c(self) -> _Options:
+        o = _Options()
+        for f in dataclasses.fields(self):
+            setattr(o, f.name, getattr(self, f.name))
+        return o
+
+
+@dataclasses.dataclass
+class SolveReport:
+    """SolveReport (solver.hpp:572-582); `iterations` holds the per-iteration
+    records as arrays keyed like IterationRecord."""
+    status: int
+    message: str
+    inner_iterations: int
+    outer_iterations: int
+    final_cost: float
+    final_violation: float
+    final_defect_l1: float
+    times: dict
+    iterations: dict
+    n_records: int
+
+    @property
+    def status_name(self) -> str:
+        return STATUS_NAMES[self.status]
+
+
+@dataclasses.dataclass
+class TrajectoryTree:
+    state: np.ndarray  # [node][nx]
+    input: np.ndarray  # [node][nu], leaf rows zero
+
+
+@dataclasses.dataclass
+class SolveResult:
+    trajectory: TrajectoryTree
+    report: SolveReport
+
+
+def _report(r: _Report, recs=None, nrec=0) -> SolveReport:
+    its = {}
+    if recs is not None:
+        k = min(nrec, len(recs))
+        its = {f: np.array([getattr(recs[i], f) for i in range(k)]) for f in RECORD_FIELDS}
+    names = ("setup_s", "backward_p1_s", "backward_p2_s", "forward_s", "line_search_s", "total_s")
+    return SolveReport(r.status, r.message.decode(), r.inner_iterations, r.outer_iterations, r.final_cost,
+                       r.final_violation, r.final_defect_l1, dict(zip(names, list(r.times))), its, r.n_records)
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """One device + one CUDA stream (bmpc_ctx)."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        h = C.c_void_p()
+        _check(lib().bmpc_ctx_create(int(device), C.byref(h)))
+        self._h = h
+        self.device = device
+        if stream is not None:
+            _check(lib().bmpc_ctx_set_stream(self._h, C.c_void_p(stream)))
+
+    @property
+    def launches(self) -> int:
+        return int(lib().bmpc_ctx_launch_count(self._h))
+
+    def synchronize(self):
+        _check(lib().bmpc_ctx_synchronize(self._h))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib_handle is not None:
+            _lib_handle.bmpc_ctx_destroy(self._h)
+            self._h = None
+
+
+_default_ctx = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default_ctx:
+        _default_ctx[device] = Context(device)
+    return _default_ctx[device]
+
+
+def solve(problem: BmpcProblem, options: Optional[SolverOptions] = None,
+          initial_inputs: Optional[np.ndarray] = None, ctx: Optional[Context] = None,
+          max_records: int = 1000) -> SolveResult:
+    """solve(problem, opts, initial_inputs) (solver.hpp:595) on the GPU."""
+    ctx = ctx or default_context()
+    n, nx, nu = problem.tree.node_count, problem.state_dim, problem.input_dim
+    x = np.zeros((n, nx))
+    u = np.zeros((n, nu))
+    rep = _Report()
+    recs = (_Record * max(max_records, 1))()
+    ii = None if initial_inputs is None else np.ascontiguousarray(initial_inputs, np.float64).reshape(n, nu)
+    opts = (options or SolverOptions())._c()
+    rc = lib().bmpc_solve(ctx._h, problem.tree._h, C.byref(problem.model), C.byref(opts), _ptr(ii), _ptr(x),
+                          _ptr(u), C.byref(rep), recs, int(max_records))
+    if rc == -4:
+        raise RuntimeError(lib().bmpc_last_error().decode())
+    _check(rc)
+    return SolveResult(TrajectoryTree(x, u), _report(rep, recs, rep.n_records))
+
+
+class Batch:
+    """Device-resident batch of independent instances with one tree shape
+    (bmpc_batch_*): one thread block per instance, one launch per solve."""
+
+    def __init__(self, ctx: Context, problems: Sequence[BmpcProblem], max_records: int = 0):
+        self.ctx = ctx
+        self.count = len(problems)
+        self.problems = list(problems)
+        p0 = problems[0]
+        self.n, self.nx, self.nu = p0.tree.node_count, p0.state_dim, p0.input_dim
+        h = C.c_void_p()
+        _check(lib().bmpc_batch_create(ctx._h, p0.tree._h, self.count, C.byref(p0.model), int(max_records),
+                                       C.byref(h)))
+        self._h = h
+        self._models = (_Model * self.count)(*[p.model for p in problems])
+
+    def set_models(self) -> int:
+        b = C.c_size_t()
+        _check(lib().bmpc_batch_set_models(self._h, self._models, C.byref(b)))
+        return b.value
+
+    def replicate(self):
+        _check(lib().bmpc_batch_replicate(self._h))
+
+    def solve(self, options: Optional[SolverOptions] = None):
+        opts = (options or SolverOptions())._c()
+        _check(lib().bmpc_batch_solve(self._h, C.byref(opts)))
+
+    def results(self, x: Optional[np.ndarray] = None, u: Optional[np.ndarray] = None, want_reports=True):
+        reps = (_Report * self.count)() if want_reports else None
+        b = C.c_size_t()
+        _check(lib().bmpc_batch_results(self._h, _ptr(x), _ptr(u), reps, C.byref(b)))
+        return ([_report(r) for r in reps] if want_reports else None), b.value
+
+    def records(self, instance: int, max_records: int = 1000) -> dict:
+        recs = (_Record * max_records)()
+        n = C.c_int()
+        _check(lib().bmpc_batch_records(self._h, int(instance), recs, int(max_records), C.byref(n)))
+        return {f: np.array([getattr(recs[i], f) for i in range(min(n.value, max_records))]) for f in RECORD_FIELDS}
+
+    def info(self) -> dict:
+        t, b, r = C.c_int(), C.c_int(), C.c_int()
+        _check(lib().bmpc_batch_info(self._h, C.byref(t), C.byref(b), C.byref(r)))
+        return {"threads_per_block": t.value, "blocks": b.value, "regs_per_thread": r.value}
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib_handle is not None:
+            _lib_handle.bmpc_batch_destroy(self._h)
+            self._h = None
+
+
+def lqr_tree(tree: TreeTopology, nx: int, nu: int, stage: np.ndarray, defect: np.ndarray, leaf: np.ndarray,
+             reg: float = 0.0, dx0: Optional[np.ndarray] = None, grid: bool = False,
+             ctx: Optional[Context] = None) -> dict:
+    """Kernel-level backward_pass + linear_rollout + EC on TreeStageModels
+    (solver.hpp:203-430), the tree-segmented scan on the GPU."""
+    ctx = ctx or default_context()
+    n = tree.node_count
+    stage = np.ascontiguousarray(stage, np.float64)
+    defect = np.ascontiguousarray(defect, np.float64)
+    leaf = np.ascontiguousarray(leaf, np.float64)
+    dx0 = np.zeros(nx) if dx0 is None else np.ascontiguousarray(dx0, np.float64)
+    K = np.zeros((n, nu * nx))
+    k = np.zeros((n, nu))
+    P = np.zeros((n, nx * nx))
+    p = np.zeros((n, nx))
+    dx = np.zeros((n, nx))
+    du = np.zeros((n, nu))
+    sc = np.zeros(4)
+    _check(lib().bmpc_lqr_tree(ctx._h, tree._h, nx, nu, _ptr(stage), _ptr(defect), _ptr(leaf), C.c_double(reg),
+                               _ptr(dx0), int(grid), _ptr(K), _ptr(k), _ptr(P), _ptr(p), _ptr(dx), _ptr(du),
+                               _ptr(sc)))
+    return dict(K=K, k=k, P=P, p=p, dx=dx, du=du, max_feedforward=sc[0], a1=sc[1], a2=sc[2], error=int(sc[3]))
+
+
+def version() -> str:
+    return lib().bmpc_version().decode()

@@ -1,0 +1,106 @@
+// Runtime (nx, nu) dispatch onto the explicit instantiations in inst_*.cu.
+#include "kernels.h"
+#include "solver.cuh"
+
+namespace bmpc_b200 {
+
+// Full solve: unicycle (4,2) and the LQ dims the reference tests use.
+#define BMPC_SOLVE_DIMS(X) X(4, 2) X(3, 2) X(2, 1)
+// Kernel-level LQR tree: the reference verification grid nx {2,4,8} x
+// nu {1,2,4} (verification.hpp:47-48) plus (3,2).
+#define BMPC_LQR_DIMS(X) \
+  X(2, 1) X(2, 2) X(2, 4) X(3, 2) X(4, 1) X(4, 2) X(4, 4) X(8, 1) X(8, 2) X(8, 4)
+
+extern template struct SolveLaunch<4, 2>;
+extern template struct SolveLaunch<3, 2>;
+extern template struct SolveLaunch<2, 1>;
+#define X(a, b) extern template struct LqrLaunch<a, b>;
+BMPC_LQR_DIMS(X)
+#undef X
+
+static_assert(kRedSlotsHost == kRedSlots, "reduction slot count mismatch");
+
+bool solve_dims_supported(int nx, int nu) {
+#define X(a, b) \
+  if (nx == a && nu == b) return true;
+  BMPC_SOLVE_DIMS(X)
+#undef X
+  return false;
+}
+
+bool lqr_dims_supported(int nx, int nu) {
+#define X(a, b) \
+  if (nx == a && nu == b) return true;
+  BMPC_LQR_DIMS(X)
+#undef X
+  return false;
+}
+
+Strides strides_for(int nx, int nu) {
+#define X(a, b) \
+  if (nx == a && nu == b) return LqrLaunch<a, b>::strides();
+  BMPC_LQR_DIMS(X)
+#undef X
+  return Strides{};
+}
+
+cudaError_t launch_solve_cta(int nx, int nu, const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
+                             const DevOptions& opts, int count, int threads, cudaStream_t stream) {
+#define X(a, b) \
+  if (nx == a && nu == b) return SolveLaunch<a, b>::solve_cta(d_topo, d_mp, d_work, opts, count, threads, stream);
+  BMPC_SOLVE_DIMS(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_solve_grid(int nx, int nu, const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
+                              const DevOptions& opts, double* red, int blocks, int threads, cudaStream_t stream) {
+#define X(a, b)           \
+  if (nx == a && nu == b) \
+    return SolveLaunch<a, b>::solve_grid(d_topo, d_mp, d_work, opts, red, blocks, threads, stream);
+  BMPC_SOLVE_DIMS(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+int solve_grid_blocks(int nx, int nu, int threads) {
+#define X(a, b) \
+  if (nx == a && nu == b) return SolveLaunch<a, b>::grid_blocks(threads);
+  BMPC_SOLVE_DIMS(X)
+#undef X
+  return 0;
+}
+
+int solve_cta_regs(int nx, int nu) {
+#define X(a, b) \
+  if (nx == a && nu == b) return SolveLaunch<a, b>::cta_regs();
+  BMPC_SOLVE_DIMS(X)
+#undef X
+  return 0;
+}
+
+cudaError_t launch_lqr_tree(int nx, int nu, bool grid, const Topo* d_topo, const Work* d_work, double reg,
+                            double* d_scalars, double* red, int blocks, int threads, cudaStream_t stream) {
+#define X(a, b)           \
+  if (nx == a && nu == b) \
+    return LqrLaunch<a, b>::lqr_tree(grid, d_topo, d_work, reg, d_scalars, red, blocks, threads, stream);
+  BMPC_LQR_DIMS(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+int lqr_grid_blocks(int nx, int nu, int threads) {
+#define X(a, b) \
+  if (nx == a && nu == b) return LqrLaunch<a, b>::grid_blocks(threads);
+  BMPC_LQR_DIMS(X)
+#undef X
+  return 0;
+}
+
+size_t sizeof_topo() { return sizeof(Topo); }
+size_t sizeof_model_params() { return sizeof(ModelParams); }
+size_t sizeof_work() { return sizeof(Work); }
+size_t sizeof_dev_result() { return sizeof(DevResult); }
+size_t sizeof_dev_record() { return sizeof(DevRecord); }
+
+}  // namespace bmpc_b200

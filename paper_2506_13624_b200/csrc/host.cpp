@@ -1,0 +1,1216 @@
+// Host runtime of bmpc_b200: the C ABI (include/bmpc_b200.h), tree building,
+// scenario builders, segment planning, device buffers and launches.
+//
+// Compiled with -ffp-contract=off so the host-side builders reproduce the
+// reference builders' floating-point results bit for bit (tree weights,
+// references, vehicle predictions).
+#include "bmpc_b200.h"
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "types.h"
+
+using namespace bmpc_b200;
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int code, const std::string& msg) {
+  g_error = msg;
+  return code;
+}
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------ tree
+// build_tree (tree.hpp:61-128), same validation and same arithmetic.
+std::unique_ptr<bmpc_tree, void (*)(bmpc_tree*)> make_tree(int horizon, int nb, const int* steps,
+                                                           const int* arities, const double* weights,
+                                                           int max_arity) {
+  if (horizon < 1) throw std::invalid_argument("build_tree: horizon must be >= 1");
+  for (int b = 0; b < nb; ++b) {
+    if (steps[b] < 0 || steps[b] >= horizon)
+      throw std::invalid_argument("build_tree: branching step " + std::to_string(steps[b]) +
+                                  " must lie in [0, horizon)");
+    if (b > 0 && steps[b] <= steps[b - 1])
+      throw std::invalid_argument("build_tree: branching steps must be strictly increasing");
+    if (arities[b] < 2 || arities[b] > max_arity)
+      throw std::invalid_argument("build_tree: branching needs arity >= 2 and one weight per child");
+    double sum = 0.0;
+    for (int a = 0; a < arities[b]; ++a) {
+      const double w = weights[b * max_arity + a];
+      if (!(w > 0.0)) throw std::invalid_argument("build_tree: branch weights must be positive");
+      sum += w;
+    }
+    if (std::abs(sum - 1.0) > 1e-9)
+      throw std::invalid_argument("build_tree: branch weights must sum to 1, got " + std::to_string(sum));
+  }
+  std::vector<int> parent{-1}, time_step{0};
+  std::vector<double> weight{1.0};
+  std::vector<int> step_begin(static_cast<size_t>(horizon) + 2, 0);
+  std::vector<int> level{0};
+  int next = 0;
+  for (int k = 0; k < horizon; ++k) {
+    step_begin[static_cast<size_t>(k) + 1] = static_cast<int>(parent.size());
+    int br = -1;
+    if (next < nb && steps[next] == k) br = next++;
+    std::vector<int> next_level;
+    for (int node : level) {
+      const int arity = br >= 0 ? arities[br] : 1;
+      for (int a = 0; a < arity; ++a) {
+        const int child = static_cast<int>(parent.size());
+        parent.push_back(node);
+        time_step.push_back(k + 1);
+        weight.push_back(weight[static_cast<size_t>(node)] * (br >= 0 ? weights[br * max_arity + a] : 1.0));
+        next_level.push_back(child);
+      }
+    }
+    level = std::move(next_level);
+  }
+  const int n = static_cast<int>(parent.size());
+  step_begin[static_cast<size_t>(horizon) + 1] = n;
+
+  auto* t = new bmpc_tree{};
+  t->node_count = n;
+  t->horizon = horizon;
+  t->last_branch_step = nb == 0 ? -1 : steps[nb - 1];
+  t->parent = new int[n];
+  t->time_step = new int[n];
+  t->weight = new double[n];
+  t->first_child = new int[n];
+  t->child_count = new int[n];
+  t->step_begin = new int[horizon + 2];
+  std::copy(parent.begin(), parent.end(), t->parent);
+  std::copy(time_step.begin(), time_step.end(), t->time_step);
+  std::copy(weight.begin(), weight.end(), t->weight);
+  std::copy(step_begin.begin(), step_begin.end(), t->step_begin);
+  for (int i = 0; i < n; ++i) {
+    t->first_child[i] = -1;
+    t->child_count[i] = 0;
+  }
+  for (int i = 1; i < n; ++i) {
+    const int p = parent[static_cast<size_t>(i)];
+    if (t->first_child[p] < 0) t->first_child[p] = i;
+    ++t->child_count[p];
+  }
+  std::vector<int> leaves;
+  for (int i = 0; i < n; ++i)
+    if (t->child_count[i] == 0) leaves.push_back(i);
+  t->leaf_count = static_cast<int>(leaves.size());
+  t->leaves = new int[leaves.size()];
+  std::copy(leaves.begin(), leaves.end(), t->leaves);
+  return {t, bmpc_tree_free};
+}
+
+// --------------------------------------------------------------- scenarios
+// ScenarioSpec defaults (scenarios.hpp:25-47).
+struct Vehicle {
+  double px, py, heading, speed;
+  std::vector<double> targets;
+};
+struct Spec {
+  double total_time{10.0};
+  std::vector<double> shared_times{0.1};
+  int horizon{63};
+  double ego[4]{0.0, -20.0, M_PI / 2.0, 5.0};
+  std::vector<Vehicle> vehicles;
+  double state_w[4]{1.0, 1.0, 0.1, 0.1}, input_w[2]{0.5, 0.5}, terminal_w[4]{1.0, 1.0, 0.1, 0.1};
+  double accel_limit{3.0}, yaw_rate_limit{0.5}, safety_radius{3.0}, prediction_tau{1.5};
+  double reference_turn_rate{0.4}, backup_deceleration{3.0}, continue_deceleration{2.5};
+  double dt() const { return total_time / horizon; }
+};
+
+Spec intersection_spec(int horizon, double total_time, double shared_time) {  // scenarios.hpp:178-197
+  Spec s;
+  s.total_time = total_time;
+  s.shared_times = {shared_time};
+  s.horizon = horizon;
+  s.vehicles = {{-3.5, 30.0, -M_PI / 2.0, 8.0, {8.0, 2.0, 5.0, 3.5}}, {0.0, -10.0, M_PI / 2.0, 5.0, {5.0, 1.0, 3.0, 2.0}}};
+  return s;
+}
+
+Spec latency_spec(double shared_time_1, int horizon, double total_time, double shared_time_0) {  // :300-314
+  Spec s;
+  s.total_time = total_time;
+  s.shared_times = {shared_time_0, shared_time_1};
+  s.horizon = horizon;
+  s.ego[0] = 0.0;
+  s.ego[1] = 0.0;
+  s.ego[2] = 0.0;
+  s.ego[3] = 10.0;
+  s.vehicles = {{30.0, 0.0, 0.0, 8.0, {8.0, 0.0}}};
+  return s;
+}
+
+// unicycle::step (unicycle.hpp:36-42) in the reference's operation order.
+void host_unicycle_step(const double* x, const double* u, double dt, double* out) {
+  auto deriv = [&](const double* y, double* d) {
+    d[0] = y[3] * std::cos(y[2]);
+    d[1] = y[3] * std::sin(y[2]);
+    d[2] = u[1];
+    d[3] = u[0];
+  };
+  double k1[4], k2[4], k3[4], k4[4], t[4];
+  deriv(x, k1);
+  for (int i = 0; i < 4; ++i) t[i] = x[i] + 0.5 * dt * k1[i];
+  deriv(t, k2);
+  for (int i = 0; i < 4; ++i) t[i] = x[i] + 0.5 * dt * k2[i];
+  deriv(t, k3);
+  for (int i = 0; i < 4; ++i) t[i] = x[i] + dt * k3[i];
+  deriv(t, k4);
+  for (int i = 0; i < 4; ++i) out[i] = x[i] + dt / 6.0 * (k1[i] + 2.0 * k2[i] + 2.0 * k3[i] + k4[i]);
+}
+
+// left_turn_reference (scenarios.hpp:201-214).
+std::vector<std::array<double, 4>> left_turn_reference(const Spec& spec) {
+  std::vector<std::array<double, 4>> ref(static_cast<size_t>(spec.horizon) + 1);
+  double x[4] = {spec.ego[0], spec.ego[1], spec.ego[2], spec.ego[3]};
+  const double psi_end = spec.ego[2] + M_PI / 2.0;
+  const double turn_radius = spec.ego[3] / spec.reference_turn_rate;
+  const double turn_start_y = -turn_radius;
+  for (int k = 0; k <= spec.horizon; ++k) {
+    ref[static_cast<size_t>(k)] = {x[0], x[1], x[2], x[3]};
+    double omega = 0.0;
+    if (x[1] >= turn_start_y && x[2] < psi_end) omega = spec.reference_turn_rate;
+    const double u[2] = {0.0, omega};
+    double xn[4];
+    host_unicycle_step(x, u, spec.dt(), xn);
+    std::copy(xn, xn + 4, x);
+  }
+  return ref;
+}
+
+// branch_choices (scenarios.hpp:61-77).
+std::vector<std::vector<int>> branch_choices(const bmpc_tree& t, const std::vector<int>& branch_steps) {
+  const size_t nb = branch_steps.size();
+  std::vector<std::vector<int>> ch(static_cast<size_t>(t.node_count), std::vector<int>(nb, -1));
+  for (int i = 0; i < t.node_count; ++i) {
+    for (int c = 0; c < t.child_count[i]; ++c) {
+      const int kid = t.first_child[i] + c;
+      ch[static_cast<size_t>(kid)] = ch[static_cast<size_t>(i)];
+      for (size_t b = 0; b < nb; ++b)
+        if (branch_steps[b] == t.time_step[i]) ch[static_cast<size_t>(kid)][b] = c;
+    }
+  }
+  return ch;
+}
+
+// predict_vehicles (scenarios.hpp:87-113): positions only.
+template <class TargetFn>
+std::vector<double> predict_vehicles(const bmpc_tree& t, const Spec& spec, const TargetFn& target_of) {
+  const size_t nv = spec.vehicles.size();
+  std::vector<double> pos(static_cast<size_t>(t.node_count) * nv * 2), speed(static_cast<size_t>(t.node_count) * nv);
+  for (size_t v = 0; v < nv; ++v) {
+    pos[v * 2 + 0] = spec.vehicles[v].px;
+    pos[v * 2 + 1] = spec.vehicles[v].py;
+    speed[v] = spec.vehicles[v].speed;
+  }
+  const double dt = spec.dt();
+  for (int i = 0; i < t.node_count; ++i) {
+    for (int c = 0; c < t.child_count[i]; ++c) {
+      const int ch = t.first_child[i] + c;
+      for (size_t v = 0; v < nv; ++v) {
+        const Vehicle& veh = spec.vehicles[v];
+        const size_t cur = static_cast<size_t>(i) * nv + v, nxt = static_cast<size_t>(ch) * nv + v;
+        const double target = target_of(v, ch);
+        const double step = dt * speed[cur];
+        pos[nxt * 2 + 0] = pos[cur * 2 + 0] + step * std::cos(veh.heading);
+        pos[nxt * 2 + 1] = pos[cur * 2 + 1] + step * std::sin(veh.heading);
+        speed[nxt] = speed[cur] + dt * (target - speed[cur]) / spec.prediction_tau;
+      }
+    }
+  }
+  return pos;
+}
+
+struct ProblemData {
+  bmpc_problem_data pub{};
+  std::unique_ptr<bmpc_tree, void (*)(bmpc_tree*)> tree{nullptr, bmpc_tree_free};
+  std::vector<double> x0, reference, vehicles;
+};
+
+void fill_unicycle(ProblemData& pd, const Spec& spec) {
+  bmpc_model_desc& m = pd.pub.model;
+  m.kind = BMPC_MODEL_UNICYCLE;
+  m.state_dim = 4;
+  m.input_dim = 2;
+  m.dt = spec.dt();
+  std::memset(m.state_weights, 0, sizeof m.state_weights);
+  std::memset(m.input_weights, 0, sizeof m.input_weights);
+  std::memset(m.terminal_weights, 0, sizeof m.terminal_weights);
+  for (int i = 0; i < 4; ++i) {
+    m.state_weights[i * 5] = spec.state_w[i];
+    m.terminal_weights[i * 5] = spec.terminal_w[i];
+  }
+  for (int i = 0; i < 2; ++i) m.input_weights[i * 3] = spec.input_w[i];
+  m.accel_limit = spec.accel_limit;
+  m.yaw_rate_limit = spec.yaw_rate_limit;
+  m.safety_radius = spec.safety_radius;
+  m.num_vehicles = static_cast<int>(spec.vehicles.size());
+  pd.x0.assign(spec.ego, spec.ego + 4);
+}
+
+// Measured-state perturbation (cfg4): U(-0.5,0.5) px, py; U(-0.05,0.05) psi;
+// U(-0.5,0.5) v; std::mt19937_64(seed), drawn in that order.
+void perturb(std::vector<double>& x0, unsigned long long seed) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> dp(-0.5, 0.5), dpsi(-0.05, 0.05), dv(-0.5, 0.5);
+  x0[0] += dp(rng);
+  x0[1] += dp(rng);
+  x0[2] += dpsi(rng);
+  x0[3] += dv(rng);
+}
+
+ProblemData* build_scenario(const bmpc_scenario& sc) {
+  auto pd = std::make_unique<ProblemData>();
+  Spec spec;
+  std::vector<int> steps, arities;
+  std::vector<double> weights;  // max_arity 16
+  constexpr int kMaxA = 16;
+  if (sc.family == BMPC_SCENARIO_INTERSECTION) {
+    spec = intersection_spec(sc.horizon, sc.total_time, sc.shared_time[0]);
+    const int leaves = sc.v1 * sc.v2;
+    const bool ok = leaves == 1 || leaves == 2 || leaves == 4 || leaves == 6 || leaves == 9 || leaves == 12;
+    if (!ok || sc.v1 < 1 || sc.v2 < 1)
+      throw std::invalid_argument("build_intersection_case: leaf count " + std::to_string(leaves) +
+                                  " not in {1, 2, 4, 6, 9, 12}");
+    if (sc.v1 > 4 || sc.v2 > 4)
+      throw std::invalid_argument("build_intersection_case: need 2 vehicles with enough targets");
+    const int branch_step = static_cast<int>(std::lround(spec.shared_times.at(0) / spec.dt()));
+    if (leaves > 1) {
+      if (branch_step < 0 || branch_step >= spec.horizon)
+        throw std::invalid_argument("build_intersection_case: shared time outside the horizon");
+      steps.push_back(std::max(branch_step, 0));
+      arities.push_back(leaves);
+      weights.assign(kMaxA, 0.0);
+      for (int a = 0; a < leaves; ++a) weights[static_cast<size_t>(a)] = 1.0 / leaves;
+    }
+  } else if (sc.family == BMPC_SCENARIO_LATENCY) {
+    spec = latency_spec(sc.shared_time[1], sc.horizon, sc.total_time, sc.shared_time[0]);
+    if (!(spec.shared_times[0] < spec.shared_times[1]) || !(spec.shared_times[1] < spec.total_time))
+      throw std::invalid_argument("build_latency_case: need T_sh0 < T_sh1 < T");
+    const int k0 = static_cast<int>(std::lround(spec.shared_times[0] / spec.dt()));
+    const int k1 = static_cast<int>(std::lround(spec.shared_times[1] / spec.dt()));
+    if (k0 < 0 || k0 >= k1 || k1 >= spec.horizon)
+      throw std::invalid_argument("build_latency_case: branch steps must satisfy 0 <= k0 < k1 < N");
+    steps = {k0, k1};
+    arities = {2, 2};
+    weights.assign(2 * kMaxA, 0.0);
+    weights[0] = weights[1] = weights[kMaxA] = weights[kMaxA + 1] = 0.5;
+  } else if (sc.family == BMPC_SCENARIO_MULTISTAGE) {
+    spec = intersection_spec(sc.horizon, sc.total_time, 0.1);
+    if (sc.n_branchings < 0 || sc.n_branchings > 8) throw std::invalid_argument("multistage: 0..8 branchings");
+    weights.assign(static_cast<size_t>(std::max(sc.n_branchings, 1)) * kMaxA, 0.0);
+    for (int b = 0; b < sc.n_branchings; ++b) {
+      if (sc.branch_arity[b] < 2 || sc.branch_arity[b] > 4)
+        throw std::invalid_argument("multistage: arity must be in [2, 4] (4 speed targets per vehicle)");
+      steps.push_back(sc.branch_step[b]);
+      arities.push_back(sc.branch_arity[b]);
+      for (int a = 0; a < sc.branch_arity[b]; ++a)
+        weights[static_cast<size_t>(b) * kMaxA + a] = 1.0 / sc.branch_arity[b];
+    }
+  } else {
+    throw std::invalid_argument("unknown scenario family");
+  }
+  pd->tree = make_tree(spec.horizon, static_cast<int>(steps.size()), steps.data(), arities.data(),
+                       weights.empty() ? nullptr : weights.data(), kMaxA);
+  const bmpc_tree& t = *pd->tree;
+  const auto choices = branch_choices(t, steps);
+  std::vector<double> veh;
+  std::vector<std::array<double, 4>> ref_nodes(static_cast<size_t>(t.node_count));
+  if (sc.family == BMPC_SCENARIO_INTERSECTION) {
+    const int v2 = sc.v2;
+    const auto target_of = [&](size_t vehicle, int node) {
+      const auto& c = choices[static_cast<size_t>(node)];
+      const int s = c.empty() ? -1 : c[0];
+      if (s < 0) return spec.vehicles[vehicle].speed;
+      const int option = vehicle == 0 ? s / v2 : s % v2;
+      return spec.vehicles[vehicle].targets[static_cast<size_t>(option)];
+    };
+    veh = predict_vehicles(t, spec, target_of);
+    const auto ref = left_turn_reference(spec);
+    for (int i = 0; i < t.node_count; ++i) ref_nodes[static_cast<size_t>(i)] = ref[static_cast<size_t>(t.time_step[i])];
+  } else if (sc.family == BMPC_SCENARIO_MULTISTAGE) {
+    const auto target_of = [&](size_t vehicle, int node) {
+      const auto& c = choices[static_cast<size_t>(node)];
+      double target = spec.vehicles[vehicle].speed;
+      for (size_t j = 0; j < c.size(); ++j)
+        if (j % 2 == vehicle && c[j] >= 0) target = spec.vehicles[vehicle].targets.at(static_cast<size_t>(c[j]));
+      return target;
+    };
+    veh = predict_vehicles(t, spec, target_of);
+    const auto ref = left_turn_reference(spec);
+    for (int i = 0; i < t.node_count; ++i) ref_nodes[static_cast<size_t>(i)] = ref[static_cast<size_t>(t.time_step[i])];
+  } else {  // latency (scenarios.hpp:416-441)
+    const auto target_of = [&](size_t, int node) {
+      const int s = choices[static_cast<size_t>(node)][0];
+      return s < 0 ? spec.vehicles[0].speed : spec.vehicles[0].targets[static_cast<size_t>(s)];
+    };
+    veh = predict_vehicles(t, spec, target_of);
+    const double dt = spec.dt();
+    ref_nodes[0] = {spec.ego[0], spec.ego[1], spec.ego[2], spec.ego[3]};
+    for (int i = 0; i < t.node_count; ++i) {
+      for (int c = 0; c < t.child_count[i]; ++c) {
+        const int ch = t.first_child[i] + c;
+        std::array<double, 4> r = ref_nodes[static_cast<size_t>(i)];
+        const bool lead_brakes = choices[static_cast<size_t>(ch)][0] == 1;
+        const int decision = choices[static_cast<size_t>(ch)][1];
+        double decel = 0.0;
+        if (lead_brakes && decision == 0) decel = spec.continue_deceleration;
+        if (lead_brakes && decision == 1) decel = spec.backup_deceleration;
+        const double v_ref = std::max(0.0, r[3] - decel * dt);
+        r[0] += dt * 0.5 * (r[3] + v_ref);
+        r[3] = v_ref;
+        ref_nodes[static_cast<size_t>(ch)] = r;
+      }
+    }
+  }
+  fill_unicycle(*pd, spec);
+  if (sc.perturb) perturb(pd->x0, sc.perturb_seed);
+  pd->reference.resize(static_cast<size_t>(t.node_count) * 4);
+  for (int i = 0; i < t.node_count; ++i)
+    for (int j = 0; j < 4; ++j) pd->reference[static_cast<size_t>(i) * 4 + j] = ref_nodes[static_cast<size_t>(i)][j];
+  pd->vehicles = std::move(veh);
+  pd->pub.tree = pd->tree.get();
+  pd->pub.model.initial_state = pd->x0.data();
+  pd->pub.model.reference = pd->reference.data();
+  pd->pub.model.vehicle_position = pd->vehicles.data();
+  return pd.release();
+}
+
+// ------------------------------------------------------------ device mem
+struct DevBuf {
+  void* p{nullptr};
+  size_t bytes{0};
+  DevBuf() = default;
+  explicit DevBuf(size_t n) : bytes(n) {
+    if (n) ck(cudaMalloc(&p, n), "cudaMalloc");
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(bytes, o.bytes);
+    return *this;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// Segment plan (see solver.cuh): host copy + device arrays + device Topo.
+struct Plan {
+  int n{0}, ndepth{0}, nseg{0}, scratch{0}, max_con{0};
+  bool has_constraints{false};
+  std::vector<int> depth_begin, depth_len, seg_off, seg_nodes, seg_scratch, node_seg, node_pos;
+  DevBuf d_ints, d_weight, d_topo;
+  Topo topo{};
+};
+
+std::unique_ptr<Plan> make_plan(const bmpc_tree& t, int max_con, bool has_constraints, cudaStream_t s) {
+  auto pl = std::make_unique<Plan>();
+  const int n = t.node_count;
+  pl->n = n;
+  pl->max_con = max_con;
+  pl->has_constraints = has_constraints;
+  // Validate the contiguous-children (BFS) layout the device relies on.
+  for (int i = 1; i < n; ++i) {
+    const int p = t.parent[i];
+    if (p < 0 || p >= i || i < t.first_child[p] || i >= t.first_child[p] + t.child_count[p])
+      throw std::invalid_argument("tree: children must be contiguous and indexed after their parent");
+  }
+  // Segments: heads are the root and every child of a branch node.
+  struct Seg {
+    int depth, head;
+    std::vector<int> nodes;
+  };
+  std::vector<Seg> segs;
+  std::vector<std::pair<int, int>> stack{{0, 0}};  // (head, depth)
+  while (!stack.empty()) {
+    auto [h, d] = stack.back();
+    stack.pop_back();
+    Seg sg{d, h, {}};
+    int i = h;
+    while (true) {
+      sg.nodes.push_back(i);
+      if (t.child_count[i] == 1) {
+        i = t.first_child[i];
+        continue;
+      }
+      for (int c = t.child_count[i] - 1; c >= 0; --c) stack.push_back({t.first_child[i] + c, d + 1});
+      break;
+    }
+    segs.push_back(std::move(sg));
+  }
+  std::stable_sort(segs.begin(), segs.end(), [](const Seg& a, const Seg& b) {
+    return a.depth != b.depth ? a.depth < b.depth : a.head < b.head;
+  });
+  pl->nseg = static_cast<int>(segs.size());
+  pl->ndepth = segs.back().depth + 1;
+  pl->depth_begin.assign(static_cast<size_t>(pl->ndepth) + 1, 0);
+  pl->depth_len.assign(static_cast<size_t>(pl->ndepth), 0);
+  pl->node_seg.assign(static_cast<size_t>(n), -1);
+  pl->node_pos.assign(static_cast<size_t>(n), -1);
+  pl->seg_off.push_back(0);
+  int scratch = 0;
+  for (int s = 0; s < pl->nseg; ++s) {
+    const Seg& sg = segs[static_cast<size_t>(s)];
+    const int L = static_cast<int>(sg.nodes.size());
+    if (pl->depth_len[static_cast<size_t>(sg.depth)] == 0) pl->depth_len[static_cast<size_t>(sg.depth)] = L;
+    if (pl->depth_len[static_cast<size_t>(sg.depth)] != L)
+      throw std::invalid_argument("tree: segments at one branching depth must have equal length (balanced tree)");
+    pl->depth_begin[static_cast<size_t>(sg.depth) + 1] = s + 1;
+    for (int k = 0; k < L; ++k) {
+      pl->node_seg[static_cast<size_t>(sg.nodes[static_cast<size_t>(k)])] = s;
+      pl->node_pos[static_cast<size_t>(sg.nodes[static_cast<size_t>(k)])] = k;
+      pl->seg_nodes.push_back(sg.nodes[static_cast<size_t>(k)]);
+    }
+    pl->seg_off.push_back(static_cast<int>(pl->seg_nodes.size()));
+    pl->seg_scratch.push_back(scratch);
+    scratch += 2 * L;
+  }
+  for (int d = 1; d <= pl->ndepth; ++d)
+    pl->depth_begin[static_cast<size_t>(d)] = std::max(pl->depth_begin[static_cast<size_t>(d)],
+                                                       pl->depth_begin[static_cast<size_t>(d) - 1]);
+  pl->scratch = scratch;
+
+  // One int buffer for all index arrays.
+  std::vector<int> ints;
+  auto put = [&ints](const int* p, size_t k) {
+    const size_t off = ints.size();
+    ints.insert(ints.end(), p, p + k);
+    return off;
+  };
+  const size_t o_parent = put(t.parent, n), o_fc = put(t.first_child, n), o_nc = put(t.child_count, n);
+  const size_t o_db = put(pl->depth_begin.data(), pl->depth_begin.size());
+  const size_t o_dl = put(pl->depth_len.data(), pl->depth_len.size());
+  const size_t o_so = put(pl->seg_off.data(), pl->seg_off.size());
+  const size_t o_sn = put(pl->seg_nodes.data(), pl->seg_nodes.size());
+  const size_t o_ss = put(pl->seg_scratch.data(), pl->seg_scratch.size());
+  const size_t o_ns = put(pl->node_seg.data(), pl->node_seg.size());
+  const size_t o_np = put(pl->node_pos.data(), pl->node_pos.size());
+  pl->d_ints = DevBuf(ints.size() * sizeof(int));
+  ck(cudaMemcpyAsync(pl->d_ints.p, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice, s), "plan");
+  pl->d_weight = DevBuf(static_cast<size_t>(n) * sizeof(double));
+  ck(cudaMemcpyAsync(pl->d_weight.p, t.weight, static_cast<size_t>(n) * sizeof(double), cudaMemcpyHostToDevice, s),
+     "plan");
+  const int* base = pl->d_ints.as<int>();
+  Topo& tp = pl->topo;
+  tp.n = n;
+  tp.parent = base + o_parent;
+  tp.weight = pl->d_weight.as<double>();
+  tp.first_child = base + o_fc;
+  tp.nchild = base + o_nc;
+  tp.ndepth = pl->ndepth;
+  tp.depth_begin = base + o_db;
+  tp.depth_len = base + o_dl;
+  tp.seg_off = base + o_so;
+  tp.seg_nodes = base + o_sn;
+  tp.seg_scratch = base + o_ss;
+  tp.node_seg = base + o_ns;
+  tp.node_pos = base + o_np;
+  tp.has_constraints = has_constraints ? 1 : 0;
+  tp.max_con = std::max(max_con, 1);
+  pl->d_topo = DevBuf(sizeof(Topo));
+  ck(cudaMemcpyAsync(pl->d_topo.p, &tp, sizeof(Topo), cudaMemcpyHostToDevice, s), "plan");
+  ck(cudaStreamSynchronize(s), "plan sync");
+  return pl;
+}
+
+DevOptions to_dev(const bmpc_options& o) {
+  DevOptions d{};
+  d.max_inner_iterations = o.max_inner_iterations;
+  d.max_outer_iterations = o.max_outer_iterations;
+  d.alpha_levels = o.alpha_levels;
+  d.armijo_beta = o.armijo_beta;
+  d.merit_gamma = o.merit_gamma;
+  d.merit_mu0 = o.merit_mu0;
+  d.merit_mu_init = o.merit_mu_init;
+  d.defect_epsilon = o.defect_epsilon;
+  d.tol_defect = o.tol_defect;
+  d.tol_cost = o.tol_cost;
+  d.tol_feedforward = o.tol_feedforward;
+  d.tol_constraint = o.tol_constraint;
+  d.penalty_init = o.penalty_init;
+  d.penalty_growth = o.penalty_growth;
+  d.penalty_max = o.penalty_max;
+  d.reg_init = o.reg_init;
+  d.reg_min = o.reg_min;
+  d.reg_growth = o.reg_growth;
+  d.reg_decay = o.reg_decay;
+  d.reg_max = o.reg_max;
+  return d;
+}
+
+void fill_report(const DevResult& r, bmpc_report* out) {
+  out->status = r.status;
+  out->error_code = r.error_code;
+  out->error_node = r.error_node;
+  out->inner_iterations = r.inner_iterations;
+  out->outer_iterations = r.outer_iterations;
+  out->n_records = r.n_records;
+  out->final_cost = r.final_cost;
+  out->final_violation = r.final_violation;
+  out->final_defect_l1 = r.final_defect_l1;
+  for (int k = 0; k < 6; ++k) out->times[k] = r.times[k];
+  out->final_penalty = r.final_penalty;
+  out->final_mu = r.final_mu;
+  out->final_reg = r.final_reg;
+  const char* msg = "";
+  char buf[160];
+  switch (r.error_code) {
+    case kErrRegCap: msg = "regularization exceeded its cap"; break;
+    case kErrFactorization: msg = "combine_bwd: singular (I + C P) at regularization cap"; break;
+    case kErrLineSearch: msg = "line search failed at maximum regularization"; break;
+    case kErrLinearizeNonfinite:
+      std::snprintf(buf, sizeof buf, "linearize: non-finite expansion at node %d", r.error_node);
+      msg = buf;
+      break;
+    case kErrRolloutNonfinite:
+      std::snprintf(buf, sizeof buf, "nonlinear_rollout: non-finite state at node %d", r.error_node);
+      msg = buf;
+      break;
+    case kErrAlphaLevels: msg = "alpha_levels must lie in [1, 16]"; break;
+    default: break;
+  }
+  std::snprintf(out->message, sizeof out->message, "%s", msg);
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+struct bmpc_ctx {
+  int device{0};
+  cudaStream_t stream{nullptr};
+  bool own_stream{false};
+  long long launches{0};
+  int sms{0};
+};
+
+// Device-resident instances sharing one plan.
+struct bmpc_batch {
+  bmpc_ctx* ctx{nullptr};
+  std::unique_ptr<Plan> plan;
+  int count{0}, nx{0}, nu{0}, kind{0}, nv{0}, max_records{0};
+  size_t node_data_doubles{0};  // per instance: reference+vehicles or lq stage+leaf
+  Strides st{};
+  DevBuf model_data, x0, state, records, results, mps, works, red;
+  std::vector<ModelParams> h_mps;
+  std::vector<Work> h_works;
+  size_t per_state_doubles{0};
+  int threads{256};
+  bool grid_mode{false};
+  int grid_blocks{0};
+};
+
+namespace {
+
+size_t align2(size_t v) { return (v + 1) & ~size_t{1}; }
+
+// Lays out every per-instance array; returns doubles per instance.
+size_t state_layout(const Plan& pl, int nx, int nu, const Strides& st, size_t off[12]) {
+  const size_t n = static_cast<size_t>(pl.n);
+  size_t o = 0;
+  const size_t sizes[] = {align2(n * nx),                                   // x
+                          align2(n * nu),                                   // u
+                          align2(n * static_cast<size_t>(pl.topo.max_con)), // eta
+                          n * static_cast<size_t>(st.stage),                // stage
+                          align2(n * nx),                                   // defect
+                          n * static_cast<size_t>(st.policy),               // policy
+                          static_cast<size_t>(pl.scratch) * st.bwd,          // bwd
+                          static_cast<size_t>(pl.scratch) * st.fwd,          // fwd
+                          align2(n * nx),                                   // dx
+                          align2(n * nu),                                   // du
+                          n * static_cast<size_t>(st.value)};               // value
+  for (int k = 0; k < 11; ++k) {
+    off[k] = o;
+    o += sizes[k];
+  }
+  off[11] = o;
+  return o;
+}
+
+int check_model(const bmpc_tree* tree, const bmpc_model_desc* m) {
+  if (!tree || !m) return fail(BMPC_ERR_INVALID, "null tree or model");
+  if (!solve_dims_supported(m->state_dim, m->input_dim))
+    return fail(BMPC_ERR_UNSUPPORTED, "state/input dims (" + std::to_string(m->state_dim) + "," +
+                                          std::to_string(m->input_dim) + ") not compiled in");
+  if (m->kind == BMPC_MODEL_UNICYCLE) {
+    if (m->state_dim != 4 || m->input_dim != 2) return fail(BMPC_ERR_INVALID, "unicycle needs nx=4, nu=2");
+    if (m->num_vehicles < 0 || m->num_vehicles > kMaxVehicles)
+      return fail(BMPC_ERR_UNSUPPORTED, "num_vehicles must lie in [0, 4]");
+    if (!m->reference || (m->num_vehicles > 0 && !m->vehicle_position))
+      return fail(BMPC_ERR_INVALID, "unicycle model needs reference and vehicle arrays");
+  } else if (m->kind == BMPC_MODEL_AFFINE_QUADRATIC) {
+    if (!m->lq_stage || !m->lq_leaf) return fail(BMPC_ERR_INVALID, "affine-quadratic model needs stage/leaf arrays");
+  } else {
+    return fail(BMPC_ERR_UNSUPPORTED, "unknown model kind");
+  }
+  if (!m->initial_state) return fail(BMPC_ERR_INVALID, "initial_state is null");
+  return BMPC_OK;
+}
+
+size_t lq_stage_size(int nx, int nu) { return static_cast<size_t>(2 * nx * nx + nx * nu + nx + nu * nu + nu * nx + nx + nu); }
+
+size_t node_data_doubles(const bmpc_tree* t, const bmpc_model_desc* m) {
+  const size_t n = static_cast<size_t>(t->node_count);
+  if (m->kind == BMPC_MODEL_UNICYCLE) return align2(n * 4) + align2(n * static_cast<size_t>(m->num_vehicles) * 2);
+  const int nx = m->state_dim, nu = m->input_dim;
+  return align2(n * lq_stage_size(nx, nu)) + align2(n * static_cast<size_t>(nx * nx + nx));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bmpc_last_error(void) { return g_error.c_str(); }
+const char* bmpc_version(void) { return "bmpc_b200 0.1 (sm_100a)"; }
+
+int bmpc_tree_build(int horizon, int n_branchings, const int* steps, const int* arities, const double* weights,
+                    int max_arity, bmpc_tree** out) {
+  try {
+    if (!out || (n_branchings > 0 && (!steps || !arities || !weights))) return fail(BMPC_ERR_INVALID, "null argument");
+    *out = make_tree(horizon, n_branchings, steps, arities, weights, max_arity).release();
+    return BMPC_OK;
+  } catch (const std::invalid_argument& e) {
+    return fail(BMPC_ERR_INVALID, e.what());
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_INVALID, e.what());
+  }
+}
+
+void bmpc_tree_free(bmpc_tree* t) {
+  if (!t) return;
+  delete[] t->parent;
+  delete[] t->time_step;
+  delete[] t->weight;
+  delete[] t->first_child;
+  delete[] t->child_count;
+  delete[] t->step_begin;
+  delete[] t->leaves;
+  delete t;
+}
+
+int bmpc_scenario_build(const bmpc_scenario* spec, bmpc_problem_data** out) {
+  try {
+    if (!spec || !out) return fail(BMPC_ERR_INVALID, "null argument");
+    ProblemData* pd = build_scenario(*spec);
+    *out = &pd->pub;
+    return BMPC_OK;
+  } catch (const std::out_of_range& e) {
+    return fail(BMPC_ERR_OUT_OF_RANGE, e.what());
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_INVALID, e.what());
+  }
+}
+
+void bmpc_problem_data_free(bmpc_problem_data* data) {
+  if (!data) return;
+  // pub is the first member of ProblemData.
+  delete reinterpret_cast<ProblemData*>(data);
+}
+
+void bmpc_options_default(bmpc_options* o) {  // solver.hpp:35-57
+  o->max_inner_iterations = 100;
+  o->max_outer_iterations = 10;
+  o->alpha_levels = 11;
+  o->armijo_beta = 1e-4;
+  o->merit_gamma = 0.5;
+  o->merit_mu0 = 1.0;
+  o->merit_mu_init = 1.0;
+  o->defect_epsilon = 1e-8;
+  o->tol_defect = 1e-8;
+  o->tol_cost = 1e-8;
+  o->tol_feedforward = 1e-6;
+  o->tol_constraint = 1e-4;
+  o->penalty_init = 10.0;
+  o->penalty_growth = 10.0;
+  o->penalty_max = 1e8;
+  o->reg_init = 0.0;
+  o->reg_min = 1e-6;
+  o->reg_growth = 10.0;
+  o->reg_decay = 10.0;
+  o->reg_max = 1e10;
+}
+
+int bmpc_ctx_create(int device, bmpc_ctx** out) {
+  try {
+    if (!out) return fail(BMPC_ERR_INVALID, "null argument");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return fail(BMPC_ERR_CUDA, "no CUDA device available");
+    if (device < 0 || device >= n) return fail(BMPC_ERR_INVALID, "device index out of range");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    auto* c = new bmpc_ctx{};
+    c->device = device;
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    c->own_stream = true;
+    ck(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device), "attr");
+    *out = c;
+    return BMPC_OK;
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
+}
+
+void bmpc_ctx_destroy(bmpc_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int bmpc_ctx_set_stream(bmpc_ctx* c, void* stream) {
+  if (!c) return fail(BMPC_ERR_INVALID, "null ctx");
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (stream) {
+    c->stream = static_cast<cudaStream_t>(stream);
+    c->own_stream = false;
+  } else {
+    cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    c->own_stream = true;
+  }
+  return BMPC_OK;
+}
+
+int bmpc_ctx_synchronize(bmpc_ctx* c) {
+  if (!c) return fail(BMPC_ERR_INVALID, "null ctx");
+  const cudaError_t e = cudaStreamSynchronize(c->stream);
+  return e == cudaSuccess ? BMPC_OK : fail(BMPC_ERR_CUDA, cudaGetErrorString(e));
+}
+
+long long bmpc_ctx_launch_count(const bmpc_ctx* c) { return c ? c->launches : 0; }
+
+int bmpc_batch_create(bmpc_ctx* ctx, const bmpc_tree* tree, int count, const bmpc_model_desc* tmpl, int max_records,
+                      bmpc_batch** out) {
+  try {
+    if (!ctx || !out || count < 1) return fail(BMPC_ERR_INVALID, "bad batch arguments");
+    if (const int rc = check_model(tree, tmpl); rc != BMPC_OK) return rc;
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    auto b = std::make_unique<bmpc_batch>();
+    b->ctx = ctx;
+    b->count = count;
+    b->nx = tmpl->state_dim;
+    b->nu = tmpl->input_dim;
+    b->kind = tmpl->kind;
+    b->nv = tmpl->kind == BMPC_MODEL_UNICYCLE ? tmpl->num_vehicles : 0;
+    b->max_records = std::max(max_records, 0);
+    const bool has_con = tmpl->kind == BMPC_MODEL_UNICYCLE;  // box rows at every non-leaf
+    const int max_con = tmpl->kind == BMPC_MODEL_UNICYCLE ? 4 + b->nv : 0;
+    b->plan = make_plan(*tree, max_con, has_con, ctx->stream);
+    b->st = strides_for(b->nx, b->nu);
+    size_t off[12];
+    b->per_state_doubles = state_layout(*b->plan, b->nx, b->nu, b->st, off);
+    b->node_data_doubles = node_data_doubles(tree, tmpl);
+    const size_t C = static_cast<size_t>(count);
+    b->model_data = DevBuf(C * b->node_data_doubles * sizeof(double));
+    b->x0 = DevBuf(C * align2(static_cast<size_t>(b->nx)) * sizeof(double));
+    b->state = DevBuf(C * b->per_state_doubles * sizeof(double));
+    b->records = DevBuf(C * static_cast<size_t>(std::max(b->max_records, 1)) * sizeof(DevRecord));
+    b->results = DevBuf(C * sizeof(DevResult));
+    b->mps = DevBuf(C * sizeof(ModelParams));
+    b->works = DevBuf(C * sizeof(Work));
+    // Grid mode for a single large tree: all SMs on one instance.
+    b->grid_mode = count == 1 && tree->node_count > 4096;
+    if (b->grid_mode) {
+      b->grid_blocks = solve_grid_blocks(b->nx, b->nu, b->threads);
+      if (b->grid_blocks < 1) return fail(BMPC_ERR_CUDA, "grid solve kernel cannot be made co-resident");
+      b->red = DevBuf(2 * static_cast<size_t>(b->grid_blocks) * kRedSlotsHost * sizeof(double));
+    }
+    b->h_mps.resize(C);
+    b->h_works.resize(C);
+    const size_t n = static_cast<size_t>(tree->node_count);
+    for (size_t i = 0; i < C; ++i) {
+      ModelParams& mp = b->h_mps[i];
+      std::memset(&mp, 0, sizeof mp);
+      mp.kind = tmpl->kind;
+      double* md = b->model_data.as<double>() + i * b->node_data_doubles;
+      if (tmpl->kind == BMPC_MODEL_UNICYCLE) {
+        mp.nv = b->nv;
+        mp.reference = md;
+        mp.vehicles = md + align2(n * 4);
+      } else {
+        mp.lq_stage = md;
+        mp.lq_leaf = md + align2(n * lq_stage_size(b->nx, b->nu));
+      }
+      Work& w = b->h_works[i];
+      double* s = b->state.as<double>() + i * b->per_state_doubles;
+      w.x0 = b->x0.as<double>() + i * align2(static_cast<size_t>(b->nx));
+      w.x = s + off[0];
+      w.u = s + off[1];
+      w.eta = s + off[2];
+      w.stage = s + off[3];
+      w.defect = s + off[4];
+      w.policy = s + off[5];
+      w.bwd = s + off[6];
+      w.fwd = s + off[7];
+      w.dx = s + off[8];
+      w.du = s + off[9];
+      w.value = s + off[10];
+      w.records = b->records.as<DevRecord>() + i * static_cast<size_t>(std::max(b->max_records, 1));
+      w.max_records = b->max_records;
+      w.result = b->results.as<DevResult>() + i;
+    }
+    ck(cudaMemcpyAsync(b->works.p, b->h_works.data(), C * sizeof(Work), cudaMemcpyHostToDevice, ctx->stream), "works");
+    *out = b.release();
+    return BMPC_OK;
+  } catch (const std::invalid_argument& e) {
+    return fail(BMPC_ERR_INVALID, e.what());
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
+}
+
+void bmpc_batch_destroy(bmpc_batch* b) {
+  if (!b) return;
+  cudaSetDevice(b->ctx->device);
+  cudaStreamSynchronize(b->ctx->stream);
+  delete b;
+}
+
+int bmpc_batch_set_models(bmpc_batch* b, const bmpc_model_desc* models, size_t* h2d_bytes) {
+  try {
+    if (!b || !models) return fail(BMPC_ERR_INVALID, "null argument");
+    ck(cudaSetDevice(b->ctx->device), "cudaSetDevice");
+    const size_t n = static_cast<size_t>(b->plan->n);
+    size_t bytes = 0;
+    cudaStream_t s = b->ctx->stream;
+    for (int i = 0; i < b->count; ++i) {
+      const bmpc_model_desc& m = models[i];
+      if (m.kind != b->kind || m.state_dim != b->nx || m.input_dim != b->nu ||
+          (b->kind == BMPC_MODEL_UNICYCLE && m.num_vehicles != b->nv))
+        return fail(BMPC_ERR_INVALID, "model " + std::to_string(i) + " does not match the batch template");
+      ModelParams& mp = b->h_mps[static_cast<size_t>(i)];
+      double* md = b->model_data.as<double>() + static_cast<size_t>(i) * b->node_data_doubles;
+      if (b->kind == BMPC_MODEL_UNICYCLE) {
+        mp.dt = m.dt;
+        std::memcpy(mp.Wx, m.state_weights, sizeof mp.Wx);
+        std::memcpy(mp.Wu, m.input_weights, sizeof mp.Wu);
+        std::memcpy(mp.Wf, m.terminal_weights, sizeof mp.Wf);
+        mp.a_max = m.accel_limit;
+        mp.w_max = m.yaw_rate_limit;
+        mp.radius = m.safety_radius;
+        ck(cudaMemcpyAsync(md, m.reference, n * 4 * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
+        bytes += n * 4 * sizeof(double);
+        if (b->nv > 0) {
+          const size_t vb = n * static_cast<size_t>(b->nv) * 2 * sizeof(double);
+          ck(cudaMemcpyAsync(md + align2(n * 4), m.vehicle_position, vb, cudaMemcpyHostToDevice, s), "h2d");
+          bytes += vb;
+        }
+      } else {
+        const size_t sb = n * lq_stage_size(b->nx, b->nu) * sizeof(double);
+        const size_t lb = n * static_cast<size_t>(b->nx * b->nx + b->nx) * sizeof(double);
+        ck(cudaMemcpyAsync(md, m.lq_stage, sb, cudaMemcpyHostToDevice, s), "h2d");
+        ck(cudaMemcpyAsync(md + align2(n * lq_stage_size(b->nx, b->nu)), m.lq_leaf, lb, cudaMemcpyHostToDevice, s),
+           "h2d");
+        bytes += sb + lb;
+      }
+      ck(cudaMemcpyAsync(b->x0.as<double>() + static_cast<size_t>(i) * align2(static_cast<size_t>(b->nx)),
+                         m.initial_state, static_cast<size_t>(b->nx) * sizeof(double), cudaMemcpyHostToDevice, s),
+         "h2d");
+      bytes += static_cast<size_t>(b->nx) * sizeof(double);
+    }
+    ck(cudaMemcpyAsync(b->mps.p, b->h_mps.data(), b->h_mps.size() * sizeof(ModelParams), cudaMemcpyHostToDevice, s),
+       "h2d");
+    bytes += b->h_mps.size() * sizeof(ModelParams);
+    if (h2d_bytes) *h2d_bytes = bytes;
+    return BMPC_OK;
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
+}
+
+int bmpc_batch_replicate(bmpc_batch* b) {
+  try {
+    if (!b) return fail(BMPC_ERR_INVALID, "null argument");
+    cudaStream_t s = b->ctx->stream;
+    for (int i = 1; i < b->count; ++i) {
+      b->h_mps[static_cast<size_t>(i)].dt = b->h_mps[0].dt;
+      std::memcpy(b->h_mps[static_cast<size_t>(i)].Wx, b->h_mps[0].Wx, sizeof b->h_mps[0].Wx);
+      std::memcpy(b->h_mps[static_cast<size_t>(i)].Wu, b->h_mps[0].Wu, sizeof b->h_mps[0].Wu);
+      std::memcpy(b->h_mps[static_cast<size_t>(i)].Wf, b->h_mps[0].Wf, sizeof b->h_mps[0].Wf);
+      b->h_mps[static_cast<size_t>(i)].a_max = b->h_mps[0].a_max;
+      b->h_mps[static_cast<size_t>(i)].w_max = b->h_mps[0].w_max;
+      b->h_mps[static_cast<size_t>(i)].radius = b->h_mps[0].radius;
+      ck(cudaMemcpyAsync(b->model_data.as<double>() + static_cast<size_t>(i) * b->node_data_doubles,
+                         b->model_data.as<double>(), b->node_data_doubles * sizeof(double), cudaMemcpyDeviceToDevice,
+                         s),
+         "d2d");
+      ck(cudaMemcpyAsync(b->x0.as<double>() + static_cast<size_t>(i) * align2(static_cast<size_t>(b->nx)),
+                         b->x0.as<double>(), static_cast<size_t>(b->nx) * sizeof(double), cudaMemcpyDeviceToDevice, s),
+         "d2d");
+    }
+    ck(cudaMemcpyAsync(b->mps.p, b->h_mps.data(), b->h_mps.size() * sizeof(ModelParams), cudaMemcpyHostToDevice, s),
+       "h2d");
+    return BMPC_OK;
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
+}
+
+// Initial inputs: zeros unless given (solver.hpp:604-609).
+static int batch_set_inputs(bmpc_batch* b, const double* initial_inputs) {
+  const size_t n = static_cast<size_t>(b->plan->n);
+  for (int i = 0; i < b->count; ++i) {
+    const Work& w = b->h_works[static_cast<size_t>(i)];
+    const size_t bytes = n * static_cast<size_t>(b->nu) * sizeof(double);
+    if (initial_inputs) {
+      ck(cudaMemcpyAsync(w.u, initial_inputs + static_cast<size_t>(i) * n * b->nu, bytes, cudaMemcpyHostToDevice,
+                         b->ctx->stream),
+         "inputs");
+    } else {
+      ck(cudaMemsetAsync(w.u, 0, bytes, b->ctx->stream), "inputs");
+    }
+  }
+  return BMPC_OK;
+}
+
+static int batch_launch(bmpc_batch* b, const bmpc_options* opts) {
+  bmpc_options o;
+  if (opts)
+    o = *opts;
+  else
+    bmpc_options_default(&o);
+  const DevOptions d = to_dev(o);
+  cudaError_t e;
+  if (b->grid_mode) {
+    e = launch_solve_grid(b->nx, b->nu, b->plan->d_topo.as<Topo>(), b->mps.as<ModelParams>(), b->works.as<Work>(), d,
+                          b->red.as<double>(), b->grid_blocks, b->threads, b->ctx->stream);
+  } else {
+    e = launch_solve_cta(b->nx, b->nu, b->plan->d_topo.as<Topo>(), b->mps.as<ModelParams>(), b->works.as<Work>(), d,
+                         b->count, b->threads, b->ctx->stream);
+  }
+  if (e != cudaSuccess) return fail(BMPC_ERR_CUDA, std::string("solve launch: ") + cudaGetErrorString(e));
+  ++b->ctx->launches;
+  return BMPC_OK;
+}
+
+int bmpc_batch_solve(bmpc_batch* b, const bmpc_options* opts) {
+  try {
+    if (!b) return fail(BMPC_ERR_INVALID, "null argument");
+    ck(cudaSetDevice(b->ctx->device), "cudaSetDevice");
+    // Zero initial inputs for every instance (one memset over the u arrays).
+    for (int i = 0; i < b->count; ++i)
+      ck(cudaMemsetAsync(b->h_works[static_cast<size_t>(i)].u, 0,
+                         static_cast<size_t>(b->plan->n) * static_cast<size_t>(b->nu) * sizeof(double),
+                         b->ctx->stream),
+         "inputs");
+    return batch_launch(b, opts);
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
+}
+
+int bmpc_batch_results(bmpc_batch* b, double* x_out, double* u_out, bmpc_report* reports, size_t* d2h_bytes) {
+  try {
+    if (!b) return fail(BMPC_ERR_INVALID, "null argument");
+    ck(cudaSetDevice(b->ctx->device), "cudaSetDevice");
+    cudaStream_t s = b->ctx->stream;
+    const size_t n = static_cast<size_t>(b->plan->n);
+    size_t bytes = 0;
+    std::vector<DevResult> res(static_cast<size_t>(b->count));
+    ck(cudaMemcpyAsync(res.data(), b->results.p, res.size() * sizeof(DevResult), cudaMemcpyDeviceToHost, s), "d2h");
+    bytes += res.size() * sizeof(DevResult);
+    for (int i = 0; i < b->count; ++i) {
+      const Work& w = b->h_works[static_cast<size_t>(i)];
+      if (x_out) {
+        ck(cudaMemcpyAsync(x_out + static_cast<size_t>(i) * n * b->nx, w.x, n * b->nx * sizeof(double),
+                           cudaMemcpyDeviceToHost, s),
+           "d2h");
+        bytes += n * b->nx * sizeof(double);
+      }
+      if (u_out) {
+        ck(cudaMemcpyAsync(u_out + static_cast<size_t>(i) * n * b->nu, w.u, n * b->nu * sizeof(double),
+                           cudaMemcpyDeviceToHost, s),
+           "d2h");
+        bytes += n * b->nu * sizeof(double);
+      }
+    }
+    ck(cudaStreamSynchronize(s), "sync");
+    if (reports)
+      for (int i = 0; i < b->count; ++i) fill_report(res[static_cast<size_t>(i)], &reports[i]);
+    if (d2h_bytes) *d2h_bytes = bytes;
+    return BMPC_OK;
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
+}
+
+int bmpc_batch_device_results(bmpc_batch* b, double** d_x, double** d_u, size_t* bytes_x, size_t* bytes_u) {
+  if (!b) return fail(BMPC_ERR_INVALID, "null argument");
+  // Per-instance state blocks are strided; expose instance 0 base + stride.
+  if (d_x) *d_x = b->h_works[0].x;
+  if (d_u) *d_u = b->h_works[0].u;
+  if (bytes_x) *bytes_x = b->per_state_doubles * sizeof(double);
+  if (bytes_u) *bytes_u = b->per_state_doubles * sizeof(double);
+  return BMPC_OK;
+}
+
+int bmpc_batch_records(bmpc_batch* b, int instance, bmpc_record* records, int max_records, int* n_records) {
+  try {
+    if (!b || instance < 0 || instance >= b->count) return fail(BMPC_ERR_INVALID, "bad instance");
+    DevResult r;
+    ck(cudaMemcpy(&r, b->results.as<DevResult>() + instance, sizeof r, cudaMemcpyDeviceToHost), "d2h");
+    const int k = std::min({r.n_records, max_records, b->max_records});
+    if (k > 0 && records) {
+      static_assert(sizeof(bmpc_record) == sizeof(DevRecord), "record layout");
+      ck(cudaMemcpy(records, b->h_works[static_cast<size_t>(instance)].records, static_cast<size_t>(k) * sizeof(DevRecord),
+                    cudaMemcpyDeviceToHost),
+         "d2h");
+    }
+    if (n_records) *n_records = r.n_records;
+    return BMPC_OK;
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
+}
+
+int bmpc_batch_info(const bmpc_batch* b, int* threads, int* blocks, int* regs) {
+  if (!b) return fail(BMPC_ERR_INVALID, "null argument");
+  if (threads) *threads = b->threads;
+  if (blocks) *blocks = b->grid_mode ? b->grid_blocks : b->count;
+  if (regs) *regs = solve_cta_regs(b->nx, b->nu);
+  return BMPC_OK;
+}
+
+int bmpc_solve(bmpc_ctx* ctx, const bmpc_tree* tree, const bmpc_model_desc* model, const bmpc_options* opts,
+               const double* initial_inputs, double* x_out, double* u_out, bmpc_report* report, bmpc_record* records,
+               int max_records) {
+  bmpc_batch* b = nullptr;
+  int rc = bmpc_batch_create(ctx, tree, 1, model, std::max(max_records, 0), &b);
+  if (rc != BMPC_OK) return rc;
+  std::unique_ptr<bmpc_batch, void (*)(bmpc_batch*)> guard(b, bmpc_batch_destroy);
+  rc = bmpc_batch_set_models(b, model, nullptr);
+  if (rc != BMPC_OK) return rc;
+  try {
+    batch_set_inputs(b, initial_inputs);
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
+  rc = batch_launch(b, opts);
+  if (rc != BMPC_OK) return rc;
+  bmpc_report rep{};
+  rc = bmpc_batch_results(b, x_out, u_out, &rep, nullptr);
+  if (rc != BMPC_OK) return rc;
+  if (report) *report = rep;
+  if (records && max_records > 0) {
+    int nrec = 0;
+    rc = bmpc_batch_records(b, 0, records, max_records, &nrec);
+    if (rc != BMPC_OK) return rc;
+  }
+  if (rep.error_code == kErrRolloutNonfinite) return fail(BMPC_ERR_ROLLOUT, rep.message);
+  return BMPC_OK;
+}
+
+int bmpc_lqr_tree(bmpc_ctx* ctx, const bmpc_tree* tree, int nx, int nu, const double* stage, const double* defect,
+                  const double* leaf, double reg, const double* dx0, int grid, double* K, double* k, double* P,
+                  double* p, double* dx, double* du, double* scalars) {
+  try {
+    if (!ctx || !tree || !stage || !defect || !leaf || !dx0 || !scalars) return fail(BMPC_ERR_INVALID, "null argument");
+    if (!lqr_dims_supported(nx, nu)) return fail(BMPC_ERR_UNSUPPORTED, "dims not compiled in");
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = ctx->stream;
+    auto plan = make_plan(*tree, 0, false, s);
+    const Strides st = strides_for(nx, nu);
+    size_t off[12];
+    const size_t per = state_layout(*plan, nx, nu, st, off);
+    const size_t n = static_cast<size_t>(tree->node_count);
+    // Host-side repack of the TreeStageModels into the device stage records.
+    std::vector<double> h(per, 0.0);
+    const size_t ss = lq_stage_size(nx, nu), ls = static_cast<size_t>(nx * nx + nx);
+    for (size_t i = 0; i < n; ++i) {
+      double* rec = h.data() + off[3] + i * st.stage;
+      if (tree->child_count[i] == 0) {
+        std::memcpy(rec + st.stage_Q, leaf + i * ls, sizeof(double) * nx * nx);
+        std::memcpy(rec + st.stage_q, leaf + i * ls + nx * nx, sizeof(double) * nx);
+      } else {
+        const double* src = stage + i * ss;
+        const int oA = 0, oB = nx * nx, oc = oB + nx * nu, oQ = oc + nx, oR = oQ + nx * nx, oM = oR + nu * nu,
+                  oq = oM + nu * nx, orr = oq + nx;
+        std::memcpy(rec + st.stage_A, src + oA, sizeof(double) * nx * nx);
+        std::memcpy(rec + st.stage_B, src + oB, sizeof(double) * nx * nu);
+        std::memcpy(rec + st.stage_Q, src + oQ, sizeof(double) * nx * nx);
+        std::memcpy(rec + st.stage_R, src + oR, sizeof(double) * nu * nu);
+        std::memcpy(rec + st.stage_M, src + oM, sizeof(double) * nu * nx);
+        std::memcpy(rec + st.stage_q, src + oq, sizeof(double) * nx);
+        std::memcpy(rec + st.stage_r, src + orr, sizeof(double) * nu);
+      }
+      if (i > 0) std::memcpy(h.data() + off[4] + i * nx, defect + i * nx, sizeof(double) * nx);
+    }
+    DevBuf d_state(per * sizeof(double)), d_x0(align2(static_cast<size_t>(nx)) * sizeof(double)),
+        d_sc(4 * sizeof(double)), d_work(sizeof(Work));
+    ck(cudaMemcpyAsync(d_state.p, h.data(), per * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
+    ck(cudaMemcpyAsync(d_x0.p, dx0, static_cast<size_t>(nx) * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
+    Work w{};
+    double* base = d_state.as<double>();
+    w.x0 = d_x0.as<double>();
+    w.x = base + off[0];  // zeros: the root head perturbation is x0 - x[0] = dx0
+    w.u = base + off[1];
+    w.eta = base + off[2];
+    w.stage = base + off[3];
+    w.defect = base + off[4];
+    w.policy = base + off[5];
+    w.bwd = base + off[6];
+    w.fwd = base + off[7];
+    w.dx = base + off[8];
+    w.du = base + off[9];
+    w.value = base + off[10];
+    ck(cudaMemcpyAsync(d_work.p, &w, sizeof w, cudaMemcpyHostToDevice, s), "h2d");
+    DevBuf red;
+    int blocks = 0;
+    if (grid) {
+      blocks = lqr_grid_blocks(nx, nu, 256);
+      red = DevBuf(2 * static_cast<size_t>(std::max(blocks, 1)) * kRedSlotsHost * sizeof(double));
+    }
+    ck(launch_lqr_tree(nx, nu, grid != 0, plan->d_topo.as<Topo>(), d_work.as<Work>(), reg, d_sc.as<double>(),
+                       red.as<double>(), blocks, 256, s),
+       "lqr launch");
+    ++ctx->launches;
+    ck(cudaMemcpyAsync(h.data(), d_state.p, per * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaMemcpyAsync(scalars, d_sc.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaStreamSynchronize(s), "sync");
+    for (size_t i = 0; i < n; ++i) {
+      const double* pol = h.data() + off[5] + i * st.policy;
+      const double* val = h.data() + off[10] + i * st.value;
+      if (K && tree->child_count[i] > 0) std::memcpy(K + i * nu * nx, pol + st.policy_K, sizeof(double) * nu * nx);
+      if (k && tree->child_count[i] > 0) std::memcpy(k + i * nu, pol + st.policy_k, sizeof(double) * nu);
+      if (P) std::memcpy(P + i * nx * nx, val + st.value_P, sizeof(double) * nx * nx);
+      if (p) std::memcpy(p + i * nx, val + st.value_p, sizeof(double) * nx);
+      if (dx) std::memcpy(dx + i * nx, h.data() + off[8] + i * nx, sizeof(double) * nx);
+      if (du && tree->child_count[i] > 0) std::memcpy(du + i * nu, h.data() + off[9] + i * nu, sizeof(double) * nu);
+    }
+    return BMPC_OK;
+  } catch (const std::invalid_argument& e) {
+    return fail(BMPC_ERR_INVALID, e.what());
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
+}
+
+}  // extern "C"

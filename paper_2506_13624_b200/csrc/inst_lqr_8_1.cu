@@ -1,0 +1,5 @@
+// Explicit instantiation: kernel-level LQR tree for nx=8, nu=1.
+#include "kernels_impl.cuh"
+namespace bmpc_b200 {
+template struct LqrLaunch<8, 1>;
+}  // namespace bmpc_b200

@@ -1,0 +1,332 @@
+// LQR-tree building blocks on device: stage records, the dual conditional
+// value-function scan element and its associative combination, the tree
+// Bellman step at branch nodes, feedback extraction, and the affine forward
+// maps. Each function restates one reference routine (cited) with fixed-size
+// register arithmetic; error conditions the reference signals with
+// exceptions are returned as codes so the device solve loop can take the same
+// branch (Levenberg escalation) the reference's catch sites take.
+#pragma once
+
+#include "linalg.cuh"
+
+namespace bmpc_b200 {
+
+enum BwdError : int { kBwdOk = 0, kIndefinite = 1, kFactorization = 2 };
+
+// Per-node stage record (reference StageModel, types.hpp:28-40, minus the
+// offset c, which lives per child edge as in TreeStageModels,
+// riccati.hpp:77-84). Leaves store their terminal (P, p) in the Q / q slots.
+template <int NX, int NU>
+struct StageLayout {
+  static constexpr int A = 0;
+  static constexpr int B = A + NX * NX;
+  static constexpr int Q = B + NX * NU;
+  static constexpr int R = Q + NX * NX;
+  static constexpr int M = R + NU * NU;
+  static constexpr int q = M + NU * NX;
+  static constexpr int r = q + NX;
+  static constexpr int size = r + NU;
+  static constexpr int stride = (size + 1) & ~1;  // 16-byte aligned records
+};
+
+// ScanElementBwd (lqr_scan.hpp:15-24): P, p, C, A, c.
+template <int NX>
+struct BwdLayout {
+  static constexpr int P = 0;
+  static constexpr int p = P + NX * NX;
+  static constexpr int C = p + NX;
+  static constexpr int A = C + NX * NX;
+  static constexpr int c = A + NX * NX;
+  static constexpr int size = c + NX;
+  static constexpr int stride = (size + 1) & ~1;
+};
+
+// ScanElementFwd (lqr_scan.hpp:160-163): A, c.
+template <int NX>
+struct FwdLayout {
+  static constexpr int A = 0;
+  static constexpr int c = NX * NX;
+  static constexpr int size = NX * NX + NX;
+  static constexpr int stride = (size + 1) & ~1;
+};
+
+template <int NX>
+struct ValueLayout {  // ValueFunction (types.hpp:43-50)
+  static constexpr int P = 0;
+  static constexpr int p = NX * NX;
+  static constexpr int stride = (NX * NX + NX + 1) & ~1;
+};
+
+template <int NX, int NU>
+struct PolicyLayout {  // FeedbackPolicy (types.hpp:53-56)
+  static constexpr int K = 0;
+  static constexpr int k = NU * NX;
+  static constexpr int stride = (NU * NX + NU + 1) & ~1;
+};
+
+// init_bwd_element (lqr_scan.hpp:28-49) for stage `s` (R already carrying the
+// Levenberg shift `reg`, solver.hpp:212-222) with offset `c`.
+template <int NX, int NU>
+__device__ int init_bwd_element(const double* s, double reg, const double* c, double* e) {
+  using L = StageLayout<NX, NU>;
+  using E = BwdLayout<NX>;
+  double R[NU * NU];
+  copy<NU * NU>(s + L::R, R);
+#pragma unroll
+  for (int i = 0; i < NU; ++i) R[i + i * NU] += reg;
+  Ldlt<NU> f;
+  f.compute(R);
+  if (!f.positive()) return kFactorization;
+  double RiMt[NU * NX];  // R^-1 M
+  copy<NU * NX>(s + L::M, RiMt);
+  f.template solve<NX>(RiMt);
+  double RiBt[NU * NX];  // R^-1 B'
+#pragma unroll
+  for (int j = 0; j < NX; ++j) {
+#pragma unroll
+    for (int i = 0; i < NU; ++i) RiBt[i + j * NU] = s[L::B + j + i * NX];
+  }
+  f.template solve<NX>(RiBt);
+  double Rir[NU];
+  copy<NU>(s + L::r, Rir);
+  f.template solve<1>(Rir);
+
+  double tmp[NX * NX];
+  // P = Q - M' R^-1 M
+  mtm<NX, NU, NX>(s + L::M, RiMt, tmp);
+#pragma unroll
+  for (int i = 0; i < NX * NX; ++i) e[E::P + i] = s[L::Q + i] - tmp[i];
+  // p = q - M' R^-1 r
+  double v[NX];
+  mtv<NX, NU>(s + L::M, Rir, v);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) e[E::p + i] = s[L::q + i] - v[i];
+  // C = B R^-1 B'
+  mm<NX, NU, NX>(s + L::B, RiBt, tmp);
+#pragma unroll
+  for (int i = 0; i < NX * NX; ++i) e[E::C + i] = tmp[i];
+  // A = A - B R^-1 M
+  mm<NX, NU, NX>(s + L::B, RiMt, tmp);
+#pragma unroll
+  for (int i = 0; i < NX * NX; ++i) e[E::A + i] = s[L::A + i] - tmp[i];
+  // c = c - B R^-1 r
+  mv<NX, NU>(s + L::B, Rir, v);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) e[E::c + i] = c[i] - v[i];
+  symmetrize<NX>(e + E::P);
+  symmetrize<NX>(e + E::C);
+  return kBwdOk;
+}
+
+// embed_terminal (lqr_scan.hpp:55-66).
+template <int NX>
+__device__ void embed_terminal(const double* P, const double* p, double* e) {
+  using E = BwdLayout<NX>;
+#pragma unroll
+  for (int i = 0; i < NX * NX; ++i) {
+    e[E::P + i] = P[i];
+    e[E::C + i] = 0.0;
+    e[E::A + i] = 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+    e[E::p + i] = p[i];
+    e[E::c + i] = 0.0;
+  }
+}
+
+// combine_bwd (lqr_scan.hpp:80-111): out = first (+) second, first = k->j,
+// second = j->i. One PartialPivLU of G = I + C1 P2 serves both G^-1 and
+// G^-T. Returns kFactorization when any output is non-finite.
+template <int NX>
+__device__ int combine_bwd(const double* __restrict__ e1, const double* __restrict__ e2, double* __restrict__ out) {
+  using E = BwdLayout<NX>;
+  double G[NX * NX];
+  mm<NX, NX, NX>(e1 + E::C, e2 + E::P, G);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) G[i + i * NX] += 1.0;
+  Lu<NX> lu;
+  lu.compute(G);
+
+  double X[NX * NX], Y[NX * NX], v[NX], w[NX];
+  bool ok = true;
+  // out.A = A2 G^-1 A1
+  lu.template solve<NX>(e1 + E::A, X);
+  mm<NX, NX, NX>(e2 + E::A, X, Y);
+  ok = ok && all_finite<NX * NX>(Y);
+#pragma unroll
+  for (int i = 0; i < NX * NX; ++i) out[E::A + i] = Y[i];
+  // out.c = A2 G^-1 (c1 - C1 p2) + c2
+  mv<NX, NX>(e1 + E::C, e2 + E::p, v);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) v[i] = e1[E::c + i] - v[i];
+  lu.template solve<1>(v, w);
+  mv<NX, NX>(e2 + E::A, w, v);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) v[i] += e2[E::c + i];
+  ok = ok && all_finite<NX>(v);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) out[E::c + i] = v[i];
+  // out.C = (A2 G^-1 C1) A2' + C2
+  lu.template solve<NX>(e1 + E::C, X);
+  mm<NX, NX, NX>(e2 + E::A, X, Y);
+  mmt<NX, NX, NX>(Y, e2 + E::A, X);
+#pragma unroll
+  for (int i = 0; i < NX * NX; ++i) X[i] += e2[E::C + i];
+  symmetrize<NX>(X);
+  ok = ok && all_finite<NX * NX>(X);
+#pragma unroll
+  for (int i = 0; i < NX * NX; ++i) out[E::C + i] = X[i];
+  // out.p = A1' G^-T (p2 + P2 c1) + p1
+  mv<NX, NX>(e2 + E::P, e1 + E::c, v);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) v[i] += e2[E::p + i];
+  lu.template solve_transposed<1>(v, w);
+  mtv<NX, NX>(e1 + E::A, w, v);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) v[i] += e1[E::p + i];
+  ok = ok && all_finite<NX>(v);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) out[E::p + i] = v[i];
+  // out.P = A1' G^-T (P2 A1) + P1
+  mm<NX, NX, NX>(e2 + E::P, e1 + E::A, X);
+  lu.template solve_transposed<NX>(X, Y);
+  mtm<NX, NX, NX>(e1 + E::A, Y, X);
+#pragma unroll
+  for (int i = 0; i < NX * NX; ++i) X[i] += e1[E::P + i];
+  symmetrize<NX>(X);
+  ok = ok && all_finite<NX * NX>(X);
+#pragma unroll
+  for (int i = 0; i < NX * NX; ++i) out[E::P + i] = X[i];
+  return ok ? kBwdOk : kFactorization;
+}
+
+// feedback_from_values (lqr_scan.hpp:146-157): policy at a node from the
+// value (P, p) of its single successor and the edge offset c.
+template <int NX, int NU>
+__device__ int feedback(const double* s, double reg, const double* c, const double* P, const double* p,
+                        double* K, double* k) {
+  using L = StageLayout<NX, NU>;
+  double BtP[NU * NX];
+  mtm<NU, NX, NX>(s + L::B, P, BtP);
+  double H[NU * NU];
+  mm<NU, NX, NU>(BtP, s + L::B, H);
+#pragma unroll
+  for (int i = 0; i < NU * NU; ++i) H[i] += s[L::R + i];
+#pragma unroll
+  for (int i = 0; i < NU; ++i) H[i + i * NU] += reg;
+  symmetrize<NU>(H);
+  Ldlt<NU> f;
+  f.compute(H);
+  if (!f.positive()) return kIndefinite;
+  // K = -H^-1 (M + B'PA)
+  double X[NU * NX];
+  mm<NU, NX, NX>(BtP, s + L::A, X);
+#pragma unroll
+  for (int i = 0; i < NU * NX; ++i) X[i] += s[L::M + i];
+  f.template solve<NX>(X);
+#pragma unroll
+  for (int i = 0; i < NU * NX; ++i) K[i] = -X[i];
+  // k = -H^-1 (r + B'(p + P c))
+  double pc[NX];
+  mv<NX, NX>(P, c, pc);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) pc[i] += p[i];
+  double y[NU];
+  mtv<NU, NX>(s + L::B, pc, y);
+#pragma unroll
+  for (int i = 0; i < NU; ++i) y[i] += s[L::r + i];
+  f.template solve<1>(y);
+#pragma unroll
+  for (int i = 0; i < NU; ++i) k[i] = -y[i];
+  return kBwdOk;
+}
+
+// riccati_step (riccati.hpp:22-43) at a branch node, with the continuation
+// already aggregated over the children: Pn = sum P_ch, pn = sum (p_ch + P_ch d_ch).
+template <int NX, int NU>
+__device__ int riccati_step(const double* s, double reg, const double* Pn, const double* pn, double* Pout,
+                            double* pout, double* K, double* k) {
+  using L = StageLayout<NX, NU>;
+  double AtP[NX * NX];
+  mtm<NX, NX, NX>(s + L::A, Pn, AtP);
+  double Qxx[NX * NX];
+  mm<NX, NX, NX>(AtP, s + L::A, Qxx);
+#pragma unroll
+  for (int i = 0; i < NX * NX; ++i) Qxx[i] += s[L::Q + i];
+  double BtP[NU * NX];
+  mtm<NU, NX, NX>(s + L::B, Pn, BtP);
+  double Quu[NU * NU];
+  mm<NU, NX, NU>(BtP, s + L::B, Quu);
+#pragma unroll
+  for (int i = 0; i < NU * NU; ++i) Quu[i] += s[L::R + i];
+#pragma unroll
+  for (int i = 0; i < NU; ++i) Quu[i + i * NU] += reg;
+  double Qux[NU * NX];
+  mm<NU, NX, NX>(BtP, s + L::A, Qux);
+#pragma unroll
+  for (int i = 0; i < NU * NX; ++i) Qux[i] += s[L::M + i];
+  double qx[NX];
+  mtv<NX, NX>(s + L::A, pn, qx);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) qx[i] += s[L::q + i];
+  double qu[NU];
+  mtv<NU, NX>(s + L::B, pn, qu);
+#pragma unroll
+  for (int i = 0; i < NU; ++i) qu[i] += s[L::r + i];
+  symmetrize<NU>(Quu);
+  Ldlt<NU> f;
+  f.compute(Quu);
+  if (!f.positive()) return kIndefinite;
+  double X[NU * NX];
+  copy<NU * NX>(Qux, X);
+  f.template solve<NX>(X);
+#pragma unroll
+  for (int i = 0; i < NU * NX; ++i) K[i] = -X[i];
+  double y[NU];
+  copy<NU>(qu, y);
+  f.template solve<1>(y);
+#pragma unroll
+  for (int i = 0; i < NU; ++i) k[i] = -y[i];
+  // P = Qxx + Qux' K ; p = qx + Qux' k
+  double T[NX * NX];
+  mtm<NX, NU, NX>(Qux, K, T);
+#pragma unroll
+  for (int i = 0; i < NX * NX; ++i) Pout[i] = Qxx[i] + T[i];
+  double t[NX];
+  mtv<NX, NU>(Qux, k, t);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) pout[i] = qx[i] + t[i];
+  symmetrize<NX>(Pout);
+  return kBwdOk;
+}
+
+// init_fwd_element (lqr_scan.hpp:166-168): (A + B K, c + B k).
+template <int NX, int NU>
+__device__ void init_fwd_element(const double* s, const double* c, const double* K, const double* k, double* f) {
+  using L = StageLayout<NX, NU>;
+  using F = FwdLayout<NX>;
+  double BK[NX * NX];
+  mm<NX, NU, NX>(s + L::B, K, BK);
+#pragma unroll
+  for (int i = 0; i < NX * NX; ++i) f[F::A + i] = s[L::A + i] + BK[i];
+  double Bk[NX];
+  mv<NX, NU>(s + L::B, k, Bk);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) f[F::c + i] = c[i] + Bk[i];
+}
+
+// combine_fwd (lqr_scan.hpp:171-173): (A2 A1, A2 c1 + c2).
+template <int NX>
+__device__ void combine_fwd(const double* __restrict__ f1, const double* __restrict__ f2, double* __restrict__ out) {
+  using F = FwdLayout<NX>;
+  double A[NX * NX], c[NX];
+  mm<NX, NX, NX>(f2 + F::A, f1 + F::A, A);
+  mv<NX, NX>(f2 + F::A, f1 + F::c, c);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) c[i] += f2[F::c + i];
+  copy<NX * NX>(A, out + F::A);
+  copy<NX>(c, out + F::c);
+}
+
+}  // namespace bmpc_b200

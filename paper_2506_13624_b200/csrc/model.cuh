@@ -1,0 +1,416 @@
+// Device node models: the reference's per-node callbacks (problem.hpp:15-40)
+// restated as device functions selected at compile time, since std::function
+// callbacks cannot run on the GPU. Two families cover every problem the
+// reference builds:
+//   * UnicycleTracking — kinematic unicycle with RK4 (unicycle.hpp:19-74),
+//     quadratic tracking costs (problem.hpp:194-222) and the ego constraints
+//     (scenarios.hpp:206-248): intersection, latency and multi-stage scenes.
+//   * AffineQuadratic  — affine dynamics + convex quadratic costs without
+//     constraints: testing::random_lq_problem (oracles.hpp:316-365).
+#pragma once
+
+#include "linalg.cuh"
+#include "lqr.cuh"
+#include "types.h"
+
+namespace bmpc_b200 {
+
+template <int NX, int NU>
+struct LqStage {  // packing of ModelParams::lq_stage records
+  static constexpr int A = 0, B = NX * NX, c = B + NX * NU, Q = c + NX, R = Q + NX * NX, M = R + NU * NU,
+                       q = M + NU * NX, r = q + NX, size = r + NU;
+};
+
+// Constraint rows at a node: non-leaf 4 box rows + nv distance rows, leaf nv.
+template <int NX, int NU>
+__device__ __forceinline__ int num_constraints(const ModelParams& mp, bool leaf) {
+  if (mp.kind != kModelUnicycle) return 0;
+  return (leaf ? 0 : 4) + mp.nv;
+}
+
+// --------------------------------------------------------------- unicycle
+__device__ __forceinline__ void unicycle_derivative(const double* x, const double* u, double* dx) {
+  double s, c;
+  sincos(x[2], &s, &c);
+  dx[0] = x[3] * c;
+  dx[1] = x[3] * s;
+  dx[2] = u[1];
+  dx[3] = u[0];
+}
+
+// unicycle::step (unicycle.hpp:36-42).
+__device__ __forceinline__ void unicycle_step(const double* x, const double* u, double dt, double* xn) {
+  double k1[4], k2[4], k3[4], k4[4], t[4];
+  unicycle_derivative(x, u, k1);
+  const double hdt = 0.5 * dt;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) t[i] = x[i] + hdt * k1[i];
+  unicycle_derivative(t, u, k2);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) t[i] = x[i] + hdt * k2[i];
+  unicycle_derivative(t, u, k3);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) t[i] = x[i] + dt * k3[i];
+  unicycle_derivative(t, u, k4);
+  const double s6 = dt / 6.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) xn[i] = x[i] + s6 * (((k1[i] + 2.0 * k2[i]) + 2.0 * k3[i]) + k4[i]);
+}
+
+// d(derivative)/dx at x (unicycle.hpp:25-34); only (0,2),(0,3),(1,2),(1,3) are
+// non-zero, d/du is the constant selector Ju(2,1) = Ju(3,0) = 1.
+__device__ __forceinline__ void unicycle_jx(const double* x, double* j02, double* j03, double* j12, double* j13) {
+  double s, c;
+  sincos(x[2], &s, &c);
+  *j02 = -x[3] * s;
+  *j03 = c;
+  *j12 = x[3] * c;
+  *j13 = s;
+}
+
+// unicycle::step_jacobians (unicycle.hpp:44-74): the analytic chain rule
+// through the RK4 stages, evaluated on the sparsity of the stage Jacobians
+// (J has four non-zeros, so J*(I + h dk) touches rows 0-1 only).
+__device__ __forceinline__ void unicycle_step_jacobians(const double* x, const double* u, double dt, double* A,
+                                                        double* B) {
+  double k1[4], k2[4], k3[4], x2[4], x3[4], x4[4];
+  unicycle_derivative(x, u, k1);
+  const double hdt = 0.5 * dt;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) x2[i] = x[i] + hdt * k1[i];
+  unicycle_derivative(x2, u, k2);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) x3[i] = x[i] + hdt * k2[i];
+  unicycle_derivative(x3, u, k3);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) x4[i] = x[i] + dt * k3[i];
+
+  // Dense 4x4 / 4x2 stage derivatives (column-major), kept dense for clarity;
+  // the zero pattern is exact, so rounding matches the dense reference.
+  double J[4][16];
+  {
+    const double* pts[4] = {x, x2, x3, x4};
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) J[s][i] = 0.0;
+      unicycle_jx(pts[s], &J[s][0 + 2 * 4], &J[s][0 + 3 * 4], &J[s][1 + 2 * 4], &J[s][1 + 3 * 4]);
+    }
+  }
+  // Ju: (2,1) = 1, (3,0) = 1.
+  double Ju[8] = {0, 0, 0, 1, 0, 0, 1, 0};
+  double I[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) I[i] = (i % 5 == 0) ? 1.0 : 0.0;
+
+  double dk1x[16], dk2x[16], dk3x[16], dk4x[16], T[16];
+  copy<16>(J[0], dk1x);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) T[i] = I[i] + hdt * dk1x[i];
+  mm<4, 4, 4>(J[1], T, dk2x);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) T[i] = I[i] + hdt * dk2x[i];
+  mm<4, 4, 4>(J[2], T, dk3x);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) T[i] = I[i] + dt * dk3x[i];
+  mm<4, 4, 4>(J[3], T, dk4x);
+
+  double dk1u[8], dk2u[8], dk3u[8], dk4u[8], Tu[8];
+  copy<8>(Ju, dk1u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) Tu[i] = hdt * dk1u[i];
+  mm<4, 4, 2>(J[1], Tu, dk2u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dk2u[i] += Ju[i];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) Tu[i] = hdt * dk2u[i];
+  mm<4, 4, 2>(J[2], Tu, dk3u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dk3u[i] += Ju[i];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) Tu[i] = dt * dk3u[i];
+  mm<4, 4, 2>(J[3], Tu, dk4u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dk4u[i] += Ju[i];
+
+  const double s6 = dt / 6.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) A[i] = I[i] + s6 * (((dk1x[i] + 2.0 * dk2x[i]) + 2.0 * dk3x[i]) + dk4x[i]);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) B[i] = s6 * (((dk1u[i] + 2.0 * dk2u[i]) + 2.0 * dk3u[i]) + dk4u[i]);
+}
+
+// ego_constraints (scenarios.hpp:206-248) values and, optionally, Jacobians.
+// Rows: [a-amax, -a-amax, w-wmax, -w-wmax] (non-leaf) then r - sqrt(d^2+eps).
+template <bool kJac>
+__device__ __forceinline__ int ego_constraints(const ModelParams& mp, int node, bool leaf, const double* x,
+                                               const double* u, double* g, double* Jx /*[kMaxCon*4]*/,
+                                               double* Ju /*[kMaxCon*2]*/) {
+  const int nb = leaf ? 0 : 4;
+  const int nc = nb + mp.nv;
+  if (kJac) {
+#pragma unroll
+    for (int i = 0; i < kMaxCon * 4; ++i) Jx[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < kMaxCon * 2; ++i) Ju[i] = 0.0;
+  }
+  if (!leaf) {
+    g[0] = u[0] - mp.a_max;
+    g[1] = -u[0] - mp.a_max;
+    g[2] = u[1] - mp.w_max;
+    g[3] = -u[1] - mp.w_max;
+    if (kJac) {  // Ju row-major over rows here: Ju[row*2 + col]
+      Ju[0 * 2 + 0] = 1.0;
+      Ju[1 * 2 + 0] = -1.0;
+      Ju[2 * 2 + 1] = 1.0;
+      Ju[3 * 2 + 1] = -1.0;
+    }
+  }
+  const double* vp = mp.vehicles + static_cast<long long>(node) * mp.nv * 2;
+#pragma unroll
+  for (int v = 0; v < kMaxVehicles; ++v) {
+    if (v < mp.nv) {
+      const double dx = x[0] - vp[2 * v + 0];
+      const double dy = x[1] - vp[2 * v + 1];
+      const double dist = sqrt(dx * dx + dy * dy + 1e-6);
+      g[nb + v] = mp.radius - dist;
+      if (kJac) {
+        Jx[(nb + v) * 4 + 0] = -dx / dist;
+        Jx[(nb + v) * 4 + 1] = -dy / dist;
+      }
+    }
+  }
+  return nc;
+}
+
+// Active-set AL penalty (problem.hpp:85-93).
+__device__ __forceinline__ double al_penalty(const double* g, const double* eta, int nc, double rho) {
+  double value = 0.0;
+#pragma unroll
+  for (int m = 0; m < kMaxCon; ++m) {
+    if (m < nc && (g[m] >= 0.0 || eta[m] > 0.0)) value += eta[m] * g[m] + 0.5 * rho * g[m] * g[m];
+  }
+  return value;
+}
+
+// 0.5 e' W e with W dense n x n (column-major).
+template <int N>
+__device__ __forceinline__ double quad_form(const double* W, const double* e) {
+  double We[N];
+  mv<N, N>(W, e, We);
+  return 0.5 * dot<N>(e, We);
+}
+
+// ----------------------------------------------------------- generic node API
+// Dynamics f(x, u) of non-leaf `node`.
+template <int NX, int NU>
+__device__ __forceinline__ void node_dynamics(const ModelParams& mp, int node, const double* x, const double* u,
+                                              double* xn) {
+  if constexpr (NX == 4 && NU == 2) {
+    if (mp.kind == kModelUnicycle) {
+      unicycle_step(x, u, mp.dt, xn);
+      return;
+    }
+  }
+  using S = LqStage<NX, NU>;
+  const double* s = mp.lq_stage + static_cast<long long>(node) * S::size;
+  double a[NX], b[NX];
+  mv<NX, NX>(s + S::A, x, a);
+  mv<NX, NU>(s + S::B, u, b);
+#pragma unroll
+  for (int i = 0; i < NX; ++i) xn[i] = (a[i] + b[i]) + s[S::c + i];
+}
+
+// Node objective value (weight not applied) plus AL penalty and max g.
+// Matches evaluate (problem.hpp:115-134) per node.
+template <int NX, int NU>
+__device__ __forceinline__ void node_cost(const ModelParams& mp, int node, bool leaf, const double* x,
+                                          const double* u, const double* eta, double rho, double* cost,
+                                          double* penalty, double* gmax) {
+  *penalty = 0.0;
+  *gmax = -INFINITY;
+  if constexpr (NX == 4 && NU == 2) {
+    if (mp.kind == kModelUnicycle) {
+      const double* ref = mp.reference + static_cast<long long>(node) * 4;
+      double e[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) e[i] = x[i] - ref[i];
+      if (leaf) {
+        *cost = quad_form<4>(mp.Wf, e);
+      } else {
+        *cost = quad_form<4>(mp.Wx, e) + quad_form<2>(mp.Wu, u);
+      }
+      double g[kMaxCon];
+      const int nc = ego_constraints<false>(mp, node, leaf, x, u, g, nullptr, nullptr);
+      *penalty = al_penalty(g, eta, nc, rho);
+      double m = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < kMaxCon; ++i)
+        if (i < nc) m = fmax(m, g[i]);
+      *gmax = m;
+      return;
+    }
+  }
+  if (leaf) {
+    const double* l = mp.lq_leaf + static_cast<long long>(node) * (NX * NX + NX);
+    double Px[NX];
+    mv<NX, NX>(l, x, Px);
+    *cost = 0.5 * dot<NX>(x, Px) + dot<NX>(l + NX * NX, x);
+  } else {
+    using S = LqStage<NX, NU>;
+    const double* s = mp.lq_stage + static_cast<long long>(node) * S::size;
+    double Qx[NX], Ru[NU], Mx[NU];
+    mv<NX, NX>(s + S::Q, x, Qx);
+    mv<NU, NU>(s + S::R, u, Ru);
+    mv<NU, NX>(s + S::M, x, Mx);
+    *cost = (((0.5 * dot<NX>(x, Qx) + dot<NX>(s + S::q, x)) + 0.5 * dot<NU>(u, Ru)) + dot<NU>(s + S::r, u)) +
+            dot<NU>(u, Mx);
+  }
+}
+
+// linearize (solver.hpp:76-136) of one node: weighted, AL-augmented
+// Gauss-Newton stage record (non-leaf) or terminal (P, p) in the Q/q slots.
+// Returns false on a non-finite expansion.
+template <int NX, int NU>
+__device__ __forceinline__ bool node_linearize(const ModelParams& mp, int node, bool leaf, double w, const double* x,
+                                               const double* u, const double* eta, double rho, double* rec) {
+  using L = StageLayout<NX, NU>;
+  if constexpr (NX == 4 && NU == 2) {
+    if (mp.kind == kModelUnicycle) {
+      const double* ref = mp.reference + static_cast<long long>(node) * 4;
+      double e[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) e[i] = x[i] - ref[i];
+      double g[kMaxCon], Jx[kMaxCon * 4], Ju[kMaxCon * 2];  // row-major Jacobians
+      const int nc = ego_constraints<true>(mp, node, leaf, x, u, g, Jx, Ju);
+      double as[kMaxCon], lam[kMaxCon];
+#pragma unroll
+      for (int m = 0; m < kMaxCon; ++m) {
+        as[m] = (m < nc && (g[m] >= 0.0 || eta[m] > 0.0)) ? rho : 0.0;
+        lam[m] = m < nc ? eta[m] + as[m] * g[m] : 0.0;
+      }
+      double Q[16], q[4];
+      const double* W = leaf ? mp.Wf : mp.Wx;
+      copy<16>(W, Q);
+      mv<4, 4>(W, e, q);
+      // q += Jx' lam ; Q += (Jx' diag(as)) Jx
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int m = 0; m < kMaxCon; ++m) s = fma(Jx[m * 4 + i], lam[m], s);
+        q[i] += s;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int m = 0; m < kMaxCon; ++m) s = fma(Jx[m * 4 + i] * as[m], Jx[m * 4 + j], s);
+          Q[i + 4 * j] += s;
+        }
+      }
+      bool ok = true;
+      if (leaf) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) rec[L::Q + i] = w * Q[i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) rec[L::q + i] = w * q[i];
+        ok = all_finite<16>(rec + L::Q) && all_finite<4>(rec + L::q);
+        return ok;
+      }
+      double R[4], M[8], r[2];
+      copy<4>(mp.Wu, R);
+      mv<2, 2>(mp.Wu, u, r);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) M[i] = 0.0;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int m = 0; m < kMaxCon; ++m) s = fma(Ju[m * 2 + i], lam[m], s);
+        r[i] += s;
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int m = 0; m < kMaxCon; ++m) s = fma(Ju[m * 2 + i] * as[m], Ju[m * 2 + j], s);
+          R[i + 2 * j] += s;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int m = 0; m < kMaxCon; ++m) s = fma(Ju[m * 2 + i] * as[m], Jx[m * 4 + j], s);
+          M[i + 2 * j] += s;
+        }
+      }
+      unicycle_step_jacobians(x, u, mp.dt, rec + L::A, rec + L::B);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) rec[L::Q + i] = w * Q[i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) rec[L::R + i] = w * R[i];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rec[L::M + i] = w * M[i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) rec[L::q + i] = w * q[i];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) rec[L::r + i] = w * r[i];
+      ok = all_finite<16>(rec + L::A) && all_finite<8>(rec + L::B) && all_finite<16>(rec + L::Q) &&
+           all_finite<4>(rec + L::R) && all_finite<4>(rec + L::q) && all_finite<2>(rec + L::r);
+      return ok;
+    }
+  }
+  // Affine-quadratic: expansion is point-independent except the gradients.
+  if (leaf) {
+    const double* l = mp.lq_leaf + static_cast<long long>(node) * (NX * NX + NX);
+    double Px[NX];
+    mv<NX, NX>(l, x, Px);
+#pragma unroll
+    for (int i = 0; i < NX * NX; ++i) rec[L::Q + i] = w * l[i];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) rec[L::q + i] = w * (Px[i] + l[NX * NX + i]);
+    return all_finite<NX * NX>(rec + L::Q) && all_finite<NX>(rec + L::q);
+  }
+  using S = LqStage<NX, NU>;
+  const double* s = mp.lq_stage + static_cast<long long>(node) * S::size;
+  double Qx[NX], Mtu[NX], Ru[NU], Mx[NU];
+  mv<NX, NX>(s + S::Q, x, Qx);
+  mtv<NX, NU>(s + S::M, u, Mtu);
+  mv<NU, NU>(s + S::R, u, Ru);
+  mv<NU, NX>(s + S::M, x, Mx);
+#pragma unroll
+  for (int i = 0; i < NX * NX; ++i) rec[L::A + i] = s[S::A + i];
+#pragma unroll
+  for (int i = 0; i < NX * NU; ++i) rec[L::B + i] = s[S::B + i];
+#pragma unroll
+  for (int i = 0; i < NX * NX; ++i) rec[L::Q + i] = w * s[S::Q + i];
+#pragma unroll
+  for (int i = 0; i < NU * NU; ++i) rec[L::R + i] = w * s[S::R + i];
+#pragma unroll
+  for (int i = 0; i < NU * NX; ++i) rec[L::M + i] = w * s[S::M + i];
+#pragma unroll
+  for (int i = 0; i < NX; ++i) rec[L::q + i] = w * ((Qx[i] + s[S::q + i]) + Mtu[i]);
+#pragma unroll
+  for (int i = 0; i < NU; ++i) rec[L::r + i] = w * ((Ru[i] + s[S::r + i]) + Mx[i]);
+  return all_finite<L::size>(rec);
+}
+
+// Constraint values only (multiplier update, solver.hpp:764-769).
+template <int NX, int NU>
+__device__ __forceinline__ int node_constraints(const ModelParams& mp, int node, bool leaf, const double* x,
+                                                const double* u, double* g) {
+  if constexpr (NX == 4 && NU == 2) {
+    if (mp.kind == kModelUnicycle) return ego_constraints<false>(mp, node, leaf, x, u, g, nullptr, nullptr);
+  }
+  return 0;
+}
+
+}  // namespace bmpc_b200

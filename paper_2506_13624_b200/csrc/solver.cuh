@@ -1,0 +1,810 @@
+// Device-resident MSiLQR-Tree + augmented-Lagrangian solve (the hot path of
+// bmpc::solve, solver.hpp:595-780), written once over an execution group:
+//   * CtaGroup  — one thread block solves one instance (small trees, batches;
+//                 barriers are __syncthreads, no host round trips);
+//   * GridGroup — every block of a cooperative launch solves ONE large
+//                 instance (barriers are grid.sync()).
+// Every decision the reference takes on the host (convergence, merit weight,
+// Armijo acceptance, Levenberg regularization, AL outer loop) is taken on
+// device from deterministic fixed-order reductions, so a solve is one kernel
+// launch.
+//
+// Backward pass = tree-segmented associative scan. The tree is cut into
+// segments (maximal single-child chains ending at a branch node or a leaf).
+// Depth levels are processed leaves-first; within a level all segments are
+// scanned concurrently with the reference's own work-efficient tree schedule
+// (scan.hpp:19-65). Leaf segments reproduce the reference P1 chain scan
+// exactly (lqr_scan.hpp:123-141 with the terminal appended); segments ending
+// at a branch node take the branch node's value from one Bellman step over
+// the summed children (riccati.hpp:97-122) as their terminal — this is where
+// the reference's sequential P2 becomes parallel. Forward pass = prefix scan
+// of the closed-loop affine maps of every segment at once (lqr_scan.hpp:
+// 177-187), then one depth sweep to apply them to the head perturbations.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "linalg.cuh"
+#include "lqr.cuh"
+#include "model.cuh"
+#include "types.h"
+
+namespace bmpc_b200 {
+
+namespace cg = cooperative_groups;
+
+constexpr int kRedSlots = 4 * kMaxAlpha;  // largest simultaneous reduction
+constexpr int kMaxWarps = 32;
+
+// Scan level bookkeeping (scan.hpp:19-36): n_0 = E, n_{l+1} = ceil(n_l / 2).
+__device__ __forceinline__ int level_size(int E, int l) {
+  int s = E;
+  for (int i = 0; i < l; ++i) s = (s + 1) >> 1;
+  return s;
+}
+__device__ __forceinline__ int level_offset(int E, int l) {
+  int off = 0, s = E;
+  for (int i = 0; i < l; ++i) {
+    off += s;
+    s = (s + 1) >> 1;
+  }
+  return off;
+}
+__host__ __device__ __forceinline__ int up_steps(int E) {
+  int u = 0;
+  for (int s = E; s >= 2; s = (s + 1) >> 1) ++u;
+  return u;
+}
+
+// ------------------------------------------------------------------ groups
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+struct RedSmem {
+  double part[kRedSlots][kMaxWarps];
+  double total[kRedSlots];
+  int flag;
+};
+
+// Reductions are two-stage and deterministic: warps butterfly-reduce (every
+// lane ends with the same bits) into per-warp slots; slots are then folded
+// in a fixed order. Slot k < nsum are sums, the rest maxima.
+struct CtaGroup {
+  RedSmem* sm;
+  __device__ int rank() const { return threadIdx.x; }
+  __device__ int size() const { return blockDim.x; }
+  __device__ bool leader() const { return threadIdx.x == 0; }
+  __device__ void sync() const { __syncthreads(); }
+  // Fold warp partials sm->part[0..nslot) into sm->total (all threads see it).
+  __device__ void finish(int nslot, int nsum) const {
+    __syncthreads();
+    const int nw = (blockDim.x + 31) >> 5;
+    for (int k = threadIdx.x; k < nslot; k += blockDim.x) {
+      double a = sm->part[k][0];
+      for (int w = 1; w < nw; ++w) a = k < nsum ? a + sm->part[k][w] : fmax(a, sm->part[k][w]);
+      sm->total[k] = a;
+    }
+    __syncthreads();
+  }
+};
+
+struct GridGroup {
+  RedSmem* sm;
+  double* scratch;  // [2][gridDim.x][kRedSlots] global partials (double-buffered)
+  int* parity;      // per-block private counter lives in smem via sm->flag
+  __device__ int rank() const { return blockIdx.x * blockDim.x + threadIdx.x; }
+  __device__ int size() const { return gridDim.x * blockDim.x; }
+  __device__ bool leader() const { return blockIdx.x == 0 && threadIdx.x == 0; }
+  __device__ void sync() const { cg::this_grid().sync(); }
+  __device__ void finish(int nslot, int nsum) const {
+    __syncthreads();
+    const int nw = (blockDim.x + 31) >> 5;
+    const int buf = sm->flag & 1;
+    double* out = scratch + (static_cast<size_t>(buf) * gridDim.x + blockIdx.x) * kRedSlots;
+    for (int k = threadIdx.x; k < nslot; k += blockDim.x) {
+      double a = sm->part[k][0];
+      for (int w = 1; w < nw; ++w) a = k < nsum ? a + sm->part[k][w] : fmax(a, sm->part[k][w]);
+      out[k] = a;
+    }
+    cg::this_grid().sync();
+    // Warp w folds slots w, w+nw, ... over blocks: lane-strided then butterfly.
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double* in = scratch + static_cast<size_t>(buf) * gridDim.x * kRedSlots;
+    for (int k = warp; k < nslot; k += nw) {
+      const bool is_sum = k < nsum;
+      double a = is_sum ? 0.0 : -INFINITY;
+      for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) {
+        const double v = in[static_cast<size_t>(b) * kRedSlots + k];
+        a = is_sum ? a + v : fmax(a, v);
+      }
+      a = is_sum ? warp_sum(a) : warp_max(a);
+      if (lane == 0) sm->total[k] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) sm->flag += 1;
+    __syncthreads();
+  }
+};
+
+// Contribute this thread's value to slot k (every thread of the block must call).
+__device__ __forceinline__ void red_put(RedSmem* sm, int k, double v, bool is_sum) {
+  v = is_sum ? warp_sum(v) : warp_max(v);
+  if ((threadIdx.x & 31) == 0) sm->part[k][threadIdx.x >> 5] = v;
+}
+
+// ------------------------------------------------------------------ solver
+template <int NX, int NU, class G>
+struct Solver {
+  using SL = StageLayout<NX, NU>;
+  using BL = BwdLayout<NX>;
+  using FL = FwdLayout<NX>;
+  using PL = PolicyLayout<NX, NU>;
+  using VL = ValueLayout<NX>;
+
+  G g;
+  const Topo& t;
+  const ModelParams& mp;
+  Work& w;
+  const DevOptions& o;
+  double g_rho{0.0};  // current AL penalty (uniform across the group)
+
+  __device__ Solver(G g_, const Topo& t_, const ModelParams& mp_, Work& w_, const DevOptions& o_)
+      : g(g_), t(t_), mp(mp_), w(w_), o(o_) {}
+
+  __device__ bool is_leaf(int i) const { return t.first_child[i] < 0; }
+  __device__ double* stage(int i) const { return w.stage + static_cast<size_t>(i) * SL::stride; }
+  __device__ double* bwd(int slot) const { return w.bwd + static_cast<size_t>(slot) * BL::stride; }
+  __device__ double* fwd(int slot) const { return w.fwd + static_cast<size_t>(slot) * FL::stride; }
+  __device__ double* pol(int i) const { return w.policy + static_cast<size_t>(i) * PL::stride; }
+  __device__ int seg_len(int s) const { return t.seg_off[s + 1] - t.seg_off[s]; }
+  __device__ int seg_node(int s, int k) const { return t.seg_nodes[t.seg_off[s] + k]; }
+
+  // Value of node i during/after the backward pass: slot (L-1-pos) of its
+  // segment's level-0 array (the reversed suffix scan).
+  __device__ const double* value_of(int i) const {
+    const int s = t.node_seg[i];
+    return bwd(t.seg_scratch[s] + seg_len(s) - 1 - t.node_pos[i]);
+  }
+
+  // ------------------------------------------------------ nonlinear rollout
+  // nonlinear_rollout (problem.hpp:150-166): one thread walks each segment;
+  // depth levels in order. Returns false on a non-finite state.
+  __device__ bool rollout() {
+    // Leaves carry no input (TrajectoryTree, tree.hpp:159-173).
+    for (int i = g.rank(); i < t.n; i += g.size()) {
+      if (is_leaf(i)) {
+#pragma unroll
+        for (int j = 0; j < NU; ++j) w.u[i * NU + j] = 0.0;
+      }
+    }
+    if (g.leader()) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) w.x[j] = w.x0[j];
+    }
+    g.sync();
+    double bad = 0.0;
+    for (int d = 0; d < t.ndepth; ++d) {
+      const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
+      for (int s = sb + g.rank(); s < se; s += g.size()) {
+        const int L = seg_len(s);
+        int prev = t.parent[seg_node(s, 0)];
+        for (int k = 0; k < L; ++k) {
+          const int i = seg_node(s, k);
+          if (prev >= 0) {
+            double xn[NX];
+            node_dynamics<NX, NU>(mp, prev, w.x + prev * NX, w.u + prev * NU, xn);
+            if (!all_finite<NX>(xn) && bad == 0.0) bad = prev + 1;
+            copy<NX>(xn, w.x + i * NX);
+          }
+          prev = i;
+        }
+      }
+      g.sync();
+    }
+    red_put(g.sm, 0, bad, false);
+    g.finish(1, 0);
+    if (g.sm->total[0] > 0.0) {
+      if (g.leader()) w.result->error_node = static_cast<int>(g.sm->total[0]) - 1;
+      return false;
+    }
+    return true;
+  }
+
+  // ---------------------------------------------- evaluate (problem.hpp:109)
+  // Sums into slots base..base+3: cost, cost_al, defect_l1 (sums), violation (max).
+  // With alpha >= 0 evaluates the trial x + alpha dx, u + alpha du.
+  __device__ void node_eval(int i, double alpha, double* c, double* cal, double* dl1, double* vmax,
+                            double* defect_out = nullptr) const {
+    const bool leaf = is_leaf(i);
+    double x[NX], u[NU];
+#pragma unroll
+    for (int j = 0; j < NX; ++j) x[j] = alpha > 0.0 ? fma(alpha, w.dx[i * NX + j], w.x[i * NX + j]) : w.x[i * NX + j];
+    if (!leaf) {
+#pragma unroll
+      for (int j = 0; j < NU; ++j)
+        u[j] = alpha > 0.0 ? fma(alpha, w.du[i * NU + j], w.u[i * NU + j]) : w.u[i * NU + j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < NU; ++j) u[j] = 0.0;
+    }
+    double nc, pen, gm;
+    node_cost<NX, NU>(mp, i, leaf, x, u, w.eta + static_cast<size_t>(i) * t.max_con, g_rho, &nc, &pen, &gm);
+    const double wi = t.weight[i];
+    *c = wi * nc;
+    *cal = wi * (nc + pen);
+    *vmax = gm;
+    *dl1 = 0.0;
+    const int p = t.parent[i];
+    if (p >= 0) {
+      double xp[NX], up[NU], f[NX];
+#pragma unroll
+      for (int j = 0; j < NX; ++j)
+        xp[j] = alpha > 0.0 ? fma(alpha, w.dx[p * NX + j], w.x[p * NX + j]) : w.x[p * NX + j];
+#pragma unroll
+      for (int j = 0; j < NU; ++j)
+        up[j] = alpha > 0.0 ? fma(alpha, w.du[p * NU + j], w.u[p * NU + j]) : w.u[p * NU + j];
+      node_dynamics<NX, NU>(mp, p, xp, up, f);
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < NX; ++j) {
+        const double dj = f[j] - x[j];
+        if (defect_out) defect_out[j] = dj;
+        s += fabs(dj);
+      }
+      *dl1 = s;
+    } else if (defect_out) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) defect_out[j] = 0.0;
+    }
+  }
+
+  struct Eval {
+    double cost, cost_al, defect_l1, max_violation;
+  };
+
+  __device__ Eval evaluate_current() {
+    double c = 0, cal = 0, dl = 0, vm = -INFINITY;
+    for (int i = g.rank(); i < t.n; i += g.size()) {
+      double a, b, d, v;
+      node_eval(i, 0.0, &a, &b, &d, &v);
+      c += a;
+      cal += b;
+      dl += d;
+      vm = fmax(vm, v);
+    }
+    red_put(g.sm, 0, c, true);
+    red_put(g.sm, 1, cal, true);
+    red_put(g.sm, 2, dl, true);
+    red_put(g.sm, 3, vm, false);
+    g.finish(4, 3);
+    return {g.sm->total[0], g.sm->total[1], g.sm->total[2], fmax(g.sm->total[3], 0.0)};
+  }
+
+  // ------------------------------------ linearize + evaluate (fused, Phase L)
+  // Returns the nominal evaluation; sets *bad_node (1-based) on a non-finite
+  // expansion or defect (linearize throws there, solver.hpp:106-146).
+  __device__ Eval linearize_evaluate(int* bad_node) {
+    double c = 0, cal = 0, dl = 0, vm = -INFINITY, bad = 0;
+    for (int i = g.rank(); i < t.n; i += g.size()) {
+      const bool leaf = is_leaf(i);
+      const double* eta = w.eta + static_cast<size_t>(i) * t.max_con;
+      const bool ok = node_linearize<NX, NU>(mp, i, leaf, t.weight[i], w.x + i * NX, w.u + i * NU, eta, g_rho,
+                                             stage(i));
+      double a, b, d, v;
+      // Nominal evaluate terms and the edge defect parent -> i
+      // (models.defect, solver.hpp:138-147) from one dynamics evaluation.
+      node_eval(i, 0.0, &a, &b, &d, &v, w.defect + i * NX);
+      c += a;
+      cal += b;
+      dl += d;
+      vm = fmax(vm, v);
+      const bool dok = all_finite<NX>(w.defect + i * NX);
+      if (!(ok && dok) && bad == 0) bad = i + 1;
+    }
+    red_put(g.sm, 0, c, true);
+    red_put(g.sm, 1, cal, true);
+    red_put(g.sm, 2, dl, true);
+    red_put(g.sm, 3, vm, false);
+    red_put(g.sm, 4, bad, false);
+    g.finish(5, 3);
+    *bad_node = static_cast<int>(g.sm->total[4]);
+    return {g.sm->total[0], g.sm->total[1], g.sm->total[2], fmax(g.sm->total[3], 0.0)};
+  }
+
+  // ------------------------------------------------ tree scan machinery
+  // Items of a per-segment phase over the segments of one depth level.
+  template <class F>
+  __device__ void for_depth_items(int d, int per_seg, F&& f) const {
+    const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
+    const int total = (se - sb) * per_seg;
+    for (int q = g.rank(); q < total; q += g.size()) f(sb + q / per_seg, q % per_seg);
+  }
+
+  // Backward suffix scan of segments at depth d, elements already in level 0
+  // (reversed). f(a, b) = combine_bwd(first = b, second = a).
+  __device__ int scan_bwd_depth(int d) {
+    const int E = t.depth_len[d];
+    const int U = up_steps(E);
+    int err = kBwdOk;
+    for (int l = 0; l < U; ++l) {
+      const int nl = level_size(E, l), nn = (nl + 1) >> 1;
+      const int ol = level_offset(E, l), on = ol + nl;
+      for_depth_items(d, nn, [&](int s, int i) {
+        const int base = t.seg_scratch[s];
+        double* dst = bwd(base + on + i);
+        if (2 * i + 1 < nl) {
+          double res[BL::size];
+          const int e = combine_bwd<NX>(bwd(base + ol + 2 * i + 1), bwd(base + ol + 2 * i), res);
+          err = err ? err : e;
+          copy<BL::size>(res, dst);
+        } else {
+          copy<BL::size>(bwd(base + ol + 2 * i), dst);
+        }
+      });
+      g.sync();
+    }
+    for (int l = U - 1; l >= 0; --l) {
+      const int nl = level_size(E, l), nn = (nl + 1) >> 1;
+      const int ol = level_offset(E, l), on = ol + nl;
+      for_depth_items(d, nn, [&](int s, int i) {
+        const int base = t.seg_scratch[s];
+        const double* S = bwd(base + on);
+        if (2 * i + 1 < nl) copy<BL::size>(S + static_cast<size_t>(i) * BL::stride, bwd(base + ol + 2 * i + 1));
+        if (i >= 1) {
+          double res[BL::size];
+          double* a = bwd(base + ol + 2 * i);
+          const int e = combine_bwd<NX>(a, S + static_cast<size_t>(i - 1) * BL::stride, res);
+          err = err ? err : e;
+          copy<BL::size>(res, a);
+        }
+      });
+      g.sync();
+    }
+    return err;
+  }
+
+  // ---------------------------------------------------- backward pass (B)
+  // backward_pass (solver.hpp:203-318) with Levenberg shift `reg` on R
+  // (non-leaves) and P (leaves). Returns error code and max_feedforward.
+  __device__ int backward(double reg, double* max_ff) {
+    int err = kBwdOk;
+    for (int d = t.ndepth - 1; d >= 0; --d) {
+      const int L = t.depth_len[d];
+      // Terminal of each segment: regularized leaf cost or the branch-node
+      // Bellman step over the summed children (riccati.hpp:107-120).
+      for_depth_items(d, 1, [&](int s, int) {
+        const int b = seg_node(s, L - 1);
+        double* term = bwd(t.seg_scratch[s] + 0);
+        double P[NX * NX], p[NX];
+        if (is_leaf(b)) {
+          copy<NX * NX>(stage(b) + SL::Q, P);
+          copy<NX>(stage(b) + SL::q, p);
+#pragma unroll
+          for (int j = 0; j < NX; ++j) P[j + j * NX] += reg;
+        } else {
+          double Pn[NX * NX], pn[NX];
+#pragma unroll
+          for (int j = 0; j < NX * NX; ++j) Pn[j] = 0.0;
+#pragma unroll
+          for (int j = 0; j < NX; ++j) pn[j] = 0.0;
+          const int c0 = t.first_child[b], nc = t.nchild[b];
+          for (int ch = c0; ch < c0 + nc; ++ch) {
+            const double* v = value_of(ch);
+            double Pd[NX];
+            mv<NX, NX>(v + BL::P, w.defect + ch * NX, Pd);
+#pragma unroll
+            for (int j = 0; j < NX * NX; ++j) Pn[j] += v[BL::P + j];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) pn[j] += v[BL::p + j] + Pd[j];
+          }
+          const int e = riccati_step<NX, NU>(stage(b), reg, Pn, pn, P, p, pol(b) + PL::K, pol(b) + PL::k);
+          err = err ? err : e;
+        }
+        embed_terminal<NX>(P, p, term);
+      });
+      // One-step elements of the chain nodes (chain_stage, solver.hpp:189-193:
+      // offset = defect of the next node), stored reversed.
+      if (L >= 2) {
+        for_depth_items(d, L - 1, [&](int s, int k) {
+          const int i = seg_node(s, k), nxt = seg_node(s, k + 1);
+          const int e = init_bwd_element<NX, NU>(stage(i), reg, w.defect + nxt * NX,
+                                                  bwd(t.seg_scratch[s] + L - 1 - k));
+          err = err ? err : e;
+        });
+      }
+      g.sync();
+      const int e = scan_bwd_depth(d);
+      err = err ? err : e;
+    }
+    // Policies of chain nodes from their successor's value (lqr_scan.hpp:146).
+    double mff = 0.0;
+    for (int i = g.rank(); i < t.n; i += g.size()) {
+      if (is_leaf(i)) continue;
+      const int s = t.node_seg[i], k = t.node_pos[i];
+      if (k + 1 < seg_len(s)) {
+        const int nxt = seg_node(s, k + 1);
+        const double* v = value_of(nxt);
+        const int e = feedback<NX, NU>(stage(i), reg, w.defect + nxt * NX, v + BL::P, v + BL::p, pol(i) + PL::K,
+                                       pol(i) + PL::k);
+        err = err ? err : e;
+      }
+      double m = 0.0;
+#pragma unroll
+      for (int j = 0; j < NU; ++j) m = fmax(m, fabs(pol(i)[PL::k + j]));
+      mff = fmax(mff, m);
+    }
+    red_put(g.sm, 0, mff, false);
+    red_put(g.sm, 1, static_cast<double>(err), false);
+    g.finish(2, 0);
+    *max_ff = g.sm->total[0];
+    return static_cast<int>(g.sm->total[1]);
+  }
+
+  // --------------------------------------------------- forward pass (F)
+  // linear_rollout (solver.hpp:330-387) + expected_change_coefficients
+  // (:412-430) fused. Returns (a1, a2).
+  __device__ void forward(double* a1_out, double* a2_out) {
+    // Elements of every segment at every depth at once.
+    for (int d = 0; d < t.ndepth; ++d) {
+      const int L = t.depth_len[d];
+      if (L < 2) continue;
+      for_depth_items(d, L - 1, [&](int s, int k) {
+        const int i = seg_node(s, k), nxt = seg_node(s, k + 1);
+        init_fwd_element<NX, NU>(stage(i), w.defect + nxt * NX, pol(i) + PL::K, pol(i) + PL::k,
+                                 fwd(t.seg_scratch[s] + k));
+      });
+    }
+    g.sync();
+    // Prefix scans (scan.hpp:19-50), all depths in the same phases.
+    int maxU = 0;
+    for (int d = 0; d < t.ndepth; ++d) maxU = max(maxU, up_steps(t.depth_len[d] - 1));
+    for (int l = 0; l < maxU; ++l) {
+      for (int d = 0; d < t.ndepth; ++d) {
+        const int E = t.depth_len[d] - 1;
+        if (l >= up_steps(E)) continue;
+        const int nl = level_size(E, l), nn = (nl + 1) >> 1;
+        const int ol = level_offset(E, l), on = ol + nl;
+        for_depth_items(d, nn, [&](int s, int i) {
+          const int base = t.seg_scratch[s];
+          if (2 * i + 1 < nl)
+            combine_fwd<NX>(fwd(base + ol + 2 * i), fwd(base + ol + 2 * i + 1), fwd(base + on + i));
+          else
+            copy<FL::size>(fwd(base + ol + 2 * i), fwd(base + on + i));
+        });
+      }
+      g.sync();
+    }
+    for (int l = maxU - 1; l >= 0; --l) {
+      for (int d = 0; d < t.ndepth; ++d) {
+        const int E = t.depth_len[d] - 1;
+        if (l >= up_steps(E)) continue;
+        const int nl = level_size(E, l), nn = (nl + 1) >> 1;
+        const int ol = level_offset(E, l), on = ol + nl;
+        for_depth_items(d, nn, [&](int s, int i) {
+          const int base = t.seg_scratch[s];
+          const double* S = fwd(base + on);
+          if (2 * i + 1 < nl) copy<FL::size>(S + static_cast<size_t>(i) * FL::stride, fwd(base + ol + 2 * i + 1));
+          if (i >= 1) {
+            double* a = fwd(base + ol + 2 * i);
+            combine_fwd<NX>(S + static_cast<size_t>(i - 1) * FL::stride, a, a);
+          }
+        });
+      }
+      g.sync();
+    }
+    // Depth sweep: head perturbation from the parent's closed loop, then the
+    // scanned maps; du = K dx + k and the EC terms per node.
+    double a1 = 0.0, a2 = 0.0;
+    for (int d = 0; d < t.ndepth; ++d) {
+      const int L = t.depth_len[d];
+      for_depth_items(d, L, [&](int s, int k) {
+        const int head = seg_node(s, 0);
+        const int p = t.parent[head];
+        double h[NX];
+        if (p < 0) {
+#pragma unroll
+          for (int j = 0; j < NX; ++j) h[j] = w.x0[j] - w.x[j];
+        } else {
+          // Acl = A + B K ; dx_ch = Acl dx_p + B k + defect_ch (solver.hpp:344-348)
+          const double* sp = stage(p);
+          double BK[NX * NX], Acl[NX * NX], Bk[NX], t1[NX];
+          mm<NX, NU, NX>(sp + SL::B, pol(p) + PL::K, BK);
+#pragma unroll
+          for (int j = 0; j < NX * NX; ++j) Acl[j] = sp[SL::A + j] + BK[j];
+          mv<NX, NU>(sp + SL::B, pol(p) + PL::k, Bk);
+          mv<NX, NX>(Acl, w.dx + p * NX, t1);
+#pragma unroll
+          for (int j = 0; j < NX; ++j) h[j] = (t1[j] + Bk[j]) + w.defect[head * NX + j];
+        }
+        const int i = seg_node(s, k);
+        double dxi[NX];
+        if (k == 0) {
+          copy<NX>(h, dxi);
+        } else {
+          const double* F = fwd(t.seg_scratch[s] + k - 1);
+          double t1[NX];
+          mv<NX, NX>(F + FL::A, h, t1);
+#pragma unroll
+          for (int j = 0; j < NX; ++j) dxi[j] = t1[j] + F[FL::c + j];
+        }
+        copy<NX>(dxi, w.dx + i * NX);
+        const double* si = stage(i);
+        double Qdx[NX];
+        mv<NX, NX>(si + SL::Q, dxi, Qdx);
+        if (is_leaf(i)) {
+          a1 += dot<NX>(si + SL::q, dxi);
+          a2 += 0.5 * dot<NX>(dxi, Qdx);
+        } else {
+          double dui[NU], Mdx[NU], Rdu[NU];
+          mv<NU, NX>(pol(i) + PL::K, dxi, dui);
+#pragma unroll
+          for (int j = 0; j < NU; ++j) dui[j] += pol(i)[PL::k + j];
+          copy<NU>(dui, w.du + i * NU);
+          mv<NU, NX>(si + SL::M, dxi, Mdx);
+          mv<NU, NU>(si + SL::R, dui, Rdu);
+          a1 += dot<NX>(si + SL::q, dxi) + dot<NU>(si + SL::r, dui);
+          a2 += (0.5 * dot<NX>(dxi, Qdx) + dot<NU>(dui, Mdx)) + 0.5 * dot<NU>(dui, Rdu);
+        }
+      });
+      g.sync();
+    }
+    red_put(g.sm, 0, a1, true);
+    red_put(g.sm, 1, a2, true);
+    g.finish(2, 2);
+    *a1_out = g.sm->total[0];
+    *a2_out = g.sm->total[1];
+  }
+
+  // ------------------------------------------------- line search (S)
+  // Parallel line search (solver.hpp:459-518): every alpha evaluated, sums in
+  // slots [4l .. 4l+3]; returns the first accepted level or -1.
+  __device__ int line_search(int levels, double merit0, double a1, double a2, double mu, double dl1_nom,
+                             Eval* chosen, double* merit_chosen, double* decrease_chosen) {
+    for (int l = 0; l < levels; ++l) {
+      const double alpha = ldexp(1.0, -l);
+      double c = 0, cal = 0, dl = 0, vm = -INFINITY;
+      for (int i = g.rank(); i < t.n; i += g.size()) {
+        double a, b, d, v;
+        node_eval(i, alpha, &a, &b, &d, &v);
+        c += a;
+        cal += b;
+        dl += d;
+        vm = fmax(vm, v);
+      }
+      red_put(g.sm, 3 * l + 0, c, true);
+      red_put(g.sm, 3 * l + 1, cal, true);
+      red_put(g.sm, 3 * l + 2, dl, true);
+      red_put(g.sm, 3 * levels + l, vm, false);
+    }
+    g.finish(4 * levels, 3 * levels);
+    for (int l = 0; l < levels; ++l) {
+      const double alpha = ldexp(1.0, -l);
+      const double cal = g.sm->total[3 * l + 1], dl = g.sm->total[3 * l + 2];
+      const bool finite = isfinite(cal) && isfinite(dl);
+      const double m = finite ? cal + mu * dl : INFINITY;
+      const double ec = a1 * alpha + a2 * alpha * alpha;
+      const double dec = o.armijo_beta * (ec - alpha * mu * dl1_nom);
+      if (isfinite(m) && m <= merit0 + dec) {
+        *chosen = {g.sm->total[3 * l + 0], cal, dl, fmax(g.sm->total[3 * levels + l], 0.0)};
+        *merit_chosen = m;
+        *decrease_chosen = dec;
+        return l;
+      }
+    }
+    return -1;
+  }
+
+  __device__ void take_step(double alpha) {
+    for (int i = g.rank(); i < t.n; i += g.size()) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) w.x[i * NX + j] = fma(alpha, w.dx[i * NX + j], w.x[i * NX + j]);
+      if (!is_leaf(i)) {
+#pragma unroll
+        for (int j = 0; j < NU; ++j) w.u[i * NU + j] = fma(alpha, w.du[i * NU + j], w.u[i * NU + j]);
+      }
+    }
+    g.sync();
+  }
+
+  // Projected multiplier update (solver.hpp:764-769).
+  __device__ void update_multipliers(double rho) {
+    for (int i = g.rank(); i < t.n; i += g.size()) {
+      double gv[kMaxCon];
+      const int nc = node_constraints<NX, NU>(mp, i, is_leaf(i), w.x + i * NX, w.u + i * NU, gv);
+      double* eta = w.eta + static_cast<size_t>(i) * t.max_con;
+      for (int m = 0; m < nc; ++m) eta[m] = fmax(eta[m] + rho * gv[m], 0.0);
+    }
+    g.sync();
+  }
+
+  __device__ static double now_s() {
+    unsigned long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    return static_cast<double>(ns) * 1e-9;
+  }
+
+  // ------------------------------------------------------------- solve
+  __device__ void solve() {
+    const double t_start = now_s();
+    double times[6] = {0, 0, 0, 0, 0, 0};
+    DevResult* res = w.result;
+    if (g.leader()) {
+      res->status = kError;
+      res->error_code = kErrNone;
+      res->error_node = -1;
+      res->inner_iterations = 0;
+      res->outer_iterations = 0;
+      res->n_records = 0;
+    }
+    if (o.alpha_levels < 1 || o.alpha_levels > kMaxAlpha) {
+      if (g.leader()) res->error_code = kErrAlphaLevels;
+      return;
+    }
+    // eta = 0; the caller filled w.u with the initial inputs.
+    for (int i = g.rank(); i < t.n * t.max_con; i += g.size()) w.eta[i] = 0.0;
+    g_rho = o.penalty_init;
+    if (!rollout()) {
+      if (g.leader()) res->error_code = kErrRolloutNonfinite;
+      return;
+    }
+    double mu = o.merit_mu_init;
+    double reg = o.reg_init;
+    bool inner_converged = false, failed = false;
+    int status = kError, err_code = kErrNone, err_node = -1;
+    int inner = 0, outer_count = 0, nrec = 0;
+
+    for (int outer = 0; outer < o.max_outer_iterations; ++outer) {
+      ++outer_count;
+      inner_converged = false;
+      for (int pass = 0; pass < o.max_inner_iterations; ++pass) {
+        double t0 = now_s();
+        int bad = 0;
+        const Eval ev = linearize_evaluate(&bad);
+        if (bad) {
+          err_code = kErrLinearizeNonfinite;
+          err_node = bad - 1;
+          failed = true;
+          break;
+        }
+        double t1 = now_s();
+        times[0] += t1 - t0;
+        double max_ff = 0.0;
+        const int berr = backward(reg, &max_ff);
+        double t2 = now_s();
+        times[1] += t2 - t1;
+        if (berr != kBwdOk) {
+          reg = fmax(reg * o.reg_growth, o.reg_min);
+          if (reg > o.reg_max) {
+            err_code = berr == kIndefinite ? kErrRegCap : kErrFactorization;
+            failed = true;
+            break;
+          }
+          continue;
+        }
+        double a1, a2;
+        forward(&a1, &a2);
+        double t3 = now_s();
+        times[3] += t3 - t2;
+        const double ec_full = a1 + a2;
+        if (ev.defect_l1 <= o.tol_defect && fabs(ec_full) <= o.tol_cost * (1.0 + fabs(ev.cost_al)) &&
+            max_ff <= o.tol_feedforward) {
+          inner_converged = true;
+          break;
+        }
+        // update_mu (solver.hpp:400-407)
+        {
+          double trial = mu;
+          if (ev.defect_l1 > o.defect_epsilon) trial = ec_full / ((1.0 - o.merit_gamma) * ev.defect_l1) + o.merit_mu0;
+          mu = fmax(trial, mu);
+        }
+        const double merit0 = ev.cost_al + mu * ev.defect_l1;
+        Eval after;
+        double merit_after = 0.0, dec = 0.0;
+        const int lvl = line_search(o.alpha_levels, merit0, a1, a2, mu, ev.defect_l1, &after, &merit_after, &dec);
+        double t4 = now_s();
+        times[4] += t4 - t3;
+        DevRecord rec;
+        rec.outer = outer;
+        rec.merit_before = merit0;
+        rec.mu = mu;
+        rec.max_feedforward = max_ff;
+        rec.regularization = reg;
+        rec.accepted = lvl >= 0 ? 1 : 0;
+        rec.alpha = lvl >= 0 ? ldexp(1.0, -lvl) : 0.0;
+        rec.model_decrease = lvl >= 0 ? dec : 0.0;
+        if (lvl < 0) {
+          reg = fmax(reg * o.reg_growth, o.reg_min);
+          rec.merit_after = merit0;
+          rec.cost = ev.cost;
+          rec.cost_al = ev.cost_al;
+          rec.defect_l1 = ev.defect_l1;
+          rec.violation = ev.max_violation;
+          if (g.leader() && nrec < w.max_records) w.records[nrec] = rec;
+          ++nrec;
+          if (reg > o.reg_max) {
+            err_code = kErrLineSearch;
+            failed = true;
+            break;
+          }
+          continue;
+        }
+        take_step(rec.alpha);
+        reg = reg / o.reg_decay >= o.reg_min ? reg / o.reg_decay : 0.0;
+        ++inner;
+        rec.merit_after = merit_after;
+        rec.cost = after.cost;
+        rec.cost_al = after.cost_al;
+        rec.defect_l1 = after.defect_l1;
+        rec.violation = after.max_violation;
+        if (g.leader() && nrec < w.max_records) w.records[nrec] = rec;
+        ++nrec;
+      }
+      if (failed) break;
+      const Eval ev = evaluate_current();
+      if (!t.has_constraints) {
+        status = inner_converged ? kConverged : kMaxIterations;
+        break;
+      }
+      if (inner_converged && ev.max_violation <= o.tol_constraint) {
+        status = kConverged;
+        break;
+      }
+      if (outer + 1 == o.max_outer_iterations) {
+        status = kMaxIterations;
+        break;
+      }
+      update_multipliers(g_rho);
+      g_rho = fmin(g_rho * o.penalty_growth, o.penalty_max);
+    }
+    const Eval fin = evaluate_current();
+    times[5] = now_s() - t_start;
+    if (g.leader()) {
+      res->status = failed ? kError : status;
+      res->error_code = err_code;
+      res->error_node = err_node;
+      res->inner_iterations = inner;
+      res->outer_iterations = outer_count;
+      res->n_records = nrec;
+      res->final_cost = fin.cost;
+      res->final_violation = fin.max_violation;
+      res->final_defect_l1 = fin.defect_l1;
+      for (int k = 0; k < 6; ++k) res->times[k] = times[k];
+      res->final_penalty = g_rho;
+      res->final_mu = mu;
+      res->final_reg = reg;
+    }
+  }
+
+  // Kernel-level LQR-tree entry (tests): stage records / defects already in
+  // place; backward + forward + EC, values copied out.
+  __device__ void lqr_tree(double reg, double* scalars) {
+    double max_ff = 0.0;
+    const int err = backward(reg, &max_ff);
+    if (w.value) {
+      for (int i = g.rank(); i < t.n; i += g.size()) {
+        const double* v = value_of(i);
+        copy<NX * NX>(v + BL::P, w.value + static_cast<size_t>(i) * VL::stride + VL::P);
+        copy<NX>(v + BL::p, w.value + static_cast<size_t>(i) * VL::stride + VL::p);
+      }
+    }
+    g.sync();
+    double a1 = 0, a2 = 0;
+    if (err == kBwdOk) forward(&a1, &a2);
+    if (g.leader()) {
+      scalars[0] = max_ff;
+      scalars[1] = a1;
+      scalars[2] = a2;
+      scalars[3] = err;
+    }
+  }
+};
+
+}  // namespace bmpc_b200
