@@ -494,7 +494,8 @@ std::unique_ptr<Plan> make_plan(const bmpc_tree& t, int max_con, bool has_constr
     }
     pl->seg_off.push_back(static_cast<int>(pl->seg_nodes.size()));
     pl->seg_scratch.push_back(scratch);
-    scratch += 2 * L;
+    // Scan levels n_0 = L, n_{l+1} = ceil(n_l/2): total <= 2L + (#levels).
+    scratch += 2 * L + 32;
   }
   for (int d = 1; d <= pl->ndepth; ++d)
     pl->depth_begin[static_cast<size_t>(d)] = std::max(pl->depth_begin[static_cast<size_t>(d)],

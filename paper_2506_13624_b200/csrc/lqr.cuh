@@ -318,7 +318,7 @@ __device__ void init_fwd_element(const double* s, const double* c, const double*
 
 // combine_fwd (lqr_scan.hpp:171-173): (A2 A1, A2 c1 + c2).
 template <int NX>
-__device__ void combine_fwd(const double* __restrict__ f1, const double* __restrict__ f2, double* __restrict__ out) {
+__device__ void combine_fwd(const double* f1, const double* f2, double* out) {  // out may alias f2
   using F = FwdLayout<NX>;
   double A[NX * NX], c[NX];
   mm<NX, NX, NX>(f2 + F::A, f1 + F::A, A);
