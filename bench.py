@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark: batched branch-MPC solves/sec (BASELINE.json configs[4]).
+
+Workload (one "step"): 4096 independent instances of the paper's
+intersection case (cfg0: build_intersection_case(intersection_spec(63, 10.0,
+0.1), 2, 2), 250 nodes) PER GPU, instance i's measured state perturbed with
+std::mt19937_64(42 + global index) — solved to convergence with the default
+pmsilqr options by ONE kernel launch per GPU (one thread block per instance).
+`value` = solves/sec of the whole job (all ranks; weak scaling), inputs
+resident in HBM. `e2e` = the same through the public batch API with host
+buffers: H2D of every instance's problem data, solve, D2H of trajectories and
+reports inside the timed region. For N > 1 ranks the step ends with the
+north star's final gather of all trajectories to rank 0 over NVLink (NCCL).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`--impl reference` times the reference's own CPU solver (oracle/_ref, the
+unmodified headers compiled against the Eigen shim) on all host threads over
+a bounded sample of the same instances (rank 0 only).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "BMPC solve latency (ms) vs horizon×scenarios; batched solves/sec at 1/2/4/8 GPU"
+UNIT = "solves/s"
+WORKLOAD = "cfg4: batched intersection_spec(63,10,0.1) 2x2 (250 nodes) x 4096 instances per GPU, perturbed x0"
+PER_GPU = 4096
+# Algorithmic work per non-leaf node per inner iteration:
+# linearize 1.575 + init 0.4 + 2 combines 3.0 + feedback 0.35 + fwd 0.482
+# + EC 0.086 + evaluate x2 0.4 + line search 11 x 0.212 = 8.6 kflop.
+F_NODE = 8.6e3
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--instances", type=int, default=PER_GPU)
+    ap.add_argument("--no-latency", action="store_true", help="skip the single-solve latency table")
+    ap.add_argument("--ref-sample", type=int, default=0, help="reference sample size (0 = auto)")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if len(s) > 2 + k and "Active" in s[2 + k]
+                          and "Not" not in s[2 + k]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def build_problems(B, rank, count):
+    spec = B.intersection_spec(63, 10.0, 0.1)
+    return [B.build_intersection_case(spec, 2, 2, perturb_seed=42 + rank * count + i) for i in range(count)]
+
+
+def cpu_reference(sample, threads, seed0=42):
+    """Reference CPU solver (oracle/_ref) over `sample` perturbed cfg0
+    instances on `threads` host threads; returns (solves/s, seconds)."""
+    import ctypes as C
+
+    import _refbind as R
+
+    sc = R.scenario(0, 63, perturb_seed=seed0)
+    o = R.default_options()
+    o.parallel = 0  # one solve per thread (bench.cpp:259-269 parallel_sweep pattern)
+    secs, conv, inner = C.c_double(), C.c_int(), C.c_longlong()
+    rc = R.lib().ref_batch_solve(C.byref(sc), C.byref(o), int(sample), int(threads), C.byref(secs),
+                                 C.byref(conv), C.byref(inner))
+    if rc != 0:
+        raise RuntimeError(R.lib().ref_last_error().decode())
+    return sample / secs.value, secs.value, conv.value
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    sample = args.ref_sample or max(2 * threads, 32)
+    for _ in range(args.warmup):
+        cpu_reference(min(sample, threads), threads)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, _, _ = cpu_reference(sample, threads)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference scenario builders, seeded perturbations)",
+            "config": {"workload": WORKLOAD, "sample_instances_per_step": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"{sample} perturbed cfg0 instances per step, solve() with parallel=false "
+                                       f"on {threads} std::threads"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2506_13624_b200 as B
+
+    # A dedicated (non-default) stream shared by torch events and the solver.
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = B.Context(local, stream=stream.cuda_stream)
+    count = args.instances
+    probs = build_problems(B, rank, count)
+    batch = B.Batch(ctx, probs)
+    n, nx, nu = batch.n, batch.nx, batch.nu
+    h2d_setup = batch.set_models()
+    torch.cuda.synchronize()
+    gather_buf = torch.empty(count * n * (nx + nu), dtype=torch.float64, device="cuda") if world > 1 else None
+    recv = [torch.empty_like(gather_buf) for _ in range(world)] if (world > 1 and rank == 0) else None
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step():
+        batch.solve()
+        if world > 1:  # final gather of every trajectory to rank 0 over NVLink
+            batch.pack_results(gather_buf.data_ptr())
+            dist.gather(gather_buf, recv, dst=0)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for s in range(args.steps):
+            kev[s][0].record(stream)
+            batch.solve()
+            kev[s][1].record(stream)
+            if world > 1:
+                batch.pack_results(gather_buf.data_ptr())
+                dist.gather(gather_buf, recv, dst=0)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.launches - launches0
+    elapsed = ev0.elapsed_time(ev1) / 1e3
+    kernel_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+    t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed = float(t.item())
+    value = world * count * args.steps / elapsed
+
+    reps, _ = batch.results(want_reports=True)
+    status = np.array([r.status for r in reps])
+    passes = np.array([r.n_records + r.outer_iterations for r in reps])
+    nl = int((probs[0].tree.child_count > 0).sum())
+    flops_per_launch = F_NODE * nl * float(passes.sum())
+
+    # e2e: public API with host buffers, copies inside the timed region.
+    xh = np.empty((count, n, nx))
+    uh = np.empty((count, n, nu))
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h2d = d2h = 0
+    for _ in range(e2e_steps):
+        h2d = batch.set_models()
+        batch.solve()
+        _, d2h = batch.results(xh, uh, want_reports=True)
+    e2e_el = time.perf_counter() - t0
+    te = torch.tensor([e2e_el], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * count * e2e_steps / float(te.item())
+
+    if rank == 0:
+        peak = B.fp64_peak_tflops(ctx)
+        achieved = flops_per_launch / (kernel_ms * 1e-3) / 1e12
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (in-library scenario builders, bit-identical to the reference's; seeded x0 "
+                    "perturbations)",
+            "config": {"workload": WORKLOAD, "instances_per_gpu": count, "nodes_per_instance": n,
+                       "nonleaf_nodes": nl, "parallelism": f"dp{world} (independent instances, final NCCL gather)",
+                       "l2": "per-step working set %.0f MB > 126 MB L2 (no flush needed)" %
+                             (count * batch_bytes(n, nx, nu) / 1e6),
+                       "converged": int((status == 0).sum()), "mean_inner_passes": float(passes.mean())},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "peak_source": "measured DFMA microbenchmark (bmpc_fp64_peak_tflops)",
+                         "kernel_ms": kernel_ms,
+                         "algorithmic_flops_per_launch": flops_per_launch},
+            "clocks": clocks.summary(),
+        }
+        if world == 1:
+            threads = os.cpu_count() or 1
+            sample = max(threads, 16)
+            try:
+                v, secs, _ = cpu_reference(sample, threads)
+                line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                                        "sample": f"{sample} perturbed cfg0 instances, reference solve() "
+                                                  f"(parallel=false) on {threads} threads, {secs:.1f} s"}
+            except Exception as e:  # reference library absent
+                line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                                        "sample": f"unavailable: {e}"}
+            if not args.no_latency:
+                line["latency_ms"] = latency_table(B, ctx)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def batch_bytes(n, nx, nu):
+    # state + scratch per instance, approximate (doubles)
+    return 8 * n * (nx + nu + 8 + 58 + nx + 12 + 2 * 56 + 2 * 20 + nx + nu + 20) * 1.0
+
+
+def latency_table(B, ctx):
+    """Single-solve device latency for configs 0, 1 (N sweep), 3 (kernel time
+    of the one solve launch, inputs resident)."""
+    import torch
+    cases = [("cfg0 N=63 4 leaves", B.intersection_spec(63, 10.0, 0.1), "int"),
+             ("cfg1 N=500 4 leaves", B.intersection_spec(500, 10.0, 0.1), "int"),
+             ("cfg1 N=1000 4 leaves", B.intersection_spec(1000, 10.0, 0.1), "int"),
+             ("cfg3 N=500 256 leaves {1,100,200,300}", B.multistage_spec(500, [(1, 4), (100, 4), (200, 4), (300, 4)]),
+              "ms")]
+    out = {}
+    for name, spec, kind in cases:
+        p = B.build_intersection_case(spec, 2, 2) if kind == "int" else B.build_multistage_case(spec)
+        bt = B.Batch(ctx, [p])
+        bt.set_models()
+        bt.solve()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s = torch.cuda.current_stream()
+        e0.record(s)
+        bt.solve()
+        e1.record(s)
+        torch.cuda.synchronize()
+        rep, _ = bt.results(want_reports=True)
+        out[name] = {"ms": e0.elapsed_time(e1), "nodes": p.tree.node_count, "status": rep[0].status_name,
+                     "inner": rep[0].inner_iterations, "outer": rep[0].outer_iterations}
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -178,6 +178,9 @@ void bmpc_batch_destroy(bmpc_batch* batch);
 int bmpc_batch_set_models(bmpc_batch* batch, const bmpc_model_desc* models, size_t* h2d_bytes);
 /* Device-to-device replication of instance 0's data into all instances. */
 int bmpc_batch_replicate(bmpc_batch* batch);
+/* Per-instance thread-block shape: `threads` per block with at least
+ * `min_blocks` resident per SM (compiled variants only). */
+int bmpc_batch_set_launch(bmpc_batch* batch, int threads, int min_blocks);
 /* Launch the solve of every instance (async on the ctx stream). */
 int bmpc_batch_solve(bmpc_batch* batch, const bmpc_options* opts);
 /* Device -> host copy of results and synchronize. Any pointer may be NULL.
@@ -186,10 +189,18 @@ int bmpc_batch_results(bmpc_batch* batch, double* x_out, double* u_out, bmpc_rep
                        size_t* d2h_bytes);
 /* Device pointers of the result trajectories (for an NVLink gather). */
 int bmpc_batch_device_results(bmpc_batch* batch, double** d_x, double** d_u, size_t* bytes_x, size_t* bytes_u);
+/* Packs every instance's [x (node*nx) | u (node*nu)] contiguously into the
+ * device buffer d_dst (count * node * (nx + nu) doubles), async on the ctx
+ * stream — the send buffer of the final NVLink gather. */
+int bmpc_batch_pack_results(bmpc_batch* batch, double* d_dst, size_t* bytes);
 /* Records of one instance (device -> host copy). */
 int bmpc_batch_records(bmpc_batch* batch, int instance, bmpc_record* records, int max_records, int* n_records);
 /* Kernel launches the batch solve issues (1) and the launch configuration. */
 int bmpc_batch_info(const bmpc_batch* batch, int* threads_per_block, int* blocks, int* regs_per_thread);
+
+/* Measured FP64 FMA throughput of this device (TFLOP/s): the roofline
+ * denominator of the FP64-bound solve path. */
+int bmpc_fp64_peak_tflops(bmpc_ctx* ctx, double* tflops);
 
 /* ---------------------------------------------- kernel-level LQR tree */
 /* backward_pass + linear_rollout + expected_change_coefficients

@@ -438,6 +438,10 @@ class Batch:
         self._h = h
         self._models = (_Model * self.count)(*[p.model for p in problems])
 
+    def set_launch(self, threads: int, min_blocks: int):
+        """Per-instance thread-block shape (compiled variants only)."""
+        _check(lib().bmpc_batch_set_launch(self._h, int(threads), int(min_blocks)))
+
     def set_models(self) -> int:
         b = C.c_size_t()
         _check(lib().bmpc_batch_set_models(self._h, self._models, C.byref(b)))
@@ -455,6 +459,13 @@ class Batch:
         b = C.c_size_t()
         _check(lib().bmpc_batch_results(self._h, _ptr(x), _ptr(u), reps, C.byref(b)))
         return ([_report(r) for r in reps] if want_reports else None), b.value
+
+    def pack_results(self, d_dst_ptr: int) -> int:
+        """Pack [x | u] of every instance into a device buffer (e.g. a torch
+        tensor's data_ptr()) for the NVLink gather; returns bytes."""
+        b = C.c_size_t()
+        _check(lib().bmpc_batch_pack_results(self._h, C.c_void_p(d_dst_ptr), C.byref(b)))
+        return b.value
 
     def records(self, instance: int, max_records: int = 1000) -> dict:
         recs = (_Record * max_records)()
@@ -495,6 +506,14 @@ def lqr_tree(tree: TreeTopology, nx: int, nu: int, stage: np.ndarray, defect: np
                                _ptr(dx0), int(grid), _ptr(K), _ptr(k), _ptr(P), _ptr(p), _ptr(dx), _ptr(du),
                                _ptr(sc)))
     return dict(K=K, k=k, P=P, p=p, dx=dx, du=du, max_feedforward=sc[0], a1=sc[1], a2=sc[2], error=int(sc[3]))
+
+
+def fp64_peak_tflops(ctx: Optional[Context] = None) -> float:
+    """Measured FP64 FMA peak of the device (DFMA microbenchmark)."""
+    ctx = ctx or default_context()
+    v = C.c_double()
+    _check(lib().bmpc_fp64_peak_tflops(ctx._h, C.byref(v)))
+    return v.value
 
 
 def version() -> str:

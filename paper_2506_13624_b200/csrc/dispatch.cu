@@ -44,13 +44,39 @@ Strides strides_for(int nx, int nu) {
   return Strides{};
 }
 
+// Launch-shape variants (threads, min blocks/SM) of the per-instance kernel.
+#define BMPC_CTA_VARIANTS(X)                                                                   \
+  X(4, 2, 256, 1) X(4, 2, 128, 2) X(4, 2, 64, 4) X(4, 2, 128, 3) X(4, 2, 64, 6) X(4, 2, 128, 4) \
+  X(4, 2, 64, 8) X(3, 2, 256, 1) X(3, 2, 64, 4) X(2, 1, 256, 1) X(2, 1, 64, 4)
+
+#define X(a, b, t, m) extern template struct CtaVariant<a, b, t, m>;
+BMPC_CTA_VARIANTS(X)
+#undef X
+
+bool cta_variant_supported(int nx, int nu, int threads, int min_blocks) {
+#define X(a, b, t, m) \
+  if (nx == a && nu == b && threads == t && min_blocks == m) return true;
+  BMPC_CTA_VARIANTS(X)
+#undef X
+  return false;
+}
+
 cudaError_t launch_solve_cta(int nx, int nu, const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
-                             const DevOptions& opts, int count, int threads, cudaStream_t stream) {
-#define X(a, b) \
-  if (nx == a && nu == b) return SolveLaunch<a, b>::solve_cta(d_topo, d_mp, d_work, opts, count, threads, stream);
-  BMPC_SOLVE_DIMS(X)
+                             const DevOptions& opts, int count, int threads, int min_blocks, cudaStream_t stream) {
+#define X(a, b, t, m)                                                 \
+  if (nx == a && nu == b && threads == t && min_blocks == m)          \
+    return CtaVariant<a, b, t, m>::launch(d_topo, d_mp, d_work, opts, count, stream);
+  BMPC_CTA_VARIANTS(X)
 #undef X
   return cudaErrorInvalidValue;
+}
+
+int solve_cta_regs(int nx, int nu, int threads, int min_blocks) {
+#define X(a, b, t, m) \
+  if (nx == a && nu == b && threads == t && min_blocks == m) return CtaVariant<a, b, t, m>::regs();
+  BMPC_CTA_VARIANTS(X)
+#undef X
+  return 0;
 }
 
 cudaError_t launch_solve_grid(int nx, int nu, const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
@@ -66,14 +92,6 @@ cudaError_t launch_solve_grid(int nx, int nu, const Topo* d_topo, const ModelPar
 int solve_grid_blocks(int nx, int nu, int threads) {
 #define X(a, b) \
   if (nx == a && nu == b) return SolveLaunch<a, b>::grid_blocks(threads);
-  BMPC_SOLVE_DIMS(X)
-#undef X
-  return 0;
-}
-
-int solve_cta_regs(int nx, int nu) {
-#define X(a, b) \
-  if (nx == a && nu == b) return SolveLaunch<a, b>::cta_regs();
   BMPC_SOLVE_DIMS(X)
 #undef X
   return 0;

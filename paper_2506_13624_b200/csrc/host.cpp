@@ -10,6 +10,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -626,7 +627,9 @@ struct bmpc_batch {
   std::vector<ModelParams> h_mps;
   std::vector<Work> h_works;
   size_t per_state_doubles{0};
-  int threads{256};
+  int threads{256};       // grid mode block size
+  int cta_threads{256};   // per-instance block shape (bmpc_batch_set_launch)
+  int cta_min_blocks{1};
   bool grid_mode{false};
   int grid_blocks{0};
 };
@@ -634,6 +637,29 @@ struct bmpc_batch {
 namespace {
 
 size_t align2(size_t v) { return (v + 1) & ~size_t{1}; }
+
+// Per-instance block shape: env BMPC_CTA="<threads>x<min_blocks>" overrides
+// the tuned default.
+void default_launch_shape(bmpc_batch* b) {
+  int t = 256, m = 1;
+  if (b->nx == 4 && b->nu == 2) {
+    t = 256;
+    m = 1;
+  }
+  if (const char* env = std::getenv("BMPC_CTA")) {
+    int et = 0, em = 0;
+    if (std::sscanf(env, "%dx%d", &et, &em) == 2 && cta_variant_supported(b->nx, b->nu, et, em)) {
+      t = et;
+      m = em;
+    }
+  }
+  if (!cta_variant_supported(b->nx, b->nu, t, m)) {
+    t = 256;
+    m = 1;
+  }
+  b->cta_threads = t;
+  b->cta_min_blocks = m;
+}
 
 // Lays out every per-instance array; returns doubles per instance.
 size_t state_layout(const Plan& pl, int nx, int nu, const Strides& st, size_t off[12]) {
@@ -838,12 +864,13 @@ int bmpc_batch_create(bmpc_ctx* ctx, const bmpc_tree* tree, int count, const bmp
     b->mps = DevBuf(C * sizeof(ModelParams));
     b->works = DevBuf(C * sizeof(Work));
     // Grid mode for a single large tree: all SMs on one instance.
-    b->grid_mode = count == 1 && tree->node_count > 4096;
+    b->grid_mode = count == 1 && tree->node_count > 1024;
     if (b->grid_mode) {
       b->grid_blocks = solve_grid_blocks(b->nx, b->nu, b->threads);
       if (b->grid_blocks < 1) return fail(BMPC_ERR_CUDA, "grid solve kernel cannot be made co-resident");
       b->red = DevBuf(2 * static_cast<size_t>(b->grid_blocks) * kRedSlotsHost * sizeof(double));
     }
+    default_launch_shape(b.get());
     b->h_mps.resize(C);
     b->h_works.resize(C);
     const size_t n = static_cast<size_t>(tree->node_count);
@@ -975,6 +1002,16 @@ int bmpc_batch_replicate(bmpc_batch* b) {
   }
 }
 
+int bmpc_batch_set_launch(bmpc_batch* b, int threads, int min_blocks) {
+  if (!b) return fail(BMPC_ERR_INVALID, "null argument");
+  if (!cta_variant_supported(b->nx, b->nu, threads, min_blocks))
+    return fail(BMPC_ERR_UNSUPPORTED, "launch shape " + std::to_string(threads) + "x" + std::to_string(min_blocks) +
+                                          " not compiled for these dims");
+  b->cta_threads = threads;
+  b->cta_min_blocks = min_blocks;
+  return BMPC_OK;
+}
+
 // Initial inputs: zeros unless given (solver.hpp:604-609).
 static int batch_set_inputs(bmpc_batch* b, const double* initial_inputs) {
   const size_t n = static_cast<size_t>(b->plan->n);
@@ -992,20 +1029,21 @@ static int batch_set_inputs(bmpc_batch* b, const double* initial_inputs) {
   return BMPC_OK;
 }
 
-static int batch_launch(bmpc_batch* b, const bmpc_options* opts) {
+static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_inputs) {
   bmpc_options o;
   if (opts)
     o = *opts;
   else
     bmpc_options_default(&o);
-  const DevOptions d = to_dev(o);
+  DevOptions d = to_dev(o);
+  d.zero_inputs = zero_inputs ? 1 : 0;
   cudaError_t e;
   if (b->grid_mode) {
     e = launch_solve_grid(b->nx, b->nu, b->plan->d_topo.as<Topo>(), b->mps.as<ModelParams>(), b->works.as<Work>(), d,
                           b->red.as<double>(), b->grid_blocks, b->threads, b->ctx->stream);
   } else {
     e = launch_solve_cta(b->nx, b->nu, b->plan->d_topo.as<Topo>(), b->mps.as<ModelParams>(), b->works.as<Work>(), d,
-                         b->count, b->threads, b->ctx->stream);
+                         b->count, b->cta_threads, b->cta_min_blocks, b->ctx->stream);
   }
   if (e != cudaSuccess) return fail(BMPC_ERR_CUDA, std::string("solve launch: ") + cudaGetErrorString(e));
   ++b->ctx->launches;
@@ -1016,13 +1054,7 @@ int bmpc_batch_solve(bmpc_batch* b, const bmpc_options* opts) {
   try {
     if (!b) return fail(BMPC_ERR_INVALID, "null argument");
     ck(cudaSetDevice(b->ctx->device), "cudaSetDevice");
-    // Zero initial inputs for every instance (one memset over the u arrays).
-    for (int i = 0; i < b->count; ++i)
-      ck(cudaMemsetAsync(b->h_works[static_cast<size_t>(i)].u, 0,
-                         static_cast<size_t>(b->plan->n) * static_cast<size_t>(b->nu) * sizeof(double),
-                         b->ctx->stream),
-         "inputs");
-    return batch_launch(b, opts);
+    return batch_launch(b, opts, true);  // zero initial inputs, set on device
   } catch (const std::exception& e) {
     return fail(BMPC_ERR_CUDA, e.what());
   }
@@ -1073,6 +1105,24 @@ int bmpc_batch_device_results(bmpc_batch* b, double** d_x, double** d_u, size_t*
   return BMPC_OK;
 }
 
+int bmpc_batch_pack_results(bmpc_batch* b, double* d_dst, size_t* bytes) {
+  if (!b || !d_dst) return fail(BMPC_ERR_INVALID, "null argument");
+  cudaSetDevice(b->ctx->device);
+  const cudaError_t e = launch_pack_results(b->works.as<Work>(), b->count, b->plan->n, b->nx, b->nu, d_dst,
+                                            b->ctx->stream);
+  if (e != cudaSuccess) return fail(BMPC_ERR_CUDA, cudaGetErrorString(e));
+  ++b->ctx->launches;
+  if (bytes) *bytes = static_cast<size_t>(b->count) * b->plan->n * (b->nx + b->nu) * sizeof(double);
+  return BMPC_OK;
+}
+
+int bmpc_fp64_peak_tflops(bmpc_ctx* ctx, double* tflops) {
+  if (!ctx || !tflops) return fail(BMPC_ERR_INVALID, "null argument");
+  cudaSetDevice(ctx->device);
+  *tflops = measure_fp64_peak_tflops(ctx->stream);
+  return cudaGetLastError() == cudaSuccess ? BMPC_OK : fail(BMPC_ERR_CUDA, "fp64 microbenchmark failed");
+}
+
 int bmpc_batch_records(bmpc_batch* b, int instance, bmpc_record* records, int max_records, int* n_records) {
   try {
     if (!b || instance < 0 || instance >= b->count) return fail(BMPC_ERR_INVALID, "bad instance");
@@ -1094,9 +1144,9 @@ int bmpc_batch_records(bmpc_batch* b, int instance, bmpc_record* records, int ma
 
 int bmpc_batch_info(const bmpc_batch* b, int* threads, int* blocks, int* regs) {
   if (!b) return fail(BMPC_ERR_INVALID, "null argument");
-  if (threads) *threads = b->threads;
+  if (threads) *threads = b->grid_mode ? b->threads : b->cta_threads;
   if (blocks) *blocks = b->grid_mode ? b->grid_blocks : b->count;
-  if (regs) *regs = solve_cta_regs(b->nx, b->nu);
+  if (regs) *regs = b->grid_mode ? 0 : solve_cta_regs(b->nx, b->nu, b->cta_threads, b->cta_min_blocks);
   return BMPC_OK;
 }
 
@@ -1110,11 +1160,11 @@ int bmpc_solve(bmpc_ctx* ctx, const bmpc_tree* tree, const bmpc_model_desc* mode
   rc = bmpc_batch_set_models(b, model, nullptr);
   if (rc != BMPC_OK) return rc;
   try {
-    batch_set_inputs(b, initial_inputs);
+    if (initial_inputs) batch_set_inputs(b, initial_inputs);
   } catch (const std::exception& e) {
     return fail(BMPC_ERR_CUDA, e.what());
   }
-  rc = batch_launch(b, opts);
+  rc = batch_launch(b, opts, initial_inputs == nullptr);
   if (rc != BMPC_OK) return rc;
   bmpc_report rep{};
   rc = bmpc_batch_results(b, x_out, u_out, &rep, nullptr);

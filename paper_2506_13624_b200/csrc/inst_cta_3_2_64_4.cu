@@ -1,0 +1,5 @@
+// Explicit instantiation: per-instance solve kernel, nx=3 nu=2, 64 threads, >= 4 blocks/SM.
+#include "kernels_impl.cuh"
+namespace bmpc_b200 {
+template struct CtaVariant<3, 2, 64, 4>;
+}  // namespace bmpc_b200

@@ -1,4 +1,4 @@
-// Explicit instantiation: full solve for nx=3, nu=2.
+// Explicit instantiation: whole-GPU (cooperative) solve + kernel-level LQR for nx=3, nu=2.
 #include "kernels_impl.cuh"
 namespace bmpc_b200 {
 template struct SolveLaunch<3, 2>;

@@ -33,29 +33,36 @@ struct LqrLaunch {
   static int grid_blocks(int threads);
 };
 
+// One thread block of T threads per instance, >= MB blocks resident per SM
+// (registers/thread <= 65536 / (T * MB)).
+template <int NX, int NU, int T, int MB>
+struct CtaVariant {
+  static cudaError_t launch(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work, const DevOptions& opts,
+                            int count, cudaStream_t stream);
+  static int regs();
+};
+
 template <int NX, int NU>
 struct SolveLaunch {
-  // One thread block per instance.
-  static cudaError_t solve_cta(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
-                               const DevOptions& opts, int count, int threads, cudaStream_t stream);
   // All blocks on one instance (cooperative launch); `red` holds
   // 2 * blocks * kRedSlotsHost doubles.
   static cudaError_t solve_grid(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
                                 const DevOptions& opts, double* red, int blocks, int threads, cudaStream_t stream);
   static int grid_blocks(int threads);
-  static int cta_regs();
 };
 
 // Dispatch over the compiled dimension sets (dispatch.cu).
 bool solve_dims_supported(int nx, int nu);
 bool lqr_dims_supported(int nx, int nu);
 Strides strides_for(int nx, int nu);
+// Launch-shape variants of the per-instance kernel compiled for (nx, nu).
+bool cta_variant_supported(int nx, int nu, int threads, int min_blocks);
 cudaError_t launch_solve_cta(int nx, int nu, const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
-                             const DevOptions& opts, int count, int threads, cudaStream_t stream);
+                             const DevOptions& opts, int count, int threads, int min_blocks, cudaStream_t stream);
 cudaError_t launch_solve_grid(int nx, int nu, const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
                               const DevOptions& opts, double* red, int blocks, int threads, cudaStream_t stream);
 int solve_grid_blocks(int nx, int nu, int threads);
-int solve_cta_regs(int nx, int nu);
+int solve_cta_regs(int nx, int nu, int threads, int min_blocks);
 cudaError_t launch_lqr_tree(int nx, int nu, bool grid, const Topo* d_topo, const Work* d_work, double reg,
                             double* d_scalars, double* red, int blocks, int threads, cudaStream_t stream);
 int lqr_grid_blocks(int nx, int nu, int threads);
@@ -67,5 +74,10 @@ size_t sizeof_dev_result();
 size_t sizeof_dev_record();
 
 constexpr int kRedSlotsHost = 64;
+
+// util.cu
+cudaError_t launch_pack_results(const Work* d_works, int count, int n, int nx, int nu, double* dst,
+                                cudaStream_t stream);
+double measure_fp64_peak_tflops(cudaStream_t stream);
 
 }  // namespace bmpc_b200

@@ -18,8 +18,10 @@ struct BlockCtx {
   Work work;
 };
 
-template <int NX, int NU>
-__global__ void __launch_bounds__(256) solve_cta_kernel(const Topo* __restrict__ topo,
+// THREADS x MINB trade registers for resident instances per SM:
+// registers/thread <= 65536 / (THREADS * MINB).
+template <int NX, int NU, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) solve_cta_kernel(const Topo* __restrict__ topo,
                                                         const ModelParams* __restrict__ mps,
                                                         const Work* __restrict__ works, DevOptions opts,
                                                         int count) {
@@ -34,7 +36,9 @@ __global__ void __launch_bounds__(256) solve_cta_kernel(const Topo* __restrict__
     red.flag = 0;
   }
   __syncthreads();
+  __shared__ TeamSmem<NX> tsm[THREADS / (team_size<NX>() > 0 ? team_size<NX>() : THREADS)];
   Solver<NX, NU, CtaGroup> s(CtaGroup{&red}, ctx.topo, ctx.mp, ctx.work, opts);
+  s.tsm = tsm;
   s.solve();
 }
 
@@ -52,7 +56,9 @@ __global__ void __launch_bounds__(256) solve_grid_kernel(const Topo* __restrict_
     red.flag = 0;
   }
   __syncthreads();
+  __shared__ TeamSmem<NX> tsm[256 / (team_size<NX>() > 0 ? team_size<NX>() : 256)];
   Solver<NX, NU, GridGroup> s(GridGroup{&red, red_scratch, nullptr}, ctx.topo, ctx.mp, ctx.work, opts);
+  s.tsm = tsm;
   s.solve();
 }
 
@@ -60,7 +66,9 @@ template <int NX, int NU, class G>
 __device__ void lqr_tree_body(G g, BlockCtx& ctx, double reg, double* scalars) {
   ModelParams dummy{};
   DevOptions o{};
+  __shared__ TeamSmem<NX> tsm[256 / (team_size<NX>() > 0 ? team_size<NX>() : 256)];
   Solver<NX, NU, G> s(g, ctx.topo, dummy, ctx.work, o);
+  s.tsm = tsm;
   s.lqr_tree(reg, scalars);
 }
 
@@ -146,11 +154,18 @@ int LqrLaunch<NX, NU>::grid_blocks(int threads) {
   return max_coresident(lqr_tree_grid_kernel<NX, NU>, threads);
 }
 
-template <int NX, int NU>
-cudaError_t SolveLaunch<NX, NU>::solve_cta(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
-                                           const DevOptions& opts, int count, int threads, cudaStream_t stream) {
-  solve_cta_kernel<NX, NU><<<count, threads, 0, stream>>>(d_topo, d_mp, d_work, opts, count);
+template <int NX, int NU, int T, int MB>
+cudaError_t CtaVariant<NX, NU, T, MB>::launch(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
+                                              const DevOptions& opts, int count, cudaStream_t stream) {
+  solve_cta_kernel<NX, NU, T, MB><<<count, T, 0, stream>>>(d_topo, d_mp, d_work, opts, count);
   return cudaGetLastError();
+}
+
+template <int NX, int NU, int T, int MB>
+int CtaVariant<NX, NU, T, MB>::regs() {
+  cudaFuncAttributes attr{};
+  cudaFuncGetAttributes(&attr, solve_cta_kernel<NX, NU, T, MB>);
+  return attr.numRegs;
 }
 
 template <int NX, int NU>
@@ -168,11 +183,5 @@ int SolveLaunch<NX, NU>::grid_blocks(int threads) {
   return max_coresident(solve_grid_kernel<NX, NU>, threads);
 }
 
-template <int NX, int NU>
-int SolveLaunch<NX, NU>::cta_regs() {
-  cudaFuncAttributes attr{};
-  cudaFuncGetAttributes(&attr, solve_cta_kernel<NX, NU>);
-  return attr.numRegs;
-}
 
 }  // namespace bmpc_b200

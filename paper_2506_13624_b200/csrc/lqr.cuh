@@ -316,6 +316,158 @@ __device__ void init_fwd_element(const double* s, const double* c, const double*
   for (int i = 0; i < NX; ++i) f[F::c + i] = c[i] + Bk[i];
 }
 
+// ---------------------------------------------------------------------------
+// Team-cooperative combine_bwd: TS lanes (TS >= NX*NX, a power of two <= 32)
+// compute one combination, lane l owning entry (l % NX, l / NX) of every NX x
+// NX block. Operands are staged in shared memory (conflict-free column-major
+// reads), G = I + C1 P2 is inverted once (every lane factors it redundantly
+// in registers, then produces its own entry of G^-1), and the five update
+// formulas of lqr_scan.hpp:68-97 become small matrix products:
+//   A = A2 (G^-1 A1),  C = (A2 (G^-1 C1)) A2' + C2,  c = A2 G^-1 (c1 - C1 p2) + c2,
+//   P = A1' (G^-T (P2 A1)) + P1,  p = A1' G^-T (p2 + P2 c1) + p1.
+// P and C are formed symmetric directly (each lane evaluates its (i,j) and
+// (j,i) entries, the reference's symmetrize). Latency ~7 short stages
+// instead of one thread's ~1.5 kflop dependent chain. `out` may alias e1/e2.
+template <int NX>
+struct TeamSmem {
+  double e1[BwdLayout<NX>::size], e2[BwdLayout<NX>::size];
+  double G[NX * NX], GI[NX * NX], X[NX * NX], W[NX * NX], Y[NX * NX], Z[NX * NX], T[NX * NX];
+  double v[NX], v2[NX], w[NX], w2[NX];
+};
+
+template <int NX, int TS>
+__device__ int team_combine_bwd(const double* e1g, const double* e2g, double* out, int lane, unsigned mask,
+                                TeamSmem<NX>& sm) {
+  using E = BwdLayout<NX>;
+  constexpr int N2 = NX * NX;
+  static_assert(TS >= N2 && TS <= 32, "team too small");
+  // Stage the operands.
+  for (int k = lane; k < E::size; k += TS) {
+    sm.e1[k] = e1g[k];
+    sm.e2[k] = e2g[k];
+  }
+  __syncwarp(mask);
+  const int i = lane % NX, j = lane / NX;
+  const bool act = lane < N2;
+  // G = I + C1 P2 ; vector pre-terms v = c1 - C1 p2, v2 = p2 + P2 c1.
+  if (act) {
+    double s = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+    for (int l = 0; l < NX; ++l) s = fma(sm.e1[E::C + i + l * NX], sm.e2[E::P + l + j * NX], s);
+    sm.G[lane] = s;
+  }
+  if (lane < NX) {
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int l = 0; l < NX; ++l) {
+      a = fma(sm.e1[E::C + lane + l * NX], sm.e2[E::p + l], a);
+      b = fma(sm.e2[E::P + lane + l * NX], sm.e1[E::c + l], b);
+    }
+    sm.v[lane] = sm.e1[E::c + lane] - a;
+    sm.v2[lane] = b + sm.e2[E::p + lane];
+  }
+  __syncwarp(mask);
+  // G^-1: redundant register LU per lane, lane (i, j) keeps entry (i, j).
+  if (act) {
+    Lu<NX> lu;
+    lu.compute(sm.G);
+    double ej[NX], col[NX];
+#pragma unroll
+    for (int r = 0; r < NX; ++r) ej[r] = (r == j) ? 1.0 : 0.0;
+    lu.template solve<1>(ej, col);
+    double g = col[0];
+#pragma unroll
+    for (int r = 1; r < NX; ++r) g = (r == i) ? col[r] : g;
+    sm.GI[lane] = g;
+  }
+  __syncwarp(mask);
+  // X = G^-1 A1, W = G^-1 C1, Z = P2 A1 ; w = G^-1 v, w2 = G^-T v2.
+  if (act) {
+    double x = 0.0, wv = 0.0, z = 0.0;
+#pragma unroll
+    for (int l = 0; l < NX; ++l) {
+      const double gil = sm.GI[i + l * NX];
+      x = fma(gil, sm.e1[E::A + l + j * NX], x);
+      wv = fma(gil, sm.e1[E::C + l + j * NX], wv);
+      z = fma(sm.e2[E::P + i + l * NX], sm.e1[E::A + l + j * NX], z);
+    }
+    sm.X[lane] = x;
+    sm.W[lane] = wv;
+    sm.Z[lane] = z;
+  }
+  if (lane < NX) {
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int l = 0; l < NX; ++l) {
+      a = fma(sm.GI[lane + l * NX], sm.v[l], a);
+      b = fma(sm.GI[l + lane * NX], sm.v2[l], b);
+    }
+    sm.w[lane] = a;
+    sm.w2[lane] = b;
+  }
+  __syncwarp(mask);
+  // A_out = A2 X ; Y = A2 W ; T = G^-T Z ; c_out, p_out.
+  bool ok = true;
+  double a_out = 0.0, c_out = 0.0, p_out = 0.0;
+  if (act) {
+    double y = 0.0, tt = 0.0;
+#pragma unroll
+    for (int l = 0; l < NX; ++l) {
+      const double a2il = sm.e2[E::A + i + l * NX];
+      a_out = fma(a2il, sm.X[l + j * NX], a_out);
+      y = fma(a2il, sm.W[l + j * NX], y);
+      tt = fma(sm.GI[l + i * NX], sm.Z[l + j * NX], tt);
+    }
+    sm.Y[lane] = y;
+    sm.T[lane] = tt;
+  }
+  if (lane < NX) {
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int l = 0; l < NX; ++l) {
+      a = fma(sm.e2[E::A + lane + l * NX], sm.w[l], a);
+      b = fma(sm.e1[E::A + l + lane * NX], sm.w2[l], b);
+    }
+    c_out = a + sm.e2[E::c + lane];
+    p_out = b + sm.e1[E::p + lane];
+  }
+  __syncwarp(mask);
+  // C_out = Y A2' + C2 and P_out = A1' T + P1, symmetrized entrywise.
+  double C_out = 0.0, P_out = 0.0;
+  if (act) {
+    double cij = 0.0, cji = 0.0, pij = 0.0, pji = 0.0;
+#pragma unroll
+    for (int l = 0; l < NX; ++l) {
+      cij = fma(sm.Y[i + l * NX], sm.e2[E::A + j + l * NX], cij);
+      cji = fma(sm.Y[j + l * NX], sm.e2[E::A + i + l * NX], cji);
+      pij = fma(sm.e1[E::A + l + i * NX], sm.T[l + j * NX], pij);
+      pji = fma(sm.e1[E::A + l + j * NX], sm.T[l + i * NX], pji);
+    }
+    cij += sm.e2[E::C + lane];
+    cji += sm.e2[E::C + j + i * NX];
+    pij += sm.e1[E::P + lane];
+    pji += sm.e1[E::P + j + i * NX];
+    C_out = 0.5 * (cij + cji);
+    P_out = 0.5 * (pij + pji);
+    ok = isfinite(a_out) && isfinite(C_out) && isfinite(P_out);
+  }
+  if (lane < NX) ok = ok && isfinite(c_out) && isfinite(p_out);
+  // Every lane finished reading the staged operands before `out` (which may
+  // alias e1g/e2g) is written — the stores below only touch global memory.
+  if (act) {
+    out[E::A + lane] = a_out;
+    out[E::C + lane] = C_out;
+    out[E::P + lane] = P_out;
+  }
+  if (lane < NX) {
+    out[E::c + lane] = c_out;
+    out[E::p + lane] = p_out;
+  }
+  const unsigned bad = __ballot_sync(mask, !ok);
+  __syncwarp(mask);
+  return bad ? kFactorization : kBwdOk;
+}
+
 // combine_fwd (lqr_scan.hpp:171-173): (A2 A1, A2 c1 + c2).
 template <int NX>
 __device__ void combine_fwd(const double* f1, const double* f2, double* out) {  // out may alias f2

@@ -34,7 +34,7 @@ namespace bmpc_b200 {
 namespace cg = cooperative_groups;
 
 constexpr int kRedSlots = 4 * kMaxAlpha;  // largest simultaneous reduction
-constexpr int kMaxWarps = 32;
+constexpr int kMaxWarps = 8;  // blocks of <= 256 threads
 
 // Scan level bookkeeping (scan.hpp:19-36): n_0 = E, n_{l+1} = ceil(n_l / 2).
 __device__ __forceinline__ int level_size(int E, int l) {
@@ -54,6 +54,12 @@ __host__ __device__ __forceinline__ int up_steps(int E) {
   int u = 0;
   for (int s = E; s >= 2; s = (s + 1) >> 1) ++u;
   return u;
+}
+
+// Lanes per cooperative combine_bwd team (0 = one thread per combination).
+template <int NX>
+__host__ __device__ constexpr int team_size() {
+  return NX * NX <= 4 ? 4 : (NX * NX <= 16 ? 16 : (NX * NX <= 32 ? 32 : 0));
 }
 
 // ------------------------------------------------------------------ groups
@@ -155,6 +161,7 @@ struct Solver {
   Work& w;
   const DevOptions& o;
   double g_rho{0.0};  // current AL penalty (uniform across the group)
+  TeamSmem<NX>* tsm{nullptr};  // [blockDim / kTS] team scratch (kernel-provided)
 
   __device__ Solver(G g_, const Topo& t_, const ModelParams& mp_, Work& w_, const DevOptions& o_)
       : g(g_), t(t_), mp(mp_), w(w_), o(o_) {}
@@ -180,7 +187,7 @@ struct Solver {
   __device__ bool rollout() {
     // Leaves carry no input (TrajectoryTree, tree.hpp:159-173).
     for (int i = g.rank(); i < t.n; i += g.size()) {
-      if (is_leaf(i)) {
+      if (is_leaf(i) || o.zero_inputs) {
 #pragma unroll
         for (int j = 0; j < NU; ++j) w.u[i * NU + j] = 0.0;
       }
@@ -330,10 +337,67 @@ struct Solver {
 
   // Backward suffix scan of segments at depth d, elements already in level 0
   // (reversed). f(a, b) = combine_bwd(first = b, second = a).
+  // Team size of the cooperative combine (0: one thread per combination).
+  static constexpr int kTS = team_size<NX>();
+
+  // Items of a per-segment phase, one kTS-lane team per item.
+  template <class F>
+  __device__ void for_depth_items_team(int d, int per_seg, F&& f) const {
+    const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
+    const int total = (se - sb) * per_seg;
+    const int team = g.rank() / kTS, nteams = g.size() / kTS;
+    const int lane = threadIdx.x % kTS;
+    const unsigned mask =
+        kTS == 32 ? 0xffffffffu : (((1u << kTS) - 1u) << ((threadIdx.x & 31) / kTS * kTS));
+    for (int q = team; q < total; q += nteams) f(sb + q / per_seg, q % per_seg, lane, mask);
+  }
+
+  // Backward suffix scan of segments at depth d, elements already in level 0
+  // (reversed). f(a, b) = combine_bwd(first = b, second = a).
   __device__ int scan_bwd_depth(int d) {
     const int E = t.depth_len[d];
     const int U = up_steps(E);
     int err = kBwdOk;
+    if constexpr (kTS > 0) {
+      TeamSmem<NX>& my = tsm[threadIdx.x / kTS];
+      for (int l = 0; l < U; ++l) {
+        const int nl = level_size(E, l), nn = (nl + 1) >> 1;
+        const int ol = level_offset(E, l), on = ol + nl;
+        for_depth_items_team(d, nn, [&](int s, int i, int lane, unsigned mask) {
+          const int base = t.seg_scratch[s];
+          double* dst = bwd(base + on + i);
+          if (2 * i + 1 < nl) {
+            const int e = team_combine_bwd<NX, kTS>(bwd(base + ol + 2 * i + 1), bwd(base + ol + 2 * i), dst, lane,
+                                                     mask, my);
+            err = err ? err : e;
+          } else {
+            const double* src = bwd(base + ol + 2 * i);
+            for (int k = lane; k < BL::size; k += kTS) dst[k] = src[k];
+          }
+        });
+        g.sync();
+      }
+      for (int l = U - 1; l >= 0; --l) {
+        const int nl = level_size(E, l), nn = (nl + 1) >> 1;
+        const int ol = level_offset(E, l), on = ol + nl;
+        for_depth_items_team(d, nn, [&](int s, int i, int lane, unsigned mask) {
+          const int base = t.seg_scratch[s];
+          const double* S = bwd(base + on);
+          if (2 * i + 1 < nl) {
+            const double* src = S + static_cast<size_t>(i) * BL::stride;
+            double* dst = bwd(base + ol + 2 * i + 1);
+            for (int k = lane; k < BL::size; k += kTS) dst[k] = src[k];
+          }
+          if (i >= 1) {
+            double* a = bwd(base + ol + 2 * i);
+            const int e = team_combine_bwd<NX, kTS>(a, S + static_cast<size_t>(i - 1) * BL::stride, a, lane, mask, my);
+            err = err ? err : e;
+          }
+        });
+        g.sync();
+      }
+      return err;
+    }
     for (int l = 0; l < U; ++l) {
       const int nl = level_size(E, l), nn = (nl + 1) >> 1;
       const int ol = level_offset(E, l), on = ol + nl;

@@ -32,6 +32,7 @@ struct DevOptions {  // SolverOptions (solver.hpp:28-58), device copy
   double tol_defect, tol_cost, tol_feedforward, tol_constraint;
   double penalty_init, penalty_growth, penalty_max;
   double reg_init, reg_min, reg_growth, reg_decay, reg_max;
+  int zero_inputs;  // 1: initial inputs are zero (solver.hpp:604-609), skip the H2D
 };
 
 // IterationRecord (solver.hpp:547-561).

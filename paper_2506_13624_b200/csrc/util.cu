@@ -1,0 +1,74 @@
+// Utility kernels: result packing for the multi-GPU gather, and the FP64
+// FMA microbenchmark that measures the roofline denominator (MEASURED_PEAKS
+// has no FP64 figure; SURVEY.md §8d asks for a DFMA measurement).
+#include <cuda_runtime.h>
+
+#include "types.h"
+
+namespace bmpc_b200 {
+
+// dst[i] = [x_i (n*nx) | u_i (n*nu)] for every instance i, contiguous.
+__global__ void pack_results_kernel(const Work* __restrict__ works, int count, int n, int nx, int nu,
+                                    double* __restrict__ dst) {
+  const long long per = static_cast<long long>(n) * (nx + nu);
+  const long long total = per * count;
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int inst = static_cast<int>(q / per);
+    const long long r = q % per;
+    const Work& w = works[inst];
+    dst[q] = r < static_cast<long long>(n) * nx ? w.x[r] : w.u[r - static_cast<long long>(n) * nx];
+  }
+}
+
+cudaError_t launch_pack_results(const Work* d_works, int count, int n, int nx, int nu, double* dst,
+                                cudaStream_t stream) {
+  pack_results_kernel<<<1184, 256, 0, stream>>>(d_works, count, n, nx, nu, dst);
+  return cudaGetLastError();
+}
+
+// 8 independent DFMA chains per thread, `iters` rounds: 16 flops per round.
+__global__ void dfma_peak_kernel(double* out, int iters) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = 1.0 + 1e-9 * (threadIdx.x + k);
+  const double b = 0.999999999, c = 1e-12;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 42.0) out[0] = s;  // keep the chains alive
+}
+
+double measure_fp64_peak_tflops(cudaStream_t stream) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* d = nullptr;
+  cudaMalloc(&d, sizeof(double));
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  dfma_peak_kernel<<<blocks, threads, 0, stream>>>(d, iters);  // warm-up
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0, stream);
+    dfma_peak_kernel<<<blocks, threads, 0, stream>>>(d, iters);
+    cudaEventRecord(e1, stream);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  const double flops = 2.0 * 8.0 * static_cast<double>(iters) * blocks * threads;
+  return flops / (best * 1e-3) / 1e12;
+}
+
+}  // namespace bmpc_b200
