@@ -1424,3 +1424,23 @@ int bo_combine_bwd(int nx, const double* e1, const double* e2, double* out) {
   memcpy(out + 3 * nx * nx + nx, o.c, sizeof(double) * nx);
   return rc;
 }
+
+/* nonlinear_rollout (problem.hpp:150-166) and evaluate (problem.hpp:109-146)
+ * with zero multipliers, for property checks. */
+int bo_rollout(const bo_problem* p, const double* u, double* x_out) {
+  double* ub = (double*)calloc((size_t)p->n * p->nu, sizeof(double));
+  const int rc = rollout(p, u, x_out, ub);
+  free(ub);
+  return rc;
+}
+
+void bo_evaluate(const bo_problem* p, const double* x, const double* u, double rho, double* out) {
+  double* eta = (double*)calloc((size_t)p->n * NCMAX, sizeof(double));
+  const eval_t ev = evaluate(p, x, u, eta, rho);
+  out[0] = ev.cost;
+  out[1] = ev.cost_al;
+  out[2] = ev.defect_l1;
+  out[3] = ev.max_violation;
+  out[4] = ev.finite;
+  free(eta);
+}

@@ -94,6 +94,11 @@ void bo_random_lq(unsigned long long seed, int n, const int* nchild, int nx, int
 /* Raw engine / distribution (for pinning against libstdc++). */
 void bo_mt_uniform(unsigned long long seed, int count, double* out);
 
+/* nonlinear_rollout of inputs u from x0; evaluate with zero multipliers:
+ * out = {cost, cost_al, defect_l1, max_violation, finite}. */
+int bo_rollout(const bo_problem* p, const double* u, double* x_out);
+void bo_evaluate(const bo_problem* p, const double* x, const double* u, double rho, double* out);
+
 /* Unit routines on single elements (lqr_scan.hpp), element = P p C A c. */
 int bo_init_bwd_element(int nx, int nu, const double* stage /*A B c Q R M q r*/, double* e);
 int bo_combine_bwd(int nx, const double* e1, const double* e2, double* out);

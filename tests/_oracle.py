@@ -187,3 +187,19 @@ def mt_uniform(seed, count):
     out = np.zeros(count)
     lib().bo_mt_uniform(C.c_ulonglong(seed), count, _p(out))
     return out
+
+
+def rollout(prob: Problem, u):
+    x = np.zeros((prob.n, prob.nx))
+    uu = np.ascontiguousarray(u, np.float64)
+    if lib().bo_rollout(C.byref(prob.s), _p(uu), _p(x)) != 0:
+        raise RuntimeError("nonlinear_rollout: non-finite state")
+    return x
+
+
+def evaluate(prob: Problem, x, u, rho=10.0):
+    out = np.zeros(5)
+    xx = np.ascontiguousarray(x, np.float64)
+    uu = np.ascontiguousarray(u, np.float64)
+    lib().bo_evaluate(C.byref(prob.s), _p(xx), _p(uu), C.c_double(rho), _p(out))
+    return dict(cost=out[0], cost_al=out[1], defect_l1=out[2], max_violation=out[3], finite=bool(out[4]))
