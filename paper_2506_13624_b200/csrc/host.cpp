@@ -629,6 +629,13 @@ struct bmpc_batch {
   size_t per_state_doubles{0};
   int threads{256};       // grid mode block size
   int cta_threads{256};   // per-instance block shape (bmpc_batch_set_launch)
+  double* h_stage{nullptr};  // pinned H2D staging (set_models)
+  double* h_pack{nullptr};   // pinned D2H staging (results)
+  DevBuf d_pack;             // device [x | u] pack buffer
+  ~bmpc_batch() {
+    if (h_stage) cudaFreeHost(h_stage);
+    if (h_pack) cudaFreeHost(h_pack);
+  }
   int cta_min_blocks{1};
   bool grid_mode{false};
   int grid_blocks{0};
@@ -927,15 +934,22 @@ int bmpc_batch_set_models(bmpc_batch* b, const bmpc_model_desc* models, size_t* 
     if (!b || !models) return fail(BMPC_ERR_INVALID, "null argument");
     ck(cudaSetDevice(b->ctx->device), "cudaSetDevice");
     const size_t n = static_cast<size_t>(b->plan->n);
-    size_t bytes = 0;
+    const size_t C = static_cast<size_t>(b->count);
+    const size_t x0s = align2(static_cast<size_t>(b->nx));
     cudaStream_t s = b->ctx->stream;
-    for (int i = 0; i < b->count; ++i) {
+    // Gather every instance's per-node arrays into one pinned staging buffer
+    // laid out exactly like the device buffer, then ONE host-to-device copy.
+    ck(cudaStreamSynchronize(s), "staging reuse");
+    if (!b->h_stage) ck(cudaMallocHost(&b->h_stage, (C * b->node_data_doubles + C * x0s) * sizeof(double)), "pinned");
+    double* hs = b->h_stage;
+    double* hx0 = hs + C * b->node_data_doubles;
+    for (size_t i = 0; i < C; ++i) {
       const bmpc_model_desc& m = models[i];
       if (m.kind != b->kind || m.state_dim != b->nx || m.input_dim != b->nu ||
           (b->kind == BMPC_MODEL_UNICYCLE && m.num_vehicles != b->nv))
         return fail(BMPC_ERR_INVALID, "model " + std::to_string(i) + " does not match the batch template");
-      ModelParams& mp = b->h_mps[static_cast<size_t>(i)];
-      double* md = b->model_data.as<double>() + static_cast<size_t>(i) * b->node_data_doubles;
+      ModelParams& mp = b->h_mps[i];
+      double* md = hs + i * b->node_data_doubles;
       if (b->kind == BMPC_MODEL_UNICYCLE) {
         mp.dt = m.dt;
         std::memcpy(mp.Wx, m.state_weights, sizeof mp.Wx);
@@ -944,30 +958,21 @@ int bmpc_batch_set_models(bmpc_batch* b, const bmpc_model_desc* models, size_t* 
         mp.a_max = m.accel_limit;
         mp.w_max = m.yaw_rate_limit;
         mp.radius = m.safety_radius;
-        ck(cudaMemcpyAsync(md, m.reference, n * 4 * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
-        bytes += n * 4 * sizeof(double);
-        if (b->nv > 0) {
-          const size_t vb = n * static_cast<size_t>(b->nv) * 2 * sizeof(double);
-          ck(cudaMemcpyAsync(md + align2(n * 4), m.vehicle_position, vb, cudaMemcpyHostToDevice, s), "h2d");
-          bytes += vb;
-        }
+        std::memcpy(md, m.reference, n * 4 * sizeof(double));
+        if (b->nv > 0) std::memcpy(md + align2(n * 4), m.vehicle_position, n * static_cast<size_t>(b->nv) * 2 * sizeof(double));
       } else {
-        const size_t sb = n * lq_stage_size(b->nx, b->nu) * sizeof(double);
-        const size_t lb = n * static_cast<size_t>(b->nx * b->nx + b->nx) * sizeof(double);
-        ck(cudaMemcpyAsync(md, m.lq_stage, sb, cudaMemcpyHostToDevice, s), "h2d");
-        ck(cudaMemcpyAsync(md + align2(n * lq_stage_size(b->nx, b->nu)), m.lq_leaf, lb, cudaMemcpyHostToDevice, s),
-           "h2d");
-        bytes += sb + lb;
+        std::memcpy(md, m.lq_stage, n * lq_stage_size(b->nx, b->nu) * sizeof(double));
+        std::memcpy(md + align2(n * lq_stage_size(b->nx, b->nu)), m.lq_leaf,
+                    n * static_cast<size_t>(b->nx * b->nx + b->nx) * sizeof(double));
       }
-      ck(cudaMemcpyAsync(b->x0.as<double>() + static_cast<size_t>(i) * align2(static_cast<size_t>(b->nx)),
-                         m.initial_state, static_cast<size_t>(b->nx) * sizeof(double), cudaMemcpyHostToDevice, s),
-         "h2d");
-      bytes += static_cast<size_t>(b->nx) * sizeof(double);
+      std::memcpy(hx0 + i * x0s, m.initial_state, static_cast<size_t>(b->nx) * sizeof(double));
     }
+    const size_t bytes_data = C * b->node_data_doubles * sizeof(double);
+    ck(cudaMemcpyAsync(b->model_data.p, hs, bytes_data, cudaMemcpyHostToDevice, s), "h2d");
+    ck(cudaMemcpyAsync(b->x0.p, hx0, C * x0s * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
     ck(cudaMemcpyAsync(b->mps.p, b->h_mps.data(), b->h_mps.size() * sizeof(ModelParams), cudaMemcpyHostToDevice, s),
        "h2d");
-    bytes += b->h_mps.size() * sizeof(ModelParams);
-    if (h2d_bytes) *h2d_bytes = bytes;
+    if (h2d_bytes) *h2d_bytes = bytes_data + C * x0s * sizeof(double) + b->h_mps.size() * sizeof(ModelParams);
     return BMPC_OK;
   } catch (const std::exception& e) {
     return fail(BMPC_ERR_CUDA, e.what());
@@ -1066,28 +1071,32 @@ int bmpc_batch_results(bmpc_batch* b, double* x_out, double* u_out, bmpc_report*
     ck(cudaSetDevice(b->ctx->device), "cudaSetDevice");
     cudaStream_t s = b->ctx->stream;
     const size_t n = static_cast<size_t>(b->plan->n);
+    const size_t C = static_cast<size_t>(b->count);
+    const size_t per = n * static_cast<size_t>(b->nx + b->nu);
     size_t bytes = 0;
-    std::vector<DevResult> res(static_cast<size_t>(b->count));
-    ck(cudaMemcpyAsync(res.data(), b->results.p, res.size() * sizeof(DevResult), cudaMemcpyDeviceToHost, s), "d2h");
-    bytes += res.size() * sizeof(DevResult);
-    for (int i = 0; i < b->count; ++i) {
-      const Work& w = b->h_works[static_cast<size_t>(i)];
-      if (x_out) {
-        ck(cudaMemcpyAsync(x_out + static_cast<size_t>(i) * n * b->nx, w.x, n * b->nx * sizeof(double),
-                           cudaMemcpyDeviceToHost, s),
-           "d2h");
-        bytes += n * b->nx * sizeof(double);
-      }
-      if (u_out) {
-        ck(cudaMemcpyAsync(u_out + static_cast<size_t>(i) * n * b->nu, w.u, n * b->nu * sizeof(double),
-                           cudaMemcpyDeviceToHost, s),
-           "d2h");
-        bytes += n * b->nu * sizeof(double);
-      }
+    std::vector<DevResult> res(C);
+    ck(cudaMemcpyAsync(res.data(), b->results.p, C * sizeof(DevResult), cudaMemcpyDeviceToHost, s), "d2h");
+    bytes += C * sizeof(DevResult);
+    if (x_out || u_out) {
+      // Pack [x | u] of every instance on device, ONE device-to-host copy.
+      if (!b->d_pack.p) b->d_pack = DevBuf(C * per * sizeof(double));
+      if (!b->h_pack) ck(cudaMallocHost(&b->h_pack, C * per * sizeof(double)), "pinned");
+      ck(launch_pack_results(b->works.as<Work>(), b->count, b->plan->n, b->nx, b->nu, b->d_pack.as<double>(), s),
+         "pack");
+      ++b->ctx->launches;
+      ck(cudaMemcpyAsync(b->h_pack, b->d_pack.p, C * per * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+      bytes += C * per * sizeof(double);
     }
     ck(cudaStreamSynchronize(s), "sync");
+    if (x_out || u_out) {
+      for (size_t i = 0; i < C; ++i) {
+        const double* src = b->h_pack + i * per;
+        if (x_out) std::memcpy(x_out + i * n * b->nx, src, n * b->nx * sizeof(double));
+        if (u_out) std::memcpy(u_out + i * n * b->nu, src + n * b->nx, n * b->nu * sizeof(double));
+      }
+    }
     if (reports)
-      for (int i = 0; i < b->count; ++i) fill_report(res[static_cast<size_t>(i)], &reports[i]);
+      for (size_t i = 0; i < C; ++i) fill_report(res[i], &reports[i]);
     if (d2h_bytes) *d2h_bytes = bytes;
     return BMPC_OK;
   } catch (const std::exception& e) {
