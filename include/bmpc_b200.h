@@ -152,6 +152,10 @@ int bmpc_ctx_create(int device, bmpc_ctx** out);
 void bmpc_ctx_destroy(bmpc_ctx* ctx);
 int bmpc_ctx_set_stream(bmpc_ctx* ctx, void* cuda_stream); /* cudaStream_t; NULL = ctx-owned stream */
 int bmpc_ctx_synchronize(bmpc_ctx* ctx);
+/* Backward/forward strategy per tree segment: segments of at most `len`
+ * nodes use the team-cooperative sequential Riccati sweep, longer ones the
+ * associative scan (0 = scan everywhere; default 64, env BMPC_SEQ_MAX). */
+int bmpc_ctx_set_seq_max_len(bmpc_ctx* ctx, int len);
 /* Number of kernels this ctx launched since creation (evidence counter). */
 long long bmpc_ctx_launch_count(const bmpc_ctx* ctx);
 
@@ -201,6 +205,14 @@ int bmpc_batch_info(const bmpc_batch* batch, int* threads_per_block, int* blocks
 /* Measured FP64 FMA throughput of this device (TFLOP/s): the roofline
  * denominator of the FP64-bound solve path. */
 int bmpc_fp64_peak_tflops(bmpc_ctx* ctx, double* tflops);
+/* Diagnostic per-phase device timers (ns accumulated by the solve loop):
+ * slots 0 linearize+evaluate, 1 backward terminals/elements, 2 backward
+ * scans, 3 feedback, 4 forward elements, 5 forward scans, 6 forward sweep,
+ * 7 line search, 8 merit/convergence, 9 step/AL bookkeeping. */
+int bmpc_batch_set_profiling(bmpc_batch* batch, int on);
+int bmpc_batch_phase_profile(bmpc_batch* batch, int instance, double* out, int n);
+/* Diagnostic: microseconds per cooperative grid barrier at this launch shape. */
+int bmpc_debug_grid_sync_us(bmpc_ctx* ctx, int blocks, int threads, int iters, double* us);
 
 /* ---------------------------------------------- kernel-level LQR tree */
 /* backward_pass + linear_rollout + expected_change_coefficients

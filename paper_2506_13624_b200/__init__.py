@@ -518,3 +518,32 @@ def fp64_peak_tflops(ctx: Optional[Context] = None) -> float:
 
 def version() -> str:
     return lib().bmpc_version().decode()
+
+
+def debug_grid_sync_us(blocks: int, threads: int, iters: int = 2000, ctx: Optional[Context] = None) -> float:
+    """Microseconds per cooperative grid barrier at this launch shape."""
+    ctx = ctx or default_context()
+    v = C.c_double()
+    _check(lib().bmpc_debug_grid_sync_us(ctx._h, int(blocks), int(threads), int(iters), C.byref(v)))
+    return v.value
+
+
+PHASES = ("linearize", "bwd_terminal_elements", "bwd_scan", "feedback", "fwd_elements", "fwd_scan", "fwd_sweep",
+          "line_search", "merit", "step_al")
+
+
+def batch_phase_profile(batch: "Batch", instance: int = 0) -> dict:
+    """Per-phase device time (ms) of one instance after a profiled solve."""
+    out = np.zeros(16)
+    _check(lib().bmpc_batch_phase_profile(batch._h, int(instance), _ptr(out), 16))
+    return {name: out[i] * 1e-6 for i, name in enumerate(PHASES)}
+
+
+def batch_set_profiling(batch: "Batch", on: bool = True):
+    _check(lib().bmpc_batch_set_profiling(batch._h, int(on)))
+
+
+def set_seq_max_len(ctx: Context, length: int):
+    """Segments of <= length nodes use the team Riccati sweep, longer ones the
+    associative scan (0 = scan everywhere)."""
+    _check(lib().bmpc_ctx_set_seq_max_len(ctx._h, int(length)))

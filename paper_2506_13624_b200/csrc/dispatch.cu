@@ -47,7 +47,9 @@ Strides strides_for(int nx, int nu) {
 // Launch-shape variants (threads, min blocks/SM) of the per-instance kernel.
 #define BMPC_CTA_VARIANTS(X)                                                                   \
   X(4, 2, 256, 1) X(4, 2, 128, 2) X(4, 2, 64, 4) X(4, 2, 128, 3) X(4, 2, 64, 6) X(4, 2, 128, 4) \
-  X(4, 2, 64, 8) X(3, 2, 256, 1) X(3, 2, 64, 4) X(2, 1, 256, 1) X(2, 1, 64, 4)
+  X(4, 2, 64, 8) X(4, 2, 256, 2) X(4, 2, 512, 1) X(4, 2, 1024, 1) X(4, 2, 256, 3) \
+  X(4, 2, 256, 4) X(4, 2, 128, 6) X(4, 2, 128, 8) X(4, 2, 512, 2) X(3, 2, 256, 1) X(3, 2, 64, 4) \
+  X(2, 1, 256, 1) X(2, 1, 64, 4)
 
 #define X(a, b, t, m) extern template struct CtaVariant<a, b, t, m>;
 BMPC_CTA_VARIANTS(X)
@@ -98,10 +100,10 @@ int solve_grid_blocks(int nx, int nu, int threads) {
 }
 
 cudaError_t launch_lqr_tree(int nx, int nu, bool grid, const Topo* d_topo, const Work* d_work, double reg,
-                            double* d_scalars, double* red, int blocks, int threads, cudaStream_t stream) {
+                            double* d_scalars, double* red, int blocks, int threads, cudaStream_t stream, int seq_max) {
 #define X(a, b)           \
   if (nx == a && nu == b) \
-    return LqrLaunch<a, b>::lqr_tree(grid, d_topo, d_work, reg, d_scalars, red, blocks, threads, stream);
+    return LqrLaunch<a, b>::lqr_tree(grid, d_topo, d_work, reg, d_scalars, red, blocks, threads, stream, seq_max);
   BMPC_LQR_DIMS(X)
 #undef X
   return cudaErrorInvalidValue;

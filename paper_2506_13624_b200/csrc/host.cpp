@@ -609,12 +609,21 @@ void fill_report(const DevResult& r, bmpc_report* out) {
 
 // ================================================================== C ABI
 struct bmpc_ctx {
+  int seq_max_len{-1};  // segments <= this length use the team Riccati sweep (-1: default)
   int device{0};
   cudaStream_t stream{nullptr};
   bool own_stream{false};
   long long launches{0};
   int sms{0};
 };
+
+// Crossover between the team Riccati sweep and the scan (segment length).
+// Measured on B200: the O(L) sweep wins below a few hundred nodes.
+static int seq_max_for(const bmpc_ctx* c) {
+  if (c && c->seq_max_len >= 0) return c->seq_max_len;
+  if (const char* env = std::getenv("BMPC_SEQ_MAX")) return std::atoi(env);
+  return 64;
+}
 
 // Device-resident instances sharing one plan.
 struct bmpc_batch {
@@ -623,7 +632,7 @@ struct bmpc_batch {
   int count{0}, nx{0}, nu{0}, kind{0}, nv{0}, max_records{0};
   size_t node_data_doubles{0};  // per instance: reference+vehicles or lq stage+leaf
   Strides st{};
-  DevBuf model_data, x0, state, records, results, mps, works, red;
+  DevBuf model_data, x0, state, records, results, mps, works, red, prof;
   std::vector<ModelParams> h_mps;
   std::vector<Work> h_works;
   size_t per_state_doubles{0};
@@ -649,9 +658,9 @@ size_t align2(size_t v) { return (v + 1) & ~size_t{1}; }
 // the tuned default.
 void default_launch_shape(bmpc_batch* b) {
   int t = 256, m = 1;
-  if (b->nx == 4 && b->nu == 2) {
-    t = 256;
-    m = 1;
+  if (b->nx == 4 && b->nu == 2 && b->count > 1) {  // batches: more resident instances per SM
+    t = 128;
+    m = 4;
   }
   if (const char* env = std::getenv("BMPC_CTA")) {
     int et = 0, em = 0;
@@ -820,6 +829,12 @@ void bmpc_ctx_destroy(bmpc_ctx* c) {
   delete c;
 }
 
+int bmpc_ctx_set_seq_max_len(bmpc_ctx* c, int len) {
+  if (!c) return fail(BMPC_ERR_INVALID, "null ctx");
+  c->seq_max_len = len;
+  return BMPC_OK;
+}
+
 int bmpc_ctx_set_stream(bmpc_ctx* c, void* stream) {
   if (!c) return fail(BMPC_ERR_INVALID, "null ctx");
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -911,6 +926,7 @@ int bmpc_batch_create(bmpc_ctx* ctx, const bmpc_tree* tree, int count, const bmp
       w.records = b->records.as<DevRecord>() + i * static_cast<size_t>(std::max(b->max_records, 1));
       w.max_records = b->max_records;
       w.result = b->results.as<DevResult>() + i;
+      w.prof = nullptr;
     }
     ck(cudaMemcpyAsync(b->works.p, b->h_works.data(), C * sizeof(Work), cudaMemcpyHostToDevice, ctx->stream), "works");
     *out = b.release();
@@ -1042,6 +1058,7 @@ static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_input
     bmpc_options_default(&o);
   DevOptions d = to_dev(o);
   d.zero_inputs = zero_inputs ? 1 : 0;
+  d.seq_max_len = seq_max_for(b->ctx);
   cudaError_t e;
   if (b->grid_mode) {
     e = launch_solve_grid(b->nx, b->nu, b->plan->d_topo.as<Topo>(), b->mps.as<ModelParams>(), b->works.as<Work>(), d,
@@ -1123,6 +1140,43 @@ int bmpc_batch_pack_results(bmpc_batch* b, double* d_dst, size_t* bytes) {
   ++b->ctx->launches;
   if (bytes) *bytes = static_cast<size_t>(b->count) * b->plan->n * (b->nx + b->nu) * sizeof(double);
   return BMPC_OK;
+}
+
+int bmpc_debug_grid_sync_us(bmpc_ctx* ctx, int blocks, int threads, int iters, double* us) {
+  if (!ctx || !us) return fail(BMPC_ERR_INVALID, "null argument");
+  cudaSetDevice(ctx->device);
+  *us = grid_sync_us(blocks, threads, iters, ctx->stream);
+  return cudaGetLastError() == cudaSuccess ? BMPC_OK : fail(BMPC_ERR_CUDA, "grid sync benchmark failed");
+}
+
+int bmpc_batch_set_profiling(bmpc_batch* b, int on) {
+  try {
+    if (!b) return fail(BMPC_ERR_INVALID, "null argument");
+    cudaSetDevice(b->ctx->device);
+    const size_t C = static_cast<size_t>(b->count);
+    if (on && !b->prof.p) b->prof = DevBuf(C * kProfSlots * sizeof(double));
+    if (on) ck(cudaMemsetAsync(b->prof.p, 0, C * kProfSlots * sizeof(double), b->ctx->stream), "memset");
+    for (size_t i = 0; i < C; ++i) b->h_works[i].prof = on ? b->prof.as<double>() + i * kProfSlots : nullptr;
+    ck(cudaMemcpyAsync(b->works.p, b->h_works.data(), C * sizeof(Work), cudaMemcpyHostToDevice, b->ctx->stream),
+       "works");
+    return BMPC_OK;
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
+}
+
+int bmpc_batch_phase_profile(bmpc_batch* b, int instance, double* out, int n) {
+  try {
+    if (!b || !out || !b->prof.p || instance < 0 || instance >= b->count) return fail(BMPC_ERR_INVALID, "bad args");
+    double tmp[kProfSlots];
+    ck(cudaMemcpy(tmp, b->prof.as<double>() + static_cast<size_t>(instance) * kProfSlots, sizeof tmp,
+                  cudaMemcpyDeviceToHost),
+       "d2h");
+    for (int k = 0; k < n && k < kProfSlots; ++k) out[k] = tmp[k];
+    return BMPC_OK;
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
 }
 
 int bmpc_fp64_peak_tflops(bmpc_ctx* ctx, double* tflops) {
@@ -1249,7 +1303,7 @@ int bmpc_lqr_tree(bmpc_ctx* ctx, const bmpc_tree* tree, int nx, int nu, const do
       red = DevBuf(2 * static_cast<size_t>(std::max(blocks, 1)) * kRedSlotsHost * sizeof(double));
     }
     ck(launch_lqr_tree(nx, nu, grid != 0, plan->d_topo.as<Topo>(), d_work.as<Work>(), reg, d_sc.as<double>(),
-                       red.as<double>(), blocks, 256, s),
+                       red.as<double>(), blocks, 256, s, seq_max_for(ctx)),
        "lqr launch");
     ++ctx->launches;
     ck(cudaMemcpyAsync(h.data(), d_state.p, per * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");

@@ -29,7 +29,7 @@ template <int NX, int NU>
 struct LqrLaunch {
   static Strides strides();
   static cudaError_t lqr_tree(bool grid, const Topo* d_topo, const Work* d_work, double reg, double* d_scalars,
-                              double* red, int blocks, int threads, cudaStream_t stream);
+                              double* red, int blocks, int threads, cudaStream_t stream, int seq_max);
   static int grid_blocks(int threads);
 };
 
@@ -64,7 +64,7 @@ cudaError_t launch_solve_grid(int nx, int nu, const Topo* d_topo, const ModelPar
 int solve_grid_blocks(int nx, int nu, int threads);
 int solve_cta_regs(int nx, int nu, int threads, int min_blocks);
 cudaError_t launch_lqr_tree(int nx, int nu, bool grid, const Topo* d_topo, const Work* d_work, double reg,
-                            double* d_scalars, double* red, int blocks, int threads, cudaStream_t stream);
+                            double* d_scalars, double* red, int blocks, int threads, cudaStream_t stream, int seq_max);
 int lqr_grid_blocks(int nx, int nu, int threads);
 
 size_t sizeof_topo();
@@ -79,5 +79,6 @@ constexpr int kRedSlotsHost = 64;
 cudaError_t launch_pack_results(const Work* d_works, int count, int n, int nx, int nu, double* dst,
                                 cudaStream_t stream);
 double measure_fp64_peak_tflops(cudaStream_t stream);
+double grid_sync_us(int blocks, int threads, int iters, cudaStream_t stream);
 
 }  // namespace bmpc_b200

@@ -11,6 +11,10 @@ namespace bmpc_b200 {
 
 static_assert(kRedSlotsHost == kRedSlots, "reduction slot count mismatch");
 
+__host__ __device__ constexpr size_t red_smem_bytes(int threads) {
+  return ((static_cast<size_t>(kRedSlots) * (threads / 32) * sizeof(double)) + 15) / 16 * 16;
+}
+
 // Stage the per-instance structs in shared memory (read on every node op).
 struct BlockCtx {
   Topo topo;
@@ -35,10 +39,11 @@ __global__ void __launch_bounds__(THREADS, MINB) solve_cta_kernel(const Topo* __
     ctx.work = works[b];
     red.flag = 0;
   }
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  red.part = reinterpret_cast<double*>(dyn_smem);
   __syncthreads();
-  __shared__ TeamSmem<NX> tsm[THREADS / (team_size<NX>() > 0 ? team_size<NX>() : THREADS)];
   Solver<NX, NU, CtaGroup> s(CtaGroup{&red}, ctx.topo, ctx.mp, ctx.work, opts);
-  s.tsm = tsm;
+  s.tsm = dyn_smem + red_smem_bytes(blockDim.x);
   s.solve();
 }
 
@@ -55,26 +60,28 @@ __global__ void __launch_bounds__(256) solve_grid_kernel(const Topo* __restrict_
     ctx.work = works[0];
     red.flag = 0;
   }
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  red.part = reinterpret_cast<double*>(dyn_smem);
   __syncthreads();
-  __shared__ TeamSmem<NX> tsm[256 / (team_size<NX>() > 0 ? team_size<NX>() : 256)];
   Solver<NX, NU, GridGroup> s(GridGroup{&red, red_scratch, nullptr}, ctx.topo, ctx.mp, ctx.work, opts);
-  s.tsm = tsm;
+  s.tsm = dyn_smem + red_smem_bytes(blockDim.x);
   s.solve();
 }
 
 template <int NX, int NU, class G>
-__device__ void lqr_tree_body(G g, BlockCtx& ctx, double reg, double* scalars) {
+__device__ void lqr_tree_body(G g, BlockCtx& ctx, double reg, double* scalars, int seq_max) {
   ModelParams dummy{};
   DevOptions o{};
-  __shared__ TeamSmem<NX> tsm[256 / (team_size<NX>() > 0 ? team_size<NX>() : 256)];
+  o.seq_max_len = seq_max;
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
   Solver<NX, NU, G> s(g, ctx.topo, dummy, ctx.work, o);
-  s.tsm = tsm;
+  s.tsm = dyn_smem + red_smem_bytes(blockDim.x);
   s.lqr_tree(reg, scalars);
 }
 
 template <int NX, int NU>
 __global__ void __launch_bounds__(256) lqr_tree_cta_kernel(const Topo* topo, const Work* works, double reg,
-                                                           double* scalars) {
+                                                           double* scalars, int seq_max) {
   __shared__ RedSmem red;
   __shared__ BlockCtx ctx;
   if (threadIdx.x == 0) {
@@ -82,13 +89,15 @@ __global__ void __launch_bounds__(256) lqr_tree_cta_kernel(const Topo* topo, con
     ctx.work = works[0];
     red.flag = 0;
   }
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  red.part = reinterpret_cast<double*>(dyn_smem);
   __syncthreads();
-  lqr_tree_body<NX, NU>(CtaGroup{&red}, ctx, reg, scalars);
+  lqr_tree_body<NX, NU>(CtaGroup{&red}, ctx, reg, scalars, seq_max);
 }
 
 template <int NX, int NU>
 __global__ void __launch_bounds__(256) lqr_tree_grid_kernel(const Topo* topo, const Work* works, double reg,
-                                                            double* scalars, double* red_scratch) {
+                                                            double* scalars, double* red_scratch, int seq_max) {
   __shared__ RedSmem red;
   __shared__ BlockCtx ctx;
   if (threadIdx.x == 0) {
@@ -96,17 +105,34 @@ __global__ void __launch_bounds__(256) lqr_tree_grid_kernel(const Topo* topo, co
     ctx.work = works[0];
     red.flag = 0;
   }
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  red.part = reinterpret_cast<double*>(dyn_smem);
   __syncthreads();
-  lqr_tree_body<NX, NU>(GridGroup{&red, red_scratch, nullptr}, ctx, reg, scalars);
+  lqr_tree_body<NX, NU>(GridGroup{&red, red_scratch, nullptr}, ctx, reg, scalars, seq_max);
 }
 
 
+// Dynamic shared memory of one block: reduction warp partials, then the
+// cooperative-combine team scratch.
+template <int NX, int NU>
+static size_t team_smem_bytes(int threads) {
+  constexpr int ts = team_size<NX, NU>();
+  return red_smem_bytes(threads) + (ts > 0 ? static_cast<size_t>(threads / ts) * (sizeof(TeamSmem<NX>) > sizeof(RicSmem<NX, NU>) ? sizeof(TeamSmem<NX>) : sizeof(RicSmem<NX, NU>)) : 16);
+}
+
 template <class K>
-static int max_coresident(K kernel, int threads) {
+static void allow_smem(K kernel, size_t bytes) {
+  cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(bytes));
+}
+
+template <class K>
+static int max_coresident(K kernel, int threads, size_t smem) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+  allow_smem(kernel, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
   return sms * per_sm;
 }
 
@@ -138,26 +164,31 @@ Strides LqrLaunch<NX, NU>::strides() {
 template <int NX, int NU>
 cudaError_t LqrLaunch<NX, NU>::lqr_tree(bool grid, const Topo* d_topo, const Work* d_work, double reg,
                                         double* d_scalars, double* red, int blocks, int threads,
-                                        cudaStream_t stream) {
+                                        cudaStream_t stream, int seq_max) {
+  const size_t smem = team_smem_bytes<NX, NU>(threads);
   if (!grid) {
-    lqr_tree_cta_kernel<NX, NU><<<1, threads, 0, stream>>>(d_topo, d_work, reg, d_scalars);
+    allow_smem(lqr_tree_cta_kernel<NX, NU>, smem);
+    lqr_tree_cta_kernel<NX, NU><<<1, threads, smem, stream>>>(d_topo, d_work, reg, d_scalars, seq_max);
     return cudaGetLastError();
   }
-  void* args[] = {&d_topo, &d_work, &reg, &d_scalars, &red};
-  const int nb = blocks > 0 ? blocks : max_coresident(lqr_tree_grid_kernel<NX, NU>, threads);
+  void* args[] = {&d_topo, &d_work, &reg, &d_scalars, &red, &seq_max};
+  const int nb = blocks > 0 ? blocks : max_coresident(lqr_tree_grid_kernel<NX, NU>, threads, smem);
   return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lqr_tree_grid_kernel<NX, NU>), dim3(nb),
-                                     dim3(threads), args, 0, stream);
+                                     dim3(threads), args, smem, stream);
 }
 
 template <int NX, int NU>
 int LqrLaunch<NX, NU>::grid_blocks(int threads) {
-  return max_coresident(lqr_tree_grid_kernel<NX, NU>, threads);
+  return max_coresident(lqr_tree_grid_kernel<NX, NU>, threads, team_smem_bytes<NX, NU>(threads));
 }
 
 template <int NX, int NU, int T, int MB>
 cudaError_t CtaVariant<NX, NU, T, MB>::launch(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
                                               const DevOptions& opts, int count, cudaStream_t stream) {
-  solve_cta_kernel<NX, NU, T, MB><<<count, T, 0, stream>>>(d_topo, d_mp, d_work, opts, count);
+  const size_t smem = team_smem_bytes<NX, NU>(T);
+  static bool once = (allow_smem(solve_cta_kernel<NX, NU, T, MB>, smem), true);
+  (void)once;
+  solve_cta_kernel<NX, NU, T, MB><<<count, T, smem, stream>>>(d_topo, d_mp, d_work, opts, count);
   return cudaGetLastError();
 }
 
@@ -174,13 +205,15 @@ cudaError_t SolveLaunch<NX, NU>::solve_grid(const Topo* d_topo, const ModelParam
                                             cudaStream_t stream) {
   DevOptions o = opts;
   void* args[] = {&d_topo, &d_mp, &d_work, &o, &red};
+  const size_t smem = team_smem_bytes<NX, NU>(threads);
+  allow_smem(solve_grid_kernel<NX, NU>, smem);
   return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(solve_grid_kernel<NX, NU>), dim3(blocks),
-                                     dim3(threads), args, 0, stream);
+                                     dim3(threads), args, smem, stream);
 }
 
 template <int NX, int NU>
 int SolveLaunch<NX, NU>::grid_blocks(int threads) {
-  return max_coresident(solve_grid_kernel<NX, NU>, threads);
+  return max_coresident(solve_grid_kernel<NX, NU>, threads, team_smem_bytes<NX, NU>(threads));
 }
 
 

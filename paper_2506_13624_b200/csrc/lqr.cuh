@@ -481,4 +481,162 @@ __device__ void combine_fwd(const double* f1, const double* f2, double* out) {  
   copy<NX>(c, out + F::c);
 }
 
+// ---------------------------------------------------------------------------
+// Team-cooperative sequential Riccati sweep along one segment (short
+// segments, where the O(L) recursion beats the O(L log L)-work scan). One
+// step is riccati_step (riccati.hpp:22-43) with the continuation (P, p + P c)
+// of the successor — for single-child nodes exactly feedback_from_values
+// (lqr_scan.hpp:146-157) plus the value update; for a branch node the summed
+// children (riccati.hpp:112-116). TS lanes, entries distributed as in
+// team_combine_bwd; (P, p) stay in shared memory between steps.
+template <int NX, int NU>
+struct RicSmem {
+  double s[StageLayout<NX, NU>::size];
+  double P[NX * NX], p[NX], c[NX], psh[NX];
+  double BtP[NU * NX], AtP[NX * NX], Qxx[NX * NX], Quu[NU * NU], Qux[NU * NX], qx[NX], qu[NU];
+  double K[NU * NX], k[NU];
+};
+
+// Loads the stage record of `node` and the edge offset c (nullptr: zero).
+template <int NX, int NU, int TS>
+__device__ __forceinline__ void ric_load(const double* stage_g, const double* c_g, int lane, RicSmem<NX, NU>& sm) {
+  using L = StageLayout<NX, NU>;
+  for (int t = lane; t < L::size; t += TS) sm.s[t] = stage_g[t];
+  if (lane < NX) sm.c[lane] = c_g ? c_g[lane] : 0.0;
+}
+
+// One Bellman step on the staged stage/c/(P, p); overwrites (P, p) with the
+// node's value and writes value / policy to global memory. Returns an error
+// code (kIndefinite when R + B'PB is not positive definite).
+template <int NX, int NU, int TS>
+__device__ int team_riccati_step(double reg, int lane, unsigned mask, RicSmem<NX, NU>& sm, double* V_g, double* K_g,
+                                 double* k_g) {
+  using L = StageLayout<NX, NU>;
+  constexpr int N2 = NX * NX;
+  const double* s = sm.s;
+  __syncwarp(mask);
+  // p_shifted = p + P c ; B'P ; A'P
+  if (lane < NX) {
+    double a = sm.p[lane];
+#pragma unroll
+    for (int l = 0; l < NX; ++l) a = fma(sm.P[lane + l * NX], sm.c[l], a);
+    sm.psh[lane] = a;
+  }
+  if (lane < NU * NX) {
+    const int a = lane % NU, j = lane / NU;
+    double v = 0.0;
+#pragma unroll
+    for (int l = 0; l < NX; ++l) v = fma(s[L::B + l + a * NX], sm.P[l + j * NX], v);
+    sm.BtP[lane] = v;
+  }
+  if (lane < N2) {
+    const int i = lane % NX, j = lane / NX;
+    double v = 0.0;
+#pragma unroll
+    for (int l = 0; l < NX; ++l) v = fma(s[L::A + l + i * NX], sm.P[l + j * NX], v);
+    sm.AtP[lane] = v;
+  }
+  __syncwarp(mask);
+  // Qxx, Quu (+reg), Qux, qx, qu
+  if (lane < N2) {
+    const int i = lane % NX, j = lane / NX;
+    double v = s[L::Q + lane];
+#pragma unroll
+    for (int l = 0; l < NX; ++l) v = fma(sm.AtP[i + l * NX], s[L::A + l + j * NX], v);
+    sm.Qxx[lane] = v;
+  }
+  if (lane < NU * NX) {
+    const int a = lane % NU, j = lane / NU;
+    double v = s[L::M + lane];
+#pragma unroll
+    for (int l = 0; l < NX; ++l) v = fma(sm.BtP[a + l * NU], s[L::A + l + j * NX], v);
+    sm.Qux[lane] = v;
+  }
+  if (lane < NU * NU) {
+    const int a = lane % NU, b = lane / NU;
+    double v = s[L::R + lane] + (a == b ? reg : 0.0);
+#pragma unroll
+    for (int l = 0; l < NX; ++l) v = fma(sm.BtP[a + l * NU], s[L::B + l + b * NX], v);
+    sm.Quu[lane] = v;
+  }
+  if (lane < NX) {
+    double v = s[L::q + lane];
+#pragma unroll
+    for (int l = 0; l < NX; ++l) v = fma(s[L::A + l + lane * NX], sm.psh[l], v);
+    sm.qx[lane] = v;
+  }
+  if (lane < NU) {
+    double v = s[L::r + lane];
+#pragma unroll
+    for (int l = 0; l < NX; ++l) v = fma(s[L::B + l + lane * NX], sm.psh[l], v);
+    sm.qu[lane] = v;
+  }
+  __syncwarp(mask);
+  // Huu = sym(Quu); LDLT; K = -Huu^-1 Qux, k = -Huu^-1 qu (every lane factors).
+  bool pos;
+  {
+    double H[NU * NU];
+#pragma unroll
+    for (int t = 0; t < NU * NU; ++t) H[t] = sm.Quu[t];
+    symmetrize<NU>(H);
+    Ldlt<NU> f;
+    f.compute(H);
+    pos = f.positive();
+    if (lane < NU * NX) {
+      const int a = lane % NU, j = lane / NU;
+      double col[NU];
+#pragma unroll
+      for (int t = 0; t < NU; ++t) col[t] = sm.Qux[t + j * NU];
+      f.template solve<1>(col);
+      double v = col[0];
+#pragma unroll
+      for (int t = 1; t < NU; ++t) v = (t == a) ? col[t] : v;
+      sm.K[lane] = -v;
+      if (K_g) K_g[lane] = -v;
+    }
+    if (lane >= NU * NX && lane < NU * NX + NU) {
+      const int a = lane - NU * NX;
+      double col[NU];
+#pragma unroll
+      for (int t = 0; t < NU; ++t) col[t] = sm.qu[t];
+      f.template solve<1>(col);
+      double v = col[0];
+#pragma unroll
+      for (int t = 1; t < NU; ++t) v = (t == a) ? col[t] : v;
+      sm.k[a] = -v;
+      if (k_g) k_g[a] = -v;
+    }
+  }
+  __syncwarp(mask);
+  // P = sym(Qxx + Qux' K), p = qx + Qux' k
+  double Pij = 0.0, pi = 0.0;
+  if (lane < N2) {
+    const int i = lane % NX, j = lane / NX;
+    double a = sm.Qxx[lane], b = sm.Qxx[j + i * NX];
+#pragma unroll
+    for (int t = 0; t < NU; ++t) {
+      a = fma(sm.Qux[t + i * NU], sm.K[t + j * NU], a);
+      b = fma(sm.Qux[t + j * NU], sm.K[t + i * NU], b);
+    }
+    Pij = 0.5 * (a + b);
+  }
+  if (lane < NX) {
+    double v = sm.qx[lane];
+#pragma unroll
+    for (int t = 0; t < NU; ++t) v = fma(sm.Qux[t + lane * NU], sm.k[t], v);
+    pi = v;
+  }
+  __syncwarp(mask);
+  if (lane < N2) {
+    sm.P[lane] = Pij;
+    if (V_g) V_g[ValueLayout<NX>::P + lane] = Pij;
+  }
+  if (lane < NX) {
+    sm.p[lane] = pi;
+    if (V_g) V_g[ValueLayout<NX>::p + lane] = pi;
+  }
+  const unsigned bad = __ballot_sync(mask, !pos);
+  return bad ? kIndefinite : kBwdOk;
+}
+
 }  // namespace bmpc_b200

@@ -34,7 +34,7 @@ namespace bmpc_b200 {
 namespace cg = cooperative_groups;
 
 constexpr int kRedSlots = 4 * kMaxAlpha;  // largest simultaneous reduction
-constexpr int kMaxWarps = 8;  // blocks of <= 256 threads
+constexpr int kMaxWarps = 32;  // blocks of <= 1024 threads
 
 // Scan level bookkeeping (scan.hpp:19-36): n_0 = E, n_{l+1} = ceil(n_l / 2).
 __device__ __forceinline__ int level_size(int E, int l) {
@@ -56,10 +56,12 @@ __host__ __device__ __forceinline__ int up_steps(int E) {
   return u;
 }
 
-// Lanes per cooperative combine_bwd team (0 = one thread per combination).
-template <int NX>
+// Lanes per cooperative team (combine_bwd needs NX*NX, the Riccati step
+// NU*NX + NU); 0 = one thread per combination, scan path only.
+template <int NX, int NU>
 __host__ __device__ constexpr int team_size() {
-  return NX * NX <= 4 ? 4 : (NX * NX <= 16 ? 16 : (NX * NX <= 32 ? 32 : 0));
+  constexpr int need = NX * NX > NU * NX + NU ? NX * NX : NU * NX + NU;
+  return need <= 4 ? 4 : (need <= 16 ? 16 : (need <= 32 ? 32 : 0));
 }
 
 // ------------------------------------------------------------------ groups
@@ -75,7 +77,7 @@ __device__ __forceinline__ double warp_max(double v) {
 }
 
 struct RedSmem {
-  double part[kRedSlots][kMaxWarps];
+  double* part;  // [kRedSlots][nwarps] warp partials (dynamic shared memory)
   double total[kRedSlots];
   int flag;
 };
@@ -94,8 +96,9 @@ struct CtaGroup {
     __syncthreads();
     const int nw = (blockDim.x + 31) >> 5;
     for (int k = threadIdx.x; k < nslot; k += blockDim.x) {
-      double a = sm->part[k][0];
-      for (int w = 1; w < nw; ++w) a = k < nsum ? a + sm->part[k][w] : fmax(a, sm->part[k][w]);
+      const double* pk = sm->part + k * nw;
+      double a = pk[0];
+      for (int w = 1; w < nw; ++w) a = k < nsum ? a + pk[w] : fmax(a, pk[w]);
       sm->total[k] = a;
     }
     __syncthreads();
@@ -116,8 +119,9 @@ struct GridGroup {
     const int buf = sm->flag & 1;
     double* out = scratch + (static_cast<size_t>(buf) * gridDim.x + blockIdx.x) * kRedSlots;
     for (int k = threadIdx.x; k < nslot; k += blockDim.x) {
-      double a = sm->part[k][0];
-      for (int w = 1; w < nw; ++w) a = k < nsum ? a + sm->part[k][w] : fmax(a, sm->part[k][w]);
+      const double* pk = sm->part + k * nw;
+      double a = pk[0];
+      for (int w = 1; w < nw; ++w) a = k < nsum ? a + pk[w] : fmax(a, pk[w]);
       out[k] = a;
     }
     cg::this_grid().sync();
@@ -143,7 +147,7 @@ struct GridGroup {
 // Contribute this thread's value to slot k (every thread of the block must call).
 __device__ __forceinline__ void red_put(RedSmem* sm, int k, double v, bool is_sum) {
   v = is_sum ? warp_sum(v) : warp_max(v);
-  if ((threadIdx.x & 31) == 0) sm->part[k][threadIdx.x >> 5] = v;
+  if ((threadIdx.x & 31) == 0) sm->part[k * (blockDim.x >> 5) + (threadIdx.x >> 5)] = v;
 }
 
 // ------------------------------------------------------------------ solver
@@ -161,7 +165,7 @@ struct Solver {
   Work& w;
   const DevOptions& o;
   double g_rho{0.0};  // current AL penalty (uniform across the group)
-  TeamSmem<NX>* tsm{nullptr};  // [blockDim / kTS] team scratch (kernel-provided)
+  void* tsm{nullptr};  // [blockDim / kTS] team scratch slots of slot_bytes() (kernel-provided)
 
   __device__ Solver(G g_, const Topo& t_, const ModelParams& mp_, Work& w_, const DevOptions& o_)
       : g(g_), t(t_), mp(mp_), w(w_), o(o_) {}
@@ -179,6 +183,14 @@ struct Solver {
   __device__ const double* value_of(int i) const {
     const int s = t.node_seg[i];
     return bwd(t.seg_scratch[s] + seg_len(s) - 1 - t.node_pos[i]);
+  }
+  __device__ double* val(int i) const { return w.value + static_cast<size_t>(i) * VL::stride; }
+  // Segments of at most seq_max_len nodes take the team Riccati sweep.
+  __device__ bool seq_len(int L) const { return kTS > 0 && L <= o.seq_max_len; }
+  // (P, p) of node i after the backward pass (either path); P at +0, p at +NX*NX.
+  __device__ const double* value_ptr(int i) const {
+    const int s = t.node_seg[i];
+    return seq_len(seg_len(s)) ? val(i) : value_of(i);
   }
 
   // ------------------------------------------------------ nonlinear rollout
@@ -338,7 +350,7 @@ struct Solver {
   // Backward suffix scan of segments at depth d, elements already in level 0
   // (reversed). f(a, b) = combine_bwd(first = b, second = a).
   // Team size of the cooperative combine (0: one thread per combination).
-  static constexpr int kTS = team_size<NX>();
+  static constexpr int kTS = team_size<NX, NU>();
 
   // Items of a per-segment phase, one kTS-lane team per item.
   template <class F>
@@ -359,7 +371,7 @@ struct Solver {
     const int U = up_steps(E);
     int err = kBwdOk;
     if constexpr (kTS > 0) {
-      TeamSmem<NX>& my = tsm[threadIdx.x / kTS];
+      TeamSmem<NX>& my = comb_smem();
       for (int l = 0; l < U; ++l) {
         const int nl = level_size(E, l), nn = (nl + 1) >> 1;
         const int ol = level_offset(E, l), on = ol + nl;
@@ -436,12 +448,121 @@ struct Solver {
   }
 
   // ---------------------------------------------------- backward pass (B)
+  __device__ unsigned team_mask() const {
+    return kTS == 32 ? 0xffffffffu : (((1u << kTS) - 1u) << ((threadIdx.x & 31) / kTS * kTS));
+  }
+  __device__ RicSmem<NX, NU>& ric_smem() const {
+    return *reinterpret_cast<RicSmem<NX, NU>*>(reinterpret_cast<unsigned char*>(tsm) + (threadIdx.x / kTS) * slot_bytes());
+  }
+  __device__ TeamSmem<NX>& comb_smem() const {
+    return *reinterpret_cast<TeamSmem<NX>*>(reinterpret_cast<unsigned char*>(tsm) + (threadIdx.x / kTS) * slot_bytes());
+  }
+  __host__ __device__ static constexpr size_t slot_bytes() {
+    return sizeof(TeamSmem<NX>) > sizeof(RicSmem<NX, NU>) ? sizeof(TeamSmem<NX>) : sizeof(RicSmem<NX, NU>);
+  }
+
+  // Team Riccati sweep of every (short) segment at depth d: terminal (leaf
+  // cost + reg, or the branch-node step over the summed children), then the
+  // chain nodes tail -> head. Produces values (w.value) and policies.
+  __device__ int riccati_sweep_depth(int d, double reg) {
+    int err = kBwdOk;
+    if constexpr (kTS > 0) {
+      const int L = t.depth_len[d];
+      const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
+      const int team = g.rank() / kTS, nteams = g.size() / kTS, lane = threadIdx.x % kTS;
+      const unsigned mask = team_mask();
+      RicSmem<NX, NU>& sm = ric_smem();
+      for (int s = sb + team; s < se; s += nteams) {
+        const int b = seg_node(s, L - 1);
+        __syncwarp(mask);
+        if (is_leaf(b)) {
+          for (int k = lane; k < NX * NX; k += kTS) {
+            const double v = stage(b)[SL::Q + k] + ((k % (NX + 1)) == 0 ? reg : 0.0);
+            sm.P[k] = v;
+            val(b)[VL::P + k] = v;
+          }
+          for (int k = lane; k < NX; k += kTS) {
+            sm.p[k] = stage(b)[SL::q + k];
+            val(b)[VL::p + k] = sm.p[k];
+          }
+        } else {
+          // riccati_tree_from (riccati.hpp:112-116): children in index order.
+          const int c0 = t.first_child[b], nc = t.nchild[b];
+          for (int k = lane; k < NX * NX; k += kTS) {
+            double a = 0.0;
+            for (int ch = c0; ch < c0 + nc; ++ch) a += value_ptr(ch)[k];
+            sm.P[k] = a;
+          }
+          for (int k = lane; k < NX; k += kTS) {
+            double a = 0.0;
+            for (int ch = c0; ch < c0 + nc; ++ch) {
+              const double* v = value_ptr(ch);
+              double pd = 0.0;
+#pragma unroll
+              for (int l = 0; l < NX; ++l) pd = fma(v[k + l * NX], w.defect[ch * NX + l], pd);
+              a += v[NX * NX + k] + pd;
+            }
+            sm.p[k] = a;
+          }
+          ric_load<NX, NU, kTS>(stage(b), nullptr, lane, sm);
+          const int e = team_riccati_step<NX, NU, kTS>(reg, lane, mask, sm, val(b), pol(b) + PL::K, pol(b) + PL::k);
+          err = err ? err : e;
+        }
+        // Chain nodes tail -> head; the next node's stage record and edge
+        // offset are prefetched into registers while this step computes.
+        constexpr int PRE = (SL::size + kTS - 1) / kTS;
+        if (L >= 2) {
+          __syncwarp(mask);
+          ric_load<NX, NU, kTS>(stage(seg_node(s, L - 2)), w.defect + b * NX, lane, sm);
+        }
+        int nxt = b;
+        for (int k = L - 2; k >= 0; --k) {
+          const int i = seg_node(s, k);
+          double pre[PRE];
+          double prec = 0.0;
+          if (k >= 1) {
+            const double* sp = stage(seg_node(s, k - 1));
+#pragma unroll
+            for (int j = 0; j < PRE; ++j) {
+              const int idx = lane + j * kTS;
+              pre[j] = idx < SL::size ? sp[idx] : 0.0;
+            }
+            if (lane < NX) prec = w.defect[i * NX + lane];
+          }
+          const int e = team_riccati_step<NX, NU, kTS>(reg, lane, mask, sm, val(i), pol(i) + PL::K, pol(i) + PL::k);
+          err = err ? err : e;
+          if (k >= 1) {
+            __syncwarp(mask);
+#pragma unroll
+            for (int j = 0; j < PRE; ++j) {
+              const int idx = lane + j * kTS;
+              if (idx < SL::size) sm.s[idx] = pre[j];
+            }
+            if (lane < NX) sm.c[lane] = prec;
+          }
+          nxt = i;
+        }
+        (void)nxt;
+      }
+    }
+    g.sync();
+    return err;
+  }
+
   // backward_pass (solver.hpp:203-318) with Levenberg shift `reg` on R
-  // (non-leaves) and P (leaves). Returns error code and max_feedforward.
+  // (non-leaves) and P (leaves). Depth levels leaves-first; each level by the
+  // team Riccati sweep (short segments) or the associative scan (long ones).
+  // Returns error code and max_feedforward.
   __device__ int backward(double reg, double* max_ff) {
     int err = kBwdOk;
     for (int d = t.ndepth - 1; d >= 0; --d) {
       const int L = t.depth_len[d];
+      if (seq_len(L)) {
+        const int e = riccati_sweep_depth(d, reg);
+        err = err ? err : e;
+        mark(2);
+        continue;
+      }
       // Terminal of each segment: regularized leaf cost or the branch-node
       // Bellman step over the summed children (riccati.hpp:107-120).
       for_depth_items(d, 1, [&](int s, int) {
@@ -461,13 +582,13 @@ struct Solver {
           for (int j = 0; j < NX; ++j) pn[j] = 0.0;
           const int c0 = t.first_child[b], nc = t.nchild[b];
           for (int ch = c0; ch < c0 + nc; ++ch) {
-            const double* v = value_of(ch);
+            const double* v = value_ptr(ch);
             double Pd[NX];
-            mv<NX, NX>(v + BL::P, w.defect + ch * NX, Pd);
+            mv<NX, NX>(v, w.defect + ch * NX, Pd);
 #pragma unroll
-            for (int j = 0; j < NX * NX; ++j) Pn[j] += v[BL::P + j];
+            for (int j = 0; j < NX * NX; ++j) Pn[j] += v[j];
 #pragma unroll
-            for (int j = 0; j < NX; ++j) pn[j] += v[BL::p + j] + Pd[j];
+            for (int j = 0; j < NX; ++j) pn[j] += v[NX * NX + j] + Pd[j];
           }
           const int e = riccati_step<NX, NU>(stage(b), reg, Pn, pn, P, p, pol(b) + PL::K, pol(b) + PL::k);
           err = err ? err : e;
@@ -485,15 +606,18 @@ struct Solver {
         });
       }
       g.sync();
+      mark(1);
       const int e = scan_bwd_depth(d);
+      mark(2);
       err = err ? err : e;
     }
-    // Policies of chain nodes from their successor's value (lqr_scan.hpp:146).
+    // Policies of scanned chain nodes from their successor's value
+    // (feedback_from_values, lqr_scan.hpp:146); max_feedforward.
     double mff = 0.0;
     for (int i = g.rank(); i < t.n; i += g.size()) {
       if (is_leaf(i)) continue;
       const int s = t.node_seg[i], k = t.node_pos[i];
-      if (k + 1 < seg_len(s)) {
+      if (!seq_len(seg_len(s)) && k + 1 < seg_len(s)) {
         const int nxt = seg_node(s, k + 1);
         const double* v = value_of(nxt);
         const int e = feedback<NX, NU>(stage(i), reg, w.defect + nxt * NX, v + BL::P, v + BL::p, pol(i) + PL::K,
@@ -508,86 +632,91 @@ struct Solver {
     red_put(g.sm, 0, mff, false);
     red_put(g.sm, 1, static_cast<double>(err), false);
     g.finish(2, 0);
+    mark(3);
     *max_ff = g.sm->total[0];
     return static_cast<int>(g.sm->total[1]);
   }
 
+  // Items of a phase spanning several depths, numbered contiguously across
+  // depths so each thread gets at most its share (per_seg(d) items/segment;
+  // 0 skips the depth).
+  template <class PerSeg, class F>
+  __device__ void for_multi_depth_items(PerSeg&& per_seg, F&& f) const {
+    int total = 0;
+    for (int d = 0; d < t.ndepth; ++d) total += (t.depth_begin[d + 1] - t.depth_begin[d]) * per_seg(d);
+    for (int q = g.rank(); q < total; q += g.size()) {
+      int r = q, d = 0;
+      for (; d < t.ndepth; ++d) {
+        const int cnt = (t.depth_begin[d + 1] - t.depth_begin[d]) * per_seg(d);
+        if (r < cnt) break;
+        r -= cnt;
+      }
+      const int ps = per_seg(d);
+      f(d, t.depth_begin[d] + r / ps, r % ps);
+    }
+  }
+
   // --------------------------------------------------- forward pass (F)
   // linear_rollout (solver.hpp:330-387) + expected_change_coefficients
-  // (:412-430) fused. Returns (a1, a2).
+  // (:412-430). Long segments: prefix scan of the closed-loop maps
+  // (lqr_scan.hpp:177-187, all depths at once) then a per-node depth sweep;
+  // short segments: a team walk dx_{k+1} = A dx + B du + d. Returns (a1, a2).
   __device__ void forward(double* a1_out, double* a2_out) {
-    // Elements of every segment at every depth at once.
-    for (int d = 0; d < t.ndepth; ++d) {
-      const int L = t.depth_len[d];
-      if (L < 2) continue;
-      for_depth_items(d, L - 1, [&](int s, int k) {
-        const int i = seg_node(s, k), nxt = seg_node(s, k + 1);
-        init_fwd_element<NX, NU>(stage(i), w.defect + nxt * NX, pol(i) + PL::K, pol(i) + PL::k,
-                                 fwd(t.seg_scratch[s] + k));
-      });
-    }
+    auto scan_E = [&](int d) { return seq_len(t.depth_len[d]) ? 0 : t.depth_len[d] - 1; };
+    for_multi_depth_items([&](int d) { return scan_E(d); }, [&](int d, int s, int k) {
+      const int i = seg_node(s, k), nxt = seg_node(s, k + 1);
+      init_fwd_element<NX, NU>(stage(i), w.defect + nxt * NX, pol(i) + PL::K, pol(i) + PL::k,
+                               fwd(t.seg_scratch[s] + k));
+    });
     g.sync();
-    // Prefix scans (scan.hpp:19-50), all depths in the same phases.
+    mark(4);
+    // Prefix scans (scan.hpp:19-50), all scanned depths in the same phases.
     int maxU = 0;
-    for (int d = 0; d < t.ndepth; ++d) maxU = max(maxU, up_steps(t.depth_len[d] - 1));
+    for (int d = 0; d < t.ndepth; ++d) maxU = max(maxU, up_steps(scan_E(d)));
     for (int l = 0; l < maxU; ++l) {
-      for (int d = 0; d < t.ndepth; ++d) {
-        const int E = t.depth_len[d] - 1;
-        if (l >= up_steps(E)) continue;
-        const int nl = level_size(E, l), nn = (nl + 1) >> 1;
-        const int ol = level_offset(E, l), on = ol + nl;
-        for_depth_items(d, nn, [&](int s, int i) {
-          const int base = t.seg_scratch[s];
-          if (2 * i + 1 < nl)
-            combine_fwd<NX>(fwd(base + ol + 2 * i), fwd(base + ol + 2 * i + 1), fwd(base + on + i));
-          else
-            copy<FL::size>(fwd(base + ol + 2 * i), fwd(base + on + i));
-        });
-      }
+      for_multi_depth_items(
+          [&](int d) { return l < up_steps(scan_E(d)) ? (level_size(scan_E(d), l) + 1) >> 1 : 0; },
+          [&](int d, int s, int i) {
+            const int E = scan_E(d);
+            const int nl = level_size(E, l);
+            const int ol = level_offset(E, l), on = ol + nl;
+            const int base = t.seg_scratch[s];
+            if (2 * i + 1 < nl)
+              combine_fwd<NX>(fwd(base + ol + 2 * i), fwd(base + ol + 2 * i + 1), fwd(base + on + i));
+            else
+              copy<FL::size>(fwd(base + ol + 2 * i), fwd(base + on + i));
+          });
       g.sync();
     }
     for (int l = maxU - 1; l >= 0; --l) {
-      for (int d = 0; d < t.ndepth; ++d) {
-        const int E = t.depth_len[d] - 1;
-        if (l >= up_steps(E)) continue;
-        const int nl = level_size(E, l), nn = (nl + 1) >> 1;
-        const int ol = level_offset(E, l), on = ol + nl;
-        for_depth_items(d, nn, [&](int s, int i) {
-          const int base = t.seg_scratch[s];
-          const double* S = fwd(base + on);
-          if (2 * i + 1 < nl) copy<FL::size>(S + static_cast<size_t>(i) * FL::stride, fwd(base + ol + 2 * i + 1));
-          if (i >= 1) {
-            double* a = fwd(base + ol + 2 * i);
-            combine_fwd<NX>(S + static_cast<size_t>(i - 1) * FL::stride, a, a);
-          }
-        });
-      }
+      for_multi_depth_items(
+          [&](int d) { return l < up_steps(scan_E(d)) ? (level_size(scan_E(d), l) + 1) >> 1 : 0; },
+          [&](int d, int s, int i) {
+            const int E = scan_E(d);
+            const int nl = level_size(E, l);
+            const int ol = level_offset(E, l), on = ol + nl;
+            const int base = t.seg_scratch[s];
+            const double* S = fwd(base + on);
+            if (2 * i + 1 < nl) copy<FL::size>(S + static_cast<size_t>(i) * FL::stride, fwd(base + ol + 2 * i + 1));
+            if (i >= 1) {
+              double* a = fwd(base + ol + 2 * i);
+              combine_fwd<NX>(S + static_cast<size_t>(i - 1) * FL::stride, a, a);
+            }
+          });
       g.sync();
     }
-    // Depth sweep: head perturbation from the parent's closed loop, then the
-    // scanned maps; du = K dx + k and the EC terms per node.
-    double a1 = 0.0, a2 = 0.0;
+    mark(5);
+    // Depth sweep.
     for (int d = 0; d < t.ndepth; ++d) {
       const int L = t.depth_len[d];
+      if (seq_len(L)) {
+        forward_walk_depth(d);
+        continue;
+      }
       for_depth_items(d, L, [&](int s, int k) {
         const int head = seg_node(s, 0);
-        const int p = t.parent[head];
         double h[NX];
-        if (p < 0) {
-#pragma unroll
-          for (int j = 0; j < NX; ++j) h[j] = w.x0[j] - w.x[j];
-        } else {
-          // Acl = A + B K ; dx_ch = Acl dx_p + B k + defect_ch (solver.hpp:344-348)
-          const double* sp = stage(p);
-          double BK[NX * NX], Acl[NX * NX], Bk[NX], t1[NX];
-          mm<NX, NU, NX>(sp + SL::B, pol(p) + PL::K, BK);
-#pragma unroll
-          for (int j = 0; j < NX * NX; ++j) Acl[j] = sp[SL::A + j] + BK[j];
-          mv<NX, NU>(sp + SL::B, pol(p) + PL::k, Bk);
-          mv<NX, NX>(Acl, w.dx + p * NX, t1);
-#pragma unroll
-          for (int j = 0; j < NX; ++j) h[j] = (t1[j] + Bk[j]) + w.defect[head * NX + j];
-        }
+        head_dx(head, h);
         const int i = seg_node(s, k);
         double dxi[NX];
         if (k == 0) {
@@ -600,31 +729,151 @@ struct Solver {
           for (int j = 0; j < NX; ++j) dxi[j] = t1[j] + F[FL::c + j];
         }
         copy<NX>(dxi, w.dx + i * NX);
-        const double* si = stage(i);
-        double Qdx[NX];
-        mv<NX, NX>(si + SL::Q, dxi, Qdx);
-        if (is_leaf(i)) {
-          a1 += dot<NX>(si + SL::q, dxi);
-          a2 += 0.5 * dot<NX>(dxi, Qdx);
-        } else {
-          double dui[NU], Mdx[NU], Rdu[NU];
+        if (!is_leaf(i)) {
+          double dui[NU];
           mv<NU, NX>(pol(i) + PL::K, dxi, dui);
 #pragma unroll
-          for (int j = 0; j < NU; ++j) dui[j] += pol(i)[PL::k + j];
-          copy<NU>(dui, w.du + i * NU);
-          mv<NU, NX>(si + SL::M, dxi, Mdx);
-          mv<NU, NU>(si + SL::R, dui, Rdu);
-          a1 += dot<NX>(si + SL::q, dxi) + dot<NU>(si + SL::r, dui);
-          a2 += (0.5 * dot<NX>(dxi, Qdx) + dot<NU>(dui, Mdx)) + 0.5 * dot<NU>(dui, Rdu);
+          for (int j = 0; j < NU; ++j) w.du[i * NU + j] = dui[j] + pol(i)[PL::k + j];
         }
       });
       g.sync();
     }
+    // EC terms per node (solver.hpp:416-428).
+    double a1 = 0.0, a2 = 0.0;
+    for (int i = g.rank(); i < t.n; i += g.size()) {
+      const double* si = stage(i);
+      const double* dxi = w.dx + i * NX;
+      double Qdx[NX];
+      mv<NX, NX>(si + SL::Q, dxi, Qdx);
+      if (is_leaf(i)) {
+        a1 += dot<NX>(si + SL::q, dxi);
+        a2 += 0.5 * dot<NX>(dxi, Qdx);
+      } else {
+        const double* dui = w.du + i * NU;
+        double Mdx[NU], Rdu[NU];
+        mv<NU, NX>(si + SL::M, dxi, Mdx);
+        mv<NU, NU>(si + SL::R, dui, Rdu);
+        a1 += dot<NX>(si + SL::q, dxi) + dot<NU>(si + SL::r, dui);
+        a2 += (0.5 * dot<NX>(dxi, Qdx) + dot<NU>(dui, Mdx)) + 0.5 * dot<NU>(dui, Rdu);
+      }
+    }
     red_put(g.sm, 0, a1, true);
     red_put(g.sm, 1, a2, true);
     g.finish(2, 2);
+    mark(6);
     *a1_out = g.sm->total[0];
     *a2_out = g.sm->total[1];
+  }
+
+  // Head perturbation of a segment: dx0 at the root, else the parent's
+  // closed loop dx_ch = (A + B K) dx_p + B k + defect_ch (solver.hpp:344-348).
+  __device__ void head_dx(int head, double* h) const {
+    const int p = t.parent[head];
+    if (p < 0) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) h[j] = w.x0[j] - w.x[j];
+      return;
+    }
+    const double* sp = stage(p);
+    double BK[NX * NX], Acl[NX * NX], Bk[NX], t1[NX];
+    mm<NX, NU, NX>(sp + SL::B, pol(p) + PL::K, BK);
+#pragma unroll
+    for (int j = 0; j < NX * NX; ++j) Acl[j] = sp[SL::A + j] + BK[j];
+    mv<NX, NU>(sp + SL::B, pol(p) + PL::k, Bk);
+    mv<NX, NX>(Acl, w.dx + p * NX, t1);
+#pragma unroll
+    for (int j = 0; j < NX; ++j) h[j] = (t1[j] + Bk[j]) + w.defect[head * NX + j];
+  }
+
+  // Team walk of every short segment at depth d: du_k = K dx_k + k,
+  // dx_{k+1} = (A + B K) dx_k + B k + d (lane r owns state row r). The next
+  // node's rows / policy / offset are prefetched into registers.
+  struct WalkPre {
+    double A[NX], B[NU], K[NU * NX], k[NU], d;
+  };
+  static constexpr int kRows = NX > NU ? NX : NU;  // lanes < NX own state rows, < NU inputs
+  __device__ void walk_load(int i, int nxt, int lane, WalkPre& p) const {
+    if (lane < kRows) {
+      const double* si = stage(i);
+      const double* po = pol(i);
+      const int r = lane < NX ? lane : 0;
+#pragma unroll
+      for (int l = 0; l < NX; ++l) p.A[l] = si[SL::A + r + l * NX];
+#pragma unroll
+      for (int t2 = 0; t2 < NU; ++t2) p.B[t2] = si[SL::B + r + t2 * NX];
+#pragma unroll
+      for (int q = 0; q < NU * NX; ++q) p.K[q] = po[PL::K + q];
+#pragma unroll
+      for (int t2 = 0; t2 < NU; ++t2) p.k[t2] = po[PL::k + t2];
+      p.d = nxt >= 0 ? w.defect[nxt * NX + r] : 0.0;
+    }
+  }
+
+  __device__ void forward_walk_depth(int d) {
+    if constexpr (kTS > 0) {
+      const int L = t.depth_len[d];
+      const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
+      const int team = g.rank() / kTS, nteams = g.size() / kTS, lane = threadIdx.x % kTS;
+      const unsigned mask = team_mask();
+      RicSmem<NX, NU>& sm = ric_smem();
+      double* dx = sm.psh;  // reuse team scratch
+      for (int s = sb + team; s < se; s += nteams) {
+        const int head = seg_node(s, 0);
+        const int last = is_leaf(seg_node(s, L - 1)) ? L - 1 : L;  // nodes with an input
+        WalkPre cur, nxp;
+        if (last > 0) walk_load(head, L > 1 ? seg_node(s, 1) : -1, lane, cur);
+        __syncwarp(mask);
+        if (lane == 0) {
+          double h[NX];
+          head_dx(head, h);
+#pragma unroll
+          for (int j = 0; j < NX; ++j) {
+            dx[j] = h[j];
+            w.dx[head * NX + j] = h[j];
+          }
+        }
+        __syncwarp(mask);
+        for (int k = 0; k < last; ++k) {
+          const int i = seg_node(s, k);
+          const int nxt = k + 1 < L ? seg_node(s, k + 1) : -1;
+          if (k + 1 < last) walk_load(nxt, k + 2 < L ? seg_node(s, k + 2) : -1, lane, nxp);
+          double xr = 0.0;
+          if (lane < kRows) {
+            double dxl[NX];
+#pragma unroll
+            for (int l = 0; l < NX; ++l) dxl[l] = dx[l];
+            if (lane < NU) {
+              double a = 0.0;
+#pragma unroll
+              for (int l = 0; l < NX; ++l) a = fma(cur.K[lane + l * NU], dxl[l], a);
+              w.du[i * NU + lane] = a + cur.k[lane];
+            }
+            if (nxt >= 0 && lane < NX) {
+              double acl = 0.0, bk = 0.0;
+#pragma unroll
+              for (int l = 0; l < NX; ++l) {
+                double av = cur.A[l];
+#pragma unroll
+                for (int t2 = 0; t2 < NU; ++t2) av = fma(cur.B[t2], cur.K[t2 + l * NU], av);
+                acl = fma(av, dxl[l], acl);
+              }
+#pragma unroll
+              for (int t2 = 0; t2 < NU; ++t2) bk = fma(cur.B[t2], cur.k[t2], bk);
+              xr = (acl + bk) + cur.d;
+            }
+          }
+          if (nxt < 0 || k + 1 == L) break;
+          __syncwarp(mask);
+          if (lane < NX) {
+            dx[lane] = xr;
+            w.dx[nxt * NX + lane] = xr;
+          }
+          __syncwarp(mask);
+          cur = nxp;
+        }
+      }
+    }
+    g.sync();
   }
 
   // ------------------------------------------------- line search (S)
@@ -689,6 +938,18 @@ struct Solver {
     g.sync();
   }
 
+  // Per-phase device time (diagnostic): the leader charges the time since
+  // the previous mark to slot `id` (Work::prof, optional).
+  unsigned long long prof_last{0};
+  __device__ void mark(int id) {
+    if (w.prof && g.leader()) {
+      unsigned long long ns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+      if (prof_last) w.prof[id] += static_cast<double>(ns - prof_last);
+      prof_last = ns;
+    }
+  }
+
   __device__ static double now_s() {
     unsigned long long ns;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
@@ -731,7 +992,9 @@ struct Solver {
       for (int pass = 0; pass < o.max_inner_iterations; ++pass) {
         double t0 = now_s();
         int bad = 0;
+        mark(9);
         const Eval ev = linearize_evaluate(&bad);
+        mark(0);
         if (bad) {
           err_code = kErrLinearizeNonfinite;
           err_node = bad - 1;
@@ -772,7 +1035,9 @@ struct Solver {
         const double merit0 = ev.cost_al + mu * ev.defect_l1;
         Eval after;
         double merit_after = 0.0, dec = 0.0;
+        mark(8);
         const int lvl = line_search(o.alpha_levels, merit0, a1, a2, mu, ev.defect_l1, &after, &merit_after, &dec);
+        mark(7);
         double t4 = now_s();
         times[4] += t4 - t3;
         DevRecord rec;
@@ -854,9 +1119,11 @@ struct Solver {
     const int err = backward(reg, &max_ff);
     if (w.value) {
       for (int i = g.rank(); i < t.n; i += g.size()) {
-        const double* v = value_of(i);
-        copy<NX * NX>(v + BL::P, w.value + static_cast<size_t>(i) * VL::stride + VL::P);
-        copy<NX>(v + BL::p, w.value + static_cast<size_t>(i) * VL::stride + VL::p);
+        if (!seq_len(seg_len(t.node_seg[i]))) {
+          const double* v = value_of(i);
+          copy<NX * NX>(v + BL::P, w.value + static_cast<size_t>(i) * VL::stride + VL::P);
+          copy<NX>(v + BL::p, w.value + static_cast<size_t>(i) * VL::stride + VL::p);
+        }
       }
     }
     g.sync();

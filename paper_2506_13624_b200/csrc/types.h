@@ -24,6 +24,7 @@ struct ModelParams {
 };
 
 constexpr int kMaxAlpha = 16;
+constexpr int kProfSlots = 16;
 
 // ------------------------------------------------------------------ options
 struct DevOptions {  // SolverOptions (solver.hpp:28-58), device copy
@@ -33,6 +34,7 @@ struct DevOptions {  // SolverOptions (solver.hpp:28-58), device copy
   double penalty_init, penalty_growth, penalty_max;
   double reg_init, reg_min, reg_growth, reg_decay, reg_max;
   int zero_inputs;  // 1: initial inputs are zero (solver.hpp:604-609), skip the H2D
+  int seq_max_len;  // segments of <= this many nodes use the team Riccati sweep, longer ones the scan
 };
 
 // IterationRecord (solver.hpp:547-561).
@@ -97,6 +99,7 @@ struct Work {
   DevRecord* records;
   int max_records;
   DevResult* result;
+  double* prof;  // optional [kProfSlots] per-phase device time (ns), leader-accumulated
 };
 
 }  // namespace bmpc_b200

@@ -3,6 +3,8 @@
 // has no FP64 figure; SURVEY.md §8d asks for a DFMA measurement).
 #include <cuda_runtime.h>
 
+#include <cooperative_groups.h>
+
 #include "types.h"
 
 namespace bmpc_b200 {
@@ -69,6 +71,38 @@ double measure_fp64_peak_tflops(cudaStream_t stream) {
   cudaFree(d);
   const double flops = 2.0 * 8.0 * static_cast<double>(iters) * blocks * threads;
   return flops / (best * 1e-3) / 1e12;
+}
+
+}  // namespace bmpc_b200
+
+namespace bmpc_b200 {
+
+// Cost of one cooperative-groups grid barrier (diagnostic for grid mode).
+__global__ void grid_sync_bench_kernel(int iters, unsigned long long* out) {
+  cooperative_groups::grid_group g = cooperative_groups::this_grid();
+  unsigned long long t0 = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int i = 0; i < iters; ++i) g.sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    out[0] = t1 - t0;
+  }
+}
+
+double grid_sync_us(int blocks, int threads, int iters, cudaStream_t stream) {
+  unsigned long long* d = nullptr;
+  cudaMalloc(&d, sizeof(unsigned long long));
+  void* args[] = {&iters, &d};
+  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(grid_sync_bench_kernel), dim3(blocks), dim3(threads), args, 0,
+                              stream);
+  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(grid_sync_bench_kernel), dim3(blocks), dim3(threads), args, 0,
+                              stream);
+  unsigned long long ns = 0;
+  cudaMemcpyAsync(&ns, d, sizeof ns, cudaMemcpyDeviceToHost, stream);
+  cudaStreamSynchronize(stream);
+  cudaFree(d);
+  return ns * 1e-3 / iters;
 }
 
 }  // namespace bmpc_b200

@@ -12,7 +12,7 @@ s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
 ctx = B.Context(0, stream=s.cuda_stream)
 cnt = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
-shapes = [(256, 1), (128, 2), (64, 4), (128, 3), (64, 6), (128, 4), (64, 8)]
+shapes = [(256, 1), (256, 2), (256, 3), (256, 4), (128, 4), (128, 6), (128, 8), (512, 2)]
 probs = [B.build_intersection_case(B.intersection_spec(63, 10.0, 0.1), 2, 2, perturb_seed=42 + i) for i in range(cnt)]
 bt = B.Batch(ctx, probs)
 bt.set_models()
