@@ -547,3 +547,10 @@ def set_seq_max_len(ctx: Context, length: int):
     """Segments of <= length nodes use the team Riccati sweep, longer ones the
     associative scan (0 = scan everywhere)."""
     _check(lib().bmpc_ctx_set_seq_max_len(ctx._h, int(length)))
+
+
+def debug_ric_step_cycles(steps: int = 512, prefetch: bool = True, ctx: Optional[Context] = None) -> float:
+    ctx = ctx or default_context()
+    v = C.c_double()
+    _check(lib().bmpc_debug_ric_step_cycles(ctx._h, int(steps), int(prefetch), C.byref(v)))
+    return v.value

@@ -430,7 +430,7 @@ struct DevBuf {
 struct Plan {
   int n{0}, ndepth{0}, nseg{0}, scratch{0}, max_con{0};
   bool has_constraints{false};
-  std::vector<int> depth_begin, depth_len, seg_off, seg_nodes, seg_scratch, node_seg, node_pos;
+  std::vector<int> depth_begin, depth_len, seg_off, seg_nodes, seg_scratch, seg_stride, node_seg, node_pos;
   DevBuf d_ints, d_weight, d_topo;
   Topo topo{};
 };
@@ -495,6 +495,12 @@ std::unique_ptr<Plan> make_plan(const bmpc_tree& t, int max_con, bool has_constr
     }
     pl->seg_off.push_back(static_cast<int>(pl->seg_nodes.size()));
     pl->seg_scratch.push_back(scratch);
+    // BFS order keeps a chain at a fixed offset within equal-size levels, so
+    // consecutive nodes differ by a constant stride (build_tree, tree.hpp:96-115).
+    int stride = L >= 2 ? sg.nodes[1] - sg.nodes[0] : 1;
+    for (int k = 1; k < L && stride; ++k)
+      if (sg.nodes[static_cast<size_t>(k)] - sg.nodes[static_cast<size_t>(k) - 1] != stride) stride = 0;
+    pl->seg_stride.push_back(stride);
     // Scan levels n_0 = L, n_{l+1} = ceil(n_l/2): total <= 2L + (#levels).
     scratch += 2 * L + 32;
   }
@@ -516,6 +522,7 @@ std::unique_ptr<Plan> make_plan(const bmpc_tree& t, int max_con, bool has_constr
   const size_t o_so = put(pl->seg_off.data(), pl->seg_off.size());
   const size_t o_sn = put(pl->seg_nodes.data(), pl->seg_nodes.size());
   const size_t o_ss = put(pl->seg_scratch.data(), pl->seg_scratch.size());
+  const size_t o_st = put(pl->seg_stride.data(), pl->seg_stride.size());
   const size_t o_ns = put(pl->node_seg.data(), pl->node_seg.size());
   const size_t o_np = put(pl->node_pos.data(), pl->node_pos.size());
   pl->d_ints = DevBuf(ints.size() * sizeof(int));
@@ -536,6 +543,7 @@ std::unique_ptr<Plan> make_plan(const bmpc_tree& t, int max_con, bool has_constr
   tp.seg_off = base + o_so;
   tp.seg_nodes = base + o_sn;
   tp.seg_scratch = base + o_ss;
+  tp.seg_stride = base + o_st;
   tp.node_seg = base + o_ns;
   tp.node_pos = base + o_np;
   tp.has_constraints = has_constraints ? 1 : 0;
@@ -1177,6 +1185,13 @@ int bmpc_batch_phase_profile(bmpc_batch* b, int instance, double* out, int n) {
   } catch (const std::exception& e) {
     return fail(BMPC_ERR_CUDA, e.what());
   }
+}
+
+int bmpc_debug_ric_step_cycles(bmpc_ctx* ctx, int steps, int prefetch, double* cycles) {
+  if (!ctx || !cycles) return fail(BMPC_ERR_INVALID, "null argument");
+  cudaSetDevice(ctx->device);
+  *cycles = ric_step_cycles(steps, prefetch, ctx->stream);
+  return cudaGetLastError() == cudaSuccess ? BMPC_OK : fail(BMPC_ERR_CUDA, "ric benchmark failed");
 }
 
 int bmpc_fp64_peak_tflops(bmpc_ctx* ctx, double* tflops) {

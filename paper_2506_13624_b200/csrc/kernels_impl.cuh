@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(256) lqr_tree_grid_kernel(const Topo* topo, co
 template <int NX, int NU>
 static size_t team_smem_bytes(int threads) {
   constexpr int ts = team_size<NX, NU>();
-  return red_smem_bytes(threads) + (ts > 0 ? static_cast<size_t>(threads / ts) * (sizeof(TeamSmem<NX>) > sizeof(RicSmem<NX, NU>) ? sizeof(TeamSmem<NX>) : sizeof(RicSmem<NX, NU>)) : 16);
+  return red_smem_bytes(threads) + (ts > 0 ? static_cast<size_t>(threads / ts) * Solver<NX, NU, CtaGroup>::slot_bytes() : 16);
 }
 
 template <class K>

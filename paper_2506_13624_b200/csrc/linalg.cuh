@@ -133,6 +133,7 @@ BMPC_HD double dot(const double* a, const double* b) {
 template <int N>
 struct Ldlt {
   double m[N * N];
+  double dinv[N];  // 1 / D_ii (0 when |D_ii| <= DBL_MIN, Eigen's pseudo-inverse)
   int t[N];
   bool info_ok;
 
@@ -192,9 +193,10 @@ struct Ldlt {
         }
       }
       const double akk = m[k + k * N];
+      const double inv = 1.0 / akk;
+      dinv[k] = fabs(akk) > 2.2250738585072014e-308 ? inv : 0.0;
       if (k + 1 < N) {
         if (fabs(akk) > 0.0) {
-          const double inv = 1.0 / akk;
 #pragma unroll
           for (int i = k + 1; i < N; ++i) m[i + k * N] *= inv;
         } else {
@@ -239,10 +241,7 @@ struct Ldlt {
         for (int k = 0; k < i; ++k) x[i] = fma(-m[i + k * N], x[k], x[i]);
       }
 #pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const double d = m[i + i * N];
-        x[i] = fabs(d) > 2.2250738585072014e-308 ? x[i] / d : 0.0;
-      }
+      for (int i = 0; i < N; ++i) x[i] *= dinv[i];
 #pragma unroll
       for (int i = N - 1; i >= 0; --i) {
 #pragma unroll
@@ -261,6 +260,7 @@ struct Ldlt {
 template <int N>
 struct Lu {
   double lu[N * N];
+  double uinv[N];  // 1 / U_ii (inf / nan propagate like a division would)
   int perm[N];  // row i of P*A is row perm[i] of A
 
   BMPC_HD void compute(const double* a) {
@@ -299,6 +299,7 @@ struct Lu {
 #pragma unroll
         for (int i = k + 1; i < N; ++i) lu[i + k * N] *= inv;
       }
+      uinv[k] = 1.0 / lu[k + k * N];
 #pragma unroll
       for (int j = k + 1; j < N; ++j) {
         const double ukj = lu[k + j * N];
@@ -331,7 +332,7 @@ struct Lu {
       for (int i = N - 1; i >= 0; --i) {
 #pragma unroll
         for (int k = i + 1; k < N; ++k) xc[i] = fma(-lu[i + k * N], xc[k], xc[i]);
-        xc[i] = xc[i] / lu[i + i * N];
+        xc[i] = xc[i] * uinv[i];
       }
     }
   }
@@ -348,7 +349,7 @@ struct Lu {
         double s = bc[i];
 #pragma unroll
         for (int k = 0; k < i; ++k) s = fma(-lu[k + i * N], y[k], s);
-        y[i] = s / lu[i + i * N];
+        y[i] = s * uinv[i];
       }
 #pragma unroll
       for (int i = N - 1; i >= 0; --i) {

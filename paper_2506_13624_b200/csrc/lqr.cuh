@@ -639,4 +639,194 @@ __device__ int team_riccati_step(double reg, int lane, unsigned mask, RicSmem<NX
   return bad ? kIndefinite : kBwdOk;
 }
 
+// ---------------------------------------------------------------------------
+// Divergence-free team Riccati step. Every small product of riccati_step is a
+// "dot slot" out = base (+ reg on a diagonal) + sum_l X[xo + l xs] Y[yo + l ys]
+// over one flat shared array; each lane owns fixed slots, described once per
+// sweep, so all lanes run one instruction stream per stage (4 stages + the
+// redundant NU x NU LDLT).
+template <int NX, int NU>
+struct RicFlat {  // offsets into the team's flat shared array
+  using L = StageLayout<NX, NU>;
+  static constexpr int S = 0, A = L::A, B = L::B, Q = L::Q, R = L::R, M = L::M, q = L::q, r = L::r;
+  static constexpr int P = L::size, p = P + NX * NX, c = p + NX, psh = c + NX, BtP = psh + NX,
+                       AtP = BtP + NU * NX, Qxx = AtP + NX * NX, Qux = Qxx + NX * NX, Quu = Qux + NU * NX,
+                       qx = Quu + NU * NU, qu = qx + NX, K = qu + NU, k = K + NU * NX, ZERO = k + NU,
+                       DUMMY = ZERO + 1, size = DUMMY + 8;
+  static constexpr int n1 = NX + NU * NX + NX * NX;                  // psh, B'P, A'P
+  static constexpr int n2 = NX * NX + NU * NX + NU * NU + NX + NU;   // Qxx, Qux, Quu, qx, qu
+  static constexpr int n3 = NU * NX + NU;                            // K, k
+  static constexpr int n4 = NX * NX + NX;                            // P, p
+};
+
+struct DotSlot {
+  short bo, xo, xs, yo, ys, oo;
+  bool diag;  // add the Levenberg shift (Quu diagonal)
+};
+
+template <int NX, int NU, int TS>
+struct RicDesc {
+  using F = RicFlat<NX, NU>;
+  static constexpr int R1 = (F::n1 + TS - 1) / TS, R2 = (F::n2 + TS - 1) / TS, R4 = (F::n4 + TS - 1) / TS;
+  DotSlot s1[R1], s2[R2], s4a[R4], s4b[R4];
+  short g4[R4];   // output index into the value record (P / p), -1 none
+  short a3, v3, o3, g3;  // stage 3: Hinv row a3 . F[v3 ..], out F[o3], policy index g3 (-1 none)
+};
+
+template <int NX, int NU, int TS>
+__device__ void ric_desc_init(int lane, RicDesc<NX, NU, TS>& d) {
+  using F = RicFlat<NX, NU>;
+  const DotSlot idle{F::ZERO, F::ZERO, 0, F::ZERO, 0, F::DUMMY, false};
+#pragma unroll
+  for (int r = 0; r < RicDesc<NX, NU, TS>::R1; ++r) {
+    const int q = lane + r * TS;
+    DotSlot x = idle;
+    if (q < NX) {  // psh = p + P c
+      x = {short(F::p + q), short(F::P + q), NX, F::c, 1, short(F::psh + q), false};
+    } else if (q < NX + NU * NX) {  // B'P (a, j)
+      const int t = q - NX, a = t % NU, j = t / NU;
+      x = {F::ZERO, short(F::B + a * NX), 1, short(F::P + j * NX), 1, short(F::BtP + t), false};
+    } else if (q < F::n1) {  // A'P (i, j)
+      const int t = q - NX - NU * NX, i = t % NX, j = t / NX;
+      x = {F::ZERO, short(F::A + i * NX), 1, short(F::P + j * NX), 1, short(F::AtP + t), false};
+    }
+    d.s1[r] = x;
+  }
+#pragma unroll
+  for (int r = 0; r < RicDesc<NX, NU, TS>::R2; ++r) {
+    int q = lane + r * TS;
+    DotSlot x = idle;
+    if (q < NX * NX) {  // Qxx = Q + A'P A
+      const int i = q % NX, j = q / NX;
+      x = {short(F::Q + q), short(F::AtP + i), NX, short(F::A + j * NX), 1, short(F::Qxx + q), false};
+    } else if ((q -= NX * NX) < NU * NX) {  // Qux = M + B'P A
+      const int a = q % NU, j = q / NU;
+      x = {short(F::M + q), short(F::BtP + a), NU, short(F::A + j * NX), 1, short(F::Qux + q), false};
+    } else if ((q -= NU * NX) < NU * NU) {  // Quu = R (+reg) + B'P B
+      const int a = q % NU, b = q / NU;
+      x = {short(F::R + q), short(F::BtP + a), NU, short(F::B + b * NX), 1, short(F::Quu + q), a == b};
+    } else if ((q -= NU * NU) < NX) {  // qx = q + A' psh
+      x = {short(F::q + q), short(F::A + q * NX), 1, F::psh, 1, short(F::qx + q), false};
+    } else if ((q -= NX) < NU) {  // qu = r + B' psh
+      x = {short(F::r + q), short(F::B + q * NX), 1, F::psh, 1, short(F::qu + q), false};
+    }
+    d.s2[r] = x;
+  }
+  {  // stage 3: K(a, j) = -Hinv(a,:) Qux(:, j) ; k(a) = -Hinv(a,:) qu
+    const int q = lane;
+    if (q < NU * NX) {
+      d.a3 = q % NU;
+      d.v3 = F::Qux + (q / NU) * NU;
+      d.o3 = F::K + q;
+      d.g3 = PolicyLayout<NX, NU>::K + q;
+    } else if (q < NU * NX + NU) {
+      d.a3 = q - NU * NX;
+      d.v3 = F::qu;
+      d.o3 = F::k + d.a3;
+      d.g3 = PolicyLayout<NX, NU>::k + d.a3;
+    } else {
+      d.a3 = 0;
+      d.v3 = F::ZERO;  // reads ZERO .. ZERO+NU-1 (ZERO, DUMMY...) harmlessly
+      d.o3 = F::DUMMY;
+      d.g3 = -1;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RicDesc<NX, NU, TS>::R4; ++r) {
+    const int q = lane + r * TS;
+    DotSlot a = idle, b = idle;
+    short g = -1;
+    if (q < NX * NX) {  // P(i,j) = sym(Qxx + Qux' K)
+      const int i = q % NX, j = q / NX;
+      a = {short(F::Qxx + q), short(F::Qux + i * NU), 1, short(F::K + j * NU), 1, short(F::P + q), false};
+      b = {short(F::Qxx + j + i * NX), short(F::Qux + j * NU), 1, short(F::K + i * NU), 1, short(F::P + q), false};
+      g = short(ValueLayout<NX>::P + q);
+    } else if (q < F::n4) {  // p = qx + Qux' k
+      const int i = q - NX * NX;
+      a = {short(F::qx + i), short(F::Qux + i * NU), 1, short(F::k), 1, short(F::p + i), false};
+      b = a;
+      g = short(ValueLayout<NX>::p + i);
+    }
+    d.s4a[r] = a;
+    d.s4b[r] = b;
+    d.g4[r] = g;
+  }
+}
+
+template <int LEN>
+__device__ __forceinline__ double dot_slot(const double* Fm, const DotSlot& s, double reg) {
+  double a = Fm[s.bo] + (s.diag ? reg : 0.0);
+#pragma unroll
+  for (int l = 0; l < LEN; ++l) a = fma(Fm[s.xo + l * s.xs], Fm[s.yo + l * s.ys], a);
+  return a;
+}
+
+// One Bellman step on the team's flat array (stage, c, P, p staged).
+// Overwrites P, p; writes value / policy records. Returns kIndefinite when
+// R + B'PB is not positive definite (lqr_scan.hpp:150, riccati.hpp:31-35).
+template <int NX, int NU, int TS>
+__device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, const RicDesc<NX, NU, TS>& d, double* V_g,
+                                   double* pol_g) {
+  using F = RicFlat<NX, NU>;
+  using D = RicDesc<NX, NU, TS>;
+  __syncwarp(mask);
+  double o1[D::R1];
+#pragma unroll
+  for (int r = 0; r < D::R1; ++r) o1[r] = dot_slot<NX>(Fm, d.s1[r], 0.0);
+#pragma unroll
+  for (int r = 0; r < D::R1; ++r) Fm[d.s1[r].oo] = o1[r];
+  __syncwarp(mask);
+  double o2[D::R2];
+#pragma unroll
+  for (int r = 0; r < D::R2; ++r) o2[r] = dot_slot<NX>(Fm, d.s2[r], reg);
+#pragma unroll
+  for (int r = 0; r < D::R2; ++r) Fm[d.s2[r].oo] = o2[r];
+  __syncwarp(mask);
+  // Huu = sym(Quu); every lane factors it and forms its row of Huu^-1.
+  double H[NU * NU];
+#pragma unroll
+  for (int t = 0; t < NU * NU; ++t) H[t] = Fm[F::Quu + t];
+  symmetrize<NU>(H);
+  Ldlt<NU> f;
+  f.compute(H);
+  const bool pos = f.positive();
+  double row[NU];
+  {
+    double inv[NU * NU];
+#pragma unroll
+    for (int t = 0; t < NU * NU; ++t) inv[t] = (t % (NU + 1) == 0) ? 1.0 : 0.0;
+    f.template solve<NU>(inv);
+#pragma unroll
+    for (int b = 0; b < NU; ++b) {
+      double v = inv[0 + b * NU];
+#pragma unroll
+      for (int a = 1; a < NU; ++a) v = (a == d.a3) ? inv[a + b * NU] : v;
+      row[b] = v;
+    }
+  }
+  {
+    double v = 0.0;
+#pragma unroll
+    for (int b = 0; b < NU; ++b) v = fma(row[b], Fm[d.v3 + b], v);
+    Fm[d.o3] = -v;
+    if (pol_g && d.g3 >= 0) pol_g[d.g3] = -v;
+  }
+  __syncwarp(mask);
+  double o4[D::R4];
+#pragma unroll
+  for (int r = 0; r < D::R4; ++r) {
+    const double a = dot_slot<NU>(Fm, d.s4a[r], 0.0);
+    const double b = dot_slot<NU>(Fm, d.s4b[r], 0.0);
+    o4[r] = 0.5 * (a + b);
+  }
+  __syncwarp(mask);
+#pragma unroll
+  for (int r = 0; r < D::R4; ++r) {
+    Fm[d.s4a[r].oo] = o4[r];
+    if (V_g && d.g4[r] >= 0) V_g[d.g4[r]] = o4[r];
+  }
+  const unsigned bad = __ballot_sync(mask, !pos);
+  return bad ? kIndefinite : kBwdOk;
+}
+
 }  // namespace bmpc_b200

@@ -177,6 +177,17 @@ struct Solver {
   __device__ double* pol(int i) const { return w.policy + static_cast<size_t>(i) * PL::stride; }
   __device__ int seg_len(int s) const { return t.seg_off[s + 1] - t.seg_off[s]; }
   __device__ int seg_node(int s, int k) const { return t.seg_nodes[t.seg_off[s] + k]; }
+  // Node k of a segment without a dependent index load when the stride is constant.
+  struct SegIdx {
+    int off, head, stride;
+  };
+  __device__ SegIdx seg_idx(int s) const {
+    const int off = t.seg_off[s];
+    return {off, t.seg_nodes[off], t.seg_stride[s]};
+  }
+  __device__ int node_at(const SegIdx& q, int k) const {
+    return q.stride ? q.head + k * q.stride : t.seg_nodes[q.off + k];
+  }
 
   // Value of node i during/after the backward pass: slot (L-1-pos) of its
   // segment's level-0 array (the reversed suffix scan).
@@ -458,7 +469,9 @@ struct Solver {
     return *reinterpret_cast<TeamSmem<NX>*>(reinterpret_cast<unsigned char*>(tsm) + (threadIdx.x / kTS) * slot_bytes());
   }
   __host__ __device__ static constexpr size_t slot_bytes() {
-    return sizeof(TeamSmem<NX>) > sizeof(RicSmem<NX, NU>) ? sizeof(TeamSmem<NX>) : sizeof(RicSmem<NX, NU>);
+    constexpr size_t a = sizeof(TeamSmem<NX>) > sizeof(RicSmem<NX, NU>) ? sizeof(TeamSmem<NX>) : sizeof(RicSmem<NX, NU>);
+    constexpr size_t b = sizeof(double) * RicFlat<NX, NU>::size;
+    return a > b ? a : b;
   }
 
   // Team Riccati sweep of every (short) segment at depth d: terminal (leaf
@@ -467,23 +480,30 @@ struct Solver {
   __device__ int riccati_sweep_depth(int d, double reg) {
     int err = kBwdOk;
     if constexpr (kTS > 0) {
+      using F = RicFlat<NX, NU>;
       const int L = t.depth_len[d];
       const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
       const int team = g.rank() / kTS, nteams = g.size() / kTS, lane = threadIdx.x % kTS;
       const unsigned mask = team_mask();
-      RicSmem<NX, NU>& sm = ric_smem();
+      double* Fm = reinterpret_cast<double*>(&ric_smem());
+      RicDesc<NX, NU, kTS> desc;
+      ric_desc_init<NX, NU, kTS>(lane, desc);
+      constexpr int PRE = (SL::size + kTS - 1) / kTS;
       for (int s = sb + team; s < se; s += nteams) {
-        const int b = seg_node(s, L - 1);
+        const SegIdx sq = seg_idx(s);
+        const int b = node_at(sq, L - 1);
         __syncwarp(mask);
+        if (lane == 0) Fm[F::ZERO] = 0.0;
         if (is_leaf(b)) {
           for (int k = lane; k < NX * NX; k += kTS) {
             const double v = stage(b)[SL::Q + k] + ((k % (NX + 1)) == 0 ? reg : 0.0);
-            sm.P[k] = v;
+            Fm[F::P + k] = v;
             val(b)[VL::P + k] = v;
           }
           for (int k = lane; k < NX; k += kTS) {
-            sm.p[k] = stage(b)[SL::q + k];
-            val(b)[VL::p + k] = sm.p[k];
+            const double v = stage(b)[SL::q + k];
+            Fm[F::p + k] = v;
+            val(b)[VL::p + k] = v;
           }
         } else {
           // riccati_tree_from (riccati.hpp:112-116): children in index order.
@@ -491,7 +511,7 @@ struct Solver {
           for (int k = lane; k < NX * NX; k += kTS) {
             double a = 0.0;
             for (int ch = c0; ch < c0 + nc; ++ch) a += value_ptr(ch)[k];
-            sm.P[k] = a;
+            Fm[F::P + k] = a;
           }
           for (int k = lane; k < NX; k += kTS) {
             double a = 0.0;
@@ -502,26 +522,27 @@ struct Solver {
               for (int l = 0; l < NX; ++l) pd = fma(v[k + l * NX], w.defect[ch * NX + l], pd);
               a += v[NX * NX + k] + pd;
             }
-            sm.p[k] = a;
+            Fm[F::p + k] = a;
           }
-          ric_load<NX, NU, kTS>(stage(b), nullptr, lane, sm);
-          const int e = team_riccati_step<NX, NU, kTS>(reg, lane, mask, sm, val(b), pol(b) + PL::K, pol(b) + PL::k);
+          for (int k = lane; k < SL::size; k += kTS) Fm[F::S + k] = stage(b)[k];
+          if (lane < NX) Fm[F::c + lane] = 0.0;
+          const int e = team_riccati_step_u<NX, NU, kTS>(reg, mask, Fm, desc, val(b), pol(b));
           err = err ? err : e;
         }
         // Chain nodes tail -> head; the next node's stage record and edge
         // offset are prefetched into registers while this step computes.
-        constexpr int PRE = (SL::size + kTS - 1) / kTS;
         if (L >= 2) {
           __syncwarp(mask);
-          ric_load<NX, NU, kTS>(stage(seg_node(s, L - 2)), w.defect + b * NX, lane, sm);
+          const double* s0 = stage(node_at(sq, L - 2));
+          for (int k = lane; k < SL::size; k += kTS) Fm[F::S + k] = s0[k];
+          if (lane < NX) Fm[F::c + lane] = w.defect[b * NX + lane];
         }
-        int nxt = b;
         for (int k = L - 2; k >= 0; --k) {
-          const int i = seg_node(s, k);
+          const int i = node_at(sq, k);
           double pre[PRE];
           double prec = 0.0;
           if (k >= 1) {
-            const double* sp = stage(seg_node(s, k - 1));
+            const double* sp = stage(node_at(sq, k - 1));
 #pragma unroll
             for (int j = 0; j < PRE; ++j) {
               const int idx = lane + j * kTS;
@@ -529,20 +550,18 @@ struct Solver {
             }
             if (lane < NX) prec = w.defect[i * NX + lane];
           }
-          const int e = team_riccati_step<NX, NU, kTS>(reg, lane, mask, sm, val(i), pol(i) + PL::K, pol(i) + PL::k);
+          const int e = team_riccati_step_u<NX, NU, kTS>(reg, mask, Fm, desc, val(i), pol(i));
           err = err ? err : e;
           if (k >= 1) {
             __syncwarp(mask);
 #pragma unroll
             for (int j = 0; j < PRE; ++j) {
               const int idx = lane + j * kTS;
-              if (idx < SL::size) sm.s[idx] = pre[j];
+              if (idx < SL::size) Fm[F::S + idx] = pre[j];
             }
-            if (lane < NX) sm.c[lane] = prec;
+            if (lane < NX) Fm[F::c + lane] = prec;
           }
-          nxt = i;
         }
-        (void)nxt;
       }
     }
     g.sync();
@@ -818,10 +837,11 @@ struct Solver {
       RicSmem<NX, NU>& sm = ric_smem();
       double* dx = sm.psh;  // reuse team scratch
       for (int s = sb + team; s < se; s += nteams) {
-        const int head = seg_node(s, 0);
-        const int last = is_leaf(seg_node(s, L - 1)) ? L - 1 : L;  // nodes with an input
+        const SegIdx sq = seg_idx(s);
+        const int head = sq.head;
+        const int last = is_leaf(node_at(sq, L - 1)) ? L - 1 : L;  // nodes with an input
         WalkPre cur, nxp;
-        if (last > 0) walk_load(head, L > 1 ? seg_node(s, 1) : -1, lane, cur);
+        if (last > 0) walk_load(head, L > 1 ? node_at(sq, 1) : -1, lane, cur);
         __syncwarp(mask);
         if (lane == 0) {
           double h[NX];
@@ -834,9 +854,9 @@ struct Solver {
         }
         __syncwarp(mask);
         for (int k = 0; k < last; ++k) {
-          const int i = seg_node(s, k);
-          const int nxt = k + 1 < L ? seg_node(s, k + 1) : -1;
-          if (k + 1 < last) walk_load(nxt, k + 2 < L ? seg_node(s, k + 2) : -1, lane, nxp);
+          const int i = node_at(sq, k);
+          const int nxt = k + 1 < L ? node_at(sq, k + 1) : -1;
+          if (k + 1 < last) walk_load(nxt, k + 2 < L ? node_at(sq, k + 2) : -1, lane, nxp);
           double xr = 0.0;
           if (lane < kRows) {
             double dxl[NX];

@@ -75,6 +75,7 @@ struct Topo {
   const int* depth_len;      // [ndepth] segment length at each depth (balanced tree)
   const int* seg_off;        // [nseg+1] CSR offsets into seg_nodes
   const int* seg_nodes;      // node ids head -> tail
+  const int* seg_stride;     // [nseg] constant node-index stride along the segment (0: use seg_nodes)
   const int* seg_scratch;    // [nseg] first scratch slot (2*len + 32 slots reserved)
   const int* node_seg;       // [n]
   const int* node_pos;       // [n]

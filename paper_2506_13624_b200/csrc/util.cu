@@ -5,6 +5,8 @@
 
 #include <cooperative_groups.h>
 
+#include <vector>
+
 #include "types.h"
 
 namespace bmpc_b200 {
@@ -103,6 +105,89 @@ double grid_sync_us(int blocks, int threads, int iters, cudaStream_t stream) {
   cudaStreamSynchronize(stream);
   cudaFree(d);
   return ns * 1e-3 / iters;
+}
+
+}  // namespace bmpc_b200
+
+// ---------------------------------------------------------------------------
+// Microbenchmark of the team Riccati step (diagnostic): one 16-lane team walks
+// a synthetic chain of `steps` stage records resident in global memory.
+#include "lqr.cuh"
+
+namespace bmpc_b200 {
+
+__global__ void ric_bench_kernel(const double* stages, const double* defects, double* vals, double* pols, int steps,
+                                 int prefetch, unsigned long long* cycles) {
+  constexpr int NX = 4, NU = 2, TS = 16;
+  using SL = StageLayout<NX, NU>;
+  using F = RicFlat<NX, NU>;
+  __shared__ double Fm[F::size];
+  const int lane = threadIdx.x;
+  const unsigned mask = 0xffffu;
+  RicDesc<NX, NU, TS> desc;
+  ric_desc_init<NX, NU, TS>(lane, desc);
+  for (int k = lane; k < F::size; k += TS) Fm[k] = 0.0;
+  __syncwarp(mask);
+  for (int k = lane; k < NX * NX; k += TS) Fm[F::P + k] = (k % 5 == 0) ? 1.0 : 0.0;
+  if (lane < NX) Fm[F::p + lane] = 0.1;
+  for (int k = lane; k < SL::size; k += TS) Fm[F::S + k] = stages[k];
+  if (lane < NX) Fm[F::c + lane] = defects[lane];
+  __syncwarp(mask);
+  unsigned long long t0 = clock64();
+  int err = 0;
+  for (int k = 0; k < steps; ++k) {
+    constexpr int PRE = (SL::size + TS - 1) / TS;
+    double pre[PRE];
+    double prec = 0.0;
+    const double* sp = stages + static_cast<size_t>((k + 1) % steps) * SL::stride;
+#pragma unroll
+    for (int j = 0; j < PRE; ++j) {
+      const int idx = lane + j * TS;
+      pre[j] = idx < SL::size ? sp[idx] : 0.0;
+    }
+    if (lane < NX) prec = defects[((k + 1) % steps) * NX + lane];
+    err |= team_riccati_step_u<NX, NU, TS>(0.0, mask, Fm, desc, vals + static_cast<size_t>(k) * 20,
+                                           pols + static_cast<size_t>(k) * 10);
+    __syncwarp(mask);
+#pragma unroll
+    for (int j = 0; j < PRE; ++j) {
+      const int idx = lane + j * TS;
+      if (idx < SL::size) Fm[F::S + idx] = pre[j];
+    }
+    if (lane < NX) Fm[F::c + lane] = prec;
+  }
+  unsigned long long t1 = clock64();
+  if (lane == 0) {
+    cycles[0] = t1 - t0;
+    cycles[1] = err;
+  }
+  (void)prefetch;
+}
+
+double ric_step_cycles(int steps, int prefetch, cudaStream_t stream) {
+  using SL = StageLayout<4, 2>;
+  std::vector<double> hs(static_cast<size_t>(steps) * SL::stride, 0.0), hd(static_cast<size_t>(steps) * 4, 0.01);
+  for (int k = 0; k < steps; ++k) {
+    double* s = hs.data() + static_cast<size_t>(k) * SL::stride;
+    for (int i = 0; i < 4; ++i) s[SL::A + i * 5] = 1.0, s[SL::Q + i * 5] = 1.0, s[SL::q + i] = 0.1;
+    s[SL::B + 3] = 0.1, s[SL::B + 6] = 0.1, s[SL::R] = 0.5, s[SL::R + 3] = 0.5, s[SL::r] = 0.01;
+  }
+  double *ds, *dd, *dv, *dp;
+  unsigned long long* dc;
+  cudaMalloc(&ds, hs.size() * 8);
+  cudaMalloc(&dd, hd.size() * 8);
+  cudaMalloc(&dv, static_cast<size_t>(steps) * 20 * 8);
+  cudaMalloc(&dp, static_cast<size_t>(steps) * 10 * 8);
+  cudaMalloc(&dc, 16);
+  cudaMemcpy(ds, hs.data(), hs.size() * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(dd, hd.data(), hd.size() * 8, cudaMemcpyHostToDevice);
+  ric_bench_kernel<<<1, 16, 0, stream>>>(ds, dd, dv, dp, steps, prefetch, dc);
+  ric_bench_kernel<<<1, 16, 0, stream>>>(ds, dd, dv, dp, steps, prefetch, dc);
+  unsigned long long hc[2];
+  cudaMemcpyAsync(hc, dc, 16, cudaMemcpyDeviceToHost, stream);
+  cudaStreamSynchronize(stream);
+  cudaFree(ds), cudaFree(dd), cudaFree(dv), cudaFree(dp), cudaFree(dc);
+  return static_cast<double>(hc[0]) / steps;
 }
 
 }  // namespace bmpc_b200
