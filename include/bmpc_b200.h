@@ -211,6 +211,8 @@ int bmpc_fp64_peak_tflops(bmpc_ctx* ctx, double* tflops);
  * 7 line search, 8 merit/convergence, 9 step/AL bookkeeping. */
 int bmpc_batch_set_profiling(bmpc_batch* batch, int on);
 int bmpc_batch_phase_profile(bmpc_batch* batch, int instance, double* out, int n);
+/* Diagnostic: dependent-latency probe {DFMA, LDS, FP64 division} in SM cycles. */
+int bmpc_debug_latency_probe(bmpc_ctx* ctx, double* cycles3);
 /* Diagnostic: SM cycles per team-cooperative Riccati step on a chain. */
 int bmpc_debug_ric_step_cycles(bmpc_ctx* ctx, int steps, int prefetch, double* cycles);
 /* Diagnostic: microseconds per cooperative grid barrier at this launch shape. */

@@ -64,18 +64,19 @@ bool cta_variant_supported(int nx, int nu, int threads, int min_blocks) {
 }
 
 cudaError_t launch_solve_cta(int nx, int nu, const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
-                             const DevOptions& opts, int count, int threads, int min_blocks, cudaStream_t stream) {
+                             const DevOptions& opts, int count, int threads, int min_blocks, bool seq_only,
+                             cudaStream_t stream) {
 #define X(a, b, t, m)                                                 \
   if (nx == a && nu == b && threads == t && min_blocks == m)          \
-    return CtaVariant<a, b, t, m>::launch(d_topo, d_mp, d_work, opts, count, stream);
+    return CtaVariant<a, b, t, m>::launch(d_topo, d_mp, d_work, opts, count, seq_only, stream);
   BMPC_CTA_VARIANTS(X)
 #undef X
   return cudaErrorInvalidValue;
 }
 
-int solve_cta_regs(int nx, int nu, int threads, int min_blocks) {
+int solve_cta_regs(int nx, int nu, int threads, int min_blocks, bool seq_only) {
 #define X(a, b, t, m) \
-  if (nx == a && nu == b && threads == t && min_blocks == m) return CtaVariant<a, b, t, m>::regs();
+  if (nx == a && nu == b && threads == t && min_blocks == m) return CtaVariant<a, b, t, m>::regs(seq_only);
   BMPC_CTA_VARIANTS(X)
 #undef X
   return 0;

@@ -1058,6 +1058,13 @@ static int batch_set_inputs(bmpc_batch* b, const double* initial_inputs) {
   return BMPC_OK;
 }
 
+// Every segment short enough for the team sweep: launch the sweep-only kernel.
+static bool seq_only(const bmpc_batch* b, int seq_max) {
+  int longest = 0;
+  for (int L : b->plan->depth_len) longest = std::max(longest, L);
+  return seq_max > 0 && longest <= seq_max;
+}
+
 static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_inputs) {
   bmpc_options o;
   if (opts)
@@ -1073,7 +1080,7 @@ static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_input
                           b->red.as<double>(), b->grid_blocks, b->threads, b->ctx->stream);
   } else {
     e = launch_solve_cta(b->nx, b->nu, b->plan->d_topo.as<Topo>(), b->mps.as<ModelParams>(), b->works.as<Work>(), d,
-                         b->count, b->cta_threads, b->cta_min_blocks, b->ctx->stream);
+                         b->count, b->cta_threads, b->cta_min_blocks, seq_only(b, d.seq_max_len), b->ctx->stream);
   }
   if (e != cudaSuccess) return fail(BMPC_ERR_CUDA, std::string("solve launch: ") + cudaGetErrorString(e));
   ++b->ctx->launches;
@@ -1194,6 +1201,13 @@ int bmpc_debug_ric_step_cycles(bmpc_ctx* ctx, int steps, int prefetch, double* c
   return cudaGetLastError() == cudaSuccess ? BMPC_OK : fail(BMPC_ERR_CUDA, "ric benchmark failed");
 }
 
+int bmpc_debug_latency_probe(bmpc_ctx* ctx, double* cycles3) {
+  if (!ctx || !cycles3) return fail(BMPC_ERR_INVALID, "null argument");
+  cudaSetDevice(ctx->device);
+  latency_probe(cycles3, ctx->stream);
+  return cudaGetLastError() == cudaSuccess ? BMPC_OK : fail(BMPC_ERR_CUDA, "latency probe failed");
+}
+
 int bmpc_fp64_peak_tflops(bmpc_ctx* ctx, double* tflops) {
   if (!ctx || !tflops) return fail(BMPC_ERR_INVALID, "null argument");
   cudaSetDevice(ctx->device);
@@ -1224,7 +1238,10 @@ int bmpc_batch_info(const bmpc_batch* b, int* threads, int* blocks, int* regs) {
   if (!b) return fail(BMPC_ERR_INVALID, "null argument");
   if (threads) *threads = b->grid_mode ? b->threads : b->cta_threads;
   if (blocks) *blocks = b->grid_mode ? b->grid_blocks : b->count;
-  if (regs) *regs = b->grid_mode ? 0 : solve_cta_regs(b->nx, b->nu, b->cta_threads, b->cta_min_blocks);
+  if (regs)
+    *regs = b->grid_mode ? 0
+                         : solve_cta_regs(b->nx, b->nu, b->cta_threads, b->cta_min_blocks,
+                                          seq_only(b, seq_max_for(b->ctx)));
   return BMPC_OK;
 }
 

@@ -38,8 +38,8 @@ struct LqrLaunch {
 template <int NX, int NU, int T, int MB>
 struct CtaVariant {
   static cudaError_t launch(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work, const DevOptions& opts,
-                            int count, cudaStream_t stream);
-  static int regs();
+                            int count, bool seq_only, cudaStream_t stream);
+  static int regs(bool seq_only);
 };
 
 template <int NX, int NU>
@@ -58,11 +58,12 @@ Strides strides_for(int nx, int nu);
 // Launch-shape variants of the per-instance kernel compiled for (nx, nu).
 bool cta_variant_supported(int nx, int nu, int threads, int min_blocks);
 cudaError_t launch_solve_cta(int nx, int nu, const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
-                             const DevOptions& opts, int count, int threads, int min_blocks, cudaStream_t stream);
+                             const DevOptions& opts, int count, int threads, int min_blocks, bool seq_only,
+                             cudaStream_t stream);
 cudaError_t launch_solve_grid(int nx, int nu, const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
                               const DevOptions& opts, double* red, int blocks, int threads, cudaStream_t stream);
 int solve_grid_blocks(int nx, int nu, int threads);
-int solve_cta_regs(int nx, int nu, int threads, int min_blocks);
+int solve_cta_regs(int nx, int nu, int threads, int min_blocks, bool seq_only);
 cudaError_t launch_lqr_tree(int nx, int nu, bool grid, const Topo* d_topo, const Work* d_work, double reg,
                             double* d_scalars, double* red, int blocks, int threads, cudaStream_t stream, int seq_max);
 int lqr_grid_blocks(int nx, int nu, int threads);
@@ -81,5 +82,6 @@ cudaError_t launch_pack_results(const Work* d_works, int count, int n, int nx, i
 double measure_fp64_peak_tflops(cudaStream_t stream);
 double grid_sync_us(int blocks, int threads, int iters, cudaStream_t stream);
 double ric_step_cycles(int steps, int prefetch, cudaStream_t stream);
+void latency_probe(double* cyc3, cudaStream_t stream);
 
 }  // namespace bmpc_b200

@@ -24,7 +24,7 @@ struct BlockCtx {
 
 // THREADS x MINB trade registers for resident instances per SM:
 // registers/thread <= 65536 / (THREADS * MINB).
-template <int NX, int NU, int THREADS, int MINB>
+template <int NX, int NU, int THREADS, int MINB, bool SEQ>
 __global__ void __launch_bounds__(THREADS, MINB) solve_cta_kernel(const Topo* __restrict__ topo,
                                                         const ModelParams* __restrict__ mps,
                                                         const Work* __restrict__ works, DevOptions opts,
@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(THREADS, MINB) solve_cta_kernel(const Topo* __
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   red.part = reinterpret_cast<double*>(dyn_smem);
   __syncthreads();
-  Solver<NX, NU, CtaGroup> s(CtaGroup{&red}, ctx.topo, ctx.mp, ctx.work, opts);
+  Solver<NX, NU, CtaGroup, SEQ> s(CtaGroup{&red}, ctx.topo, ctx.mp, ctx.work, opts);
   s.tsm = dyn_smem + red_smem_bytes(blockDim.x);
   s.solve();
 }
@@ -184,18 +184,25 @@ int LqrLaunch<NX, NU>::grid_blocks(int threads) {
 
 template <int NX, int NU, int T, int MB>
 cudaError_t CtaVariant<NX, NU, T, MB>::launch(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
-                                              const DevOptions& opts, int count, cudaStream_t stream) {
+                                              const DevOptions& opts, int count, bool seq_only, cudaStream_t stream) {
   const size_t smem = team_smem_bytes<NX, NU>(T);
-  static bool once = (allow_smem(solve_cta_kernel<NX, NU, T, MB>, smem), true);
+  static bool once = (allow_smem(solve_cta_kernel<NX, NU, T, MB, false>, smem),
+                      allow_smem(solve_cta_kernel<NX, NU, T, MB, true>, smem), true);
   (void)once;
-  solve_cta_kernel<NX, NU, T, MB><<<count, T, smem, stream>>>(d_topo, d_mp, d_work, opts, count);
+  if (seq_only && team_size<NX, NU>() > 0)
+    solve_cta_kernel<NX, NU, T, MB, true><<<count, T, smem, stream>>>(d_topo, d_mp, d_work, opts, count);
+  else
+    solve_cta_kernel<NX, NU, T, MB, false><<<count, T, smem, stream>>>(d_topo, d_mp, d_work, opts, count);
   return cudaGetLastError();
 }
 
 template <int NX, int NU, int T, int MB>
-int CtaVariant<NX, NU, T, MB>::regs() {
+int CtaVariant<NX, NU, T, MB>::regs(bool seq_only) {
   cudaFuncAttributes attr{};
-  cudaFuncGetAttributes(&attr, solve_cta_kernel<NX, NU, T, MB>);
+  if (seq_only)
+    cudaFuncGetAttributes(&attr, solve_cta_kernel<NX, NU, T, MB, true>);
+  else
+    cudaFuncGetAttributes(&attr, solve_cta_kernel<NX, NU, T, MB, false>);
   return attr.numRegs;
 }
 

@@ -664,93 +664,45 @@ struct DotSlot {
   bool diag;  // add the Levenberg shift (Quu diagonal)
 };
 
-template <int NX, int NU, int TS>
-struct RicDesc {
+// Slot descriptors computed on the fly from the lane index (integer selects
+// only), so no per-lane descriptor state stays live across the sweep.
+template <int NX, int NU>
+__device__ __forceinline__ DotSlot ric_slot1(int q) {
   using F = RicFlat<NX, NU>;
-  static constexpr int R1 = (F::n1 + TS - 1) / TS, R2 = (F::n2 + TS - 1) / TS, R4 = (F::n4 + TS - 1) / TS;
-  DotSlot s1[R1], s2[R2], s4a[R4], s4b[R4];
-  short g4[R4];   // output index into the value record (P / p), -1 none
-  short a3, v3, o3, g3;  // stage 3: Hinv row a3 . F[v3 ..], out F[o3], policy index g3 (-1 none)
-};
+  if (q < NX) return {short(F::p + q), short(F::P + q), NX, F::c, 1, short(F::psh + q), false};  // psh = p + P c
+  if (q < NX + NU * NX) {  // B'P (a, j)
+    const int t = q - NX, a = t % NU, j = t / NU;
+    return {F::ZERO, short(F::B + a * NX), 1, short(F::P + j * NX), 1, short(F::BtP + t), false};
+  }
+  if (q < F::n1) {  // A'P (i, j)
+    const int t = q - NX - NU * NX, i = t % NX, j = t / NX;
+    return {F::ZERO, short(F::A + i * NX), 1, short(F::P + j * NX), 1, short(F::AtP + t), false};
+  }
+  return {F::ZERO, F::ZERO, 0, F::ZERO, 0, F::DUMMY, false};
+}
 
-template <int NX, int NU, int TS>
-__device__ void ric_desc_init(int lane, RicDesc<NX, NU, TS>& d) {
+template <int NX, int NU>
+__device__ __forceinline__ DotSlot ric_slot2(int q) {
   using F = RicFlat<NX, NU>;
-  const DotSlot idle{F::ZERO, F::ZERO, 0, F::ZERO, 0, F::DUMMY, false};
-#pragma unroll
-  for (int r = 0; r < RicDesc<NX, NU, TS>::R1; ++r) {
-    const int q = lane + r * TS;
-    DotSlot x = idle;
-    if (q < NX) {  // psh = p + P c
-      x = {short(F::p + q), short(F::P + q), NX, F::c, 1, short(F::psh + q), false};
-    } else if (q < NX + NU * NX) {  // B'P (a, j)
-      const int t = q - NX, a = t % NU, j = t / NU;
-      x = {F::ZERO, short(F::B + a * NX), 1, short(F::P + j * NX), 1, short(F::BtP + t), false};
-    } else if (q < F::n1) {  // A'P (i, j)
-      const int t = q - NX - NU * NX, i = t % NX, j = t / NX;
-      x = {F::ZERO, short(F::A + i * NX), 1, short(F::P + j * NX), 1, short(F::AtP + t), false};
-    }
-    d.s1[r] = x;
+  if (q < NX * NX) {  // Qxx = Q + A'P A
+    const int i = q % NX, j = q / NX;
+    return {short(F::Q + q), short(F::AtP + i), NX, short(F::A + j * NX), 1, short(F::Qxx + q), false};
   }
-#pragma unroll
-  for (int r = 0; r < RicDesc<NX, NU, TS>::R2; ++r) {
-    int q = lane + r * TS;
-    DotSlot x = idle;
-    if (q < NX * NX) {  // Qxx = Q + A'P A
-      const int i = q % NX, j = q / NX;
-      x = {short(F::Q + q), short(F::AtP + i), NX, short(F::A + j * NX), 1, short(F::Qxx + q), false};
-    } else if ((q -= NX * NX) < NU * NX) {  // Qux = M + B'P A
-      const int a = q % NU, j = q / NU;
-      x = {short(F::M + q), short(F::BtP + a), NU, short(F::A + j * NX), 1, short(F::Qux + q), false};
-    } else if ((q -= NU * NX) < NU * NU) {  // Quu = R (+reg) + B'P B
-      const int a = q % NU, b = q / NU;
-      x = {short(F::R + q), short(F::BtP + a), NU, short(F::B + b * NX), 1, short(F::Quu + q), a == b};
-    } else if ((q -= NU * NU) < NX) {  // qx = q + A' psh
-      x = {short(F::q + q), short(F::A + q * NX), 1, F::psh, 1, short(F::qx + q), false};
-    } else if ((q -= NX) < NU) {  // qu = r + B' psh
-      x = {short(F::r + q), short(F::B + q * NX), 1, F::psh, 1, short(F::qu + q), false};
-    }
-    d.s2[r] = x;
+  q -= NX * NX;
+  if (q < NU * NX) {  // Qux = M + B'P A
+    const int a = q % NU, j = q / NU;
+    return {short(F::M + q), short(F::BtP + a), NU, short(F::A + j * NX), 1, short(F::Qux + q), false};
   }
-  {  // stage 3: K(a, j) = -Hinv(a,:) Qux(:, j) ; k(a) = -Hinv(a,:) qu
-    const int q = lane;
-    if (q < NU * NX) {
-      d.a3 = q % NU;
-      d.v3 = F::Qux + (q / NU) * NU;
-      d.o3 = F::K + q;
-      d.g3 = PolicyLayout<NX, NU>::K + q;
-    } else if (q < NU * NX + NU) {
-      d.a3 = q - NU * NX;
-      d.v3 = F::qu;
-      d.o3 = F::k + d.a3;
-      d.g3 = PolicyLayout<NX, NU>::k + d.a3;
-    } else {
-      d.a3 = 0;
-      d.v3 = F::ZERO;  // reads ZERO .. ZERO+NU-1 (ZERO, DUMMY...) harmlessly
-      d.o3 = F::DUMMY;
-      d.g3 = -1;
-    }
+  q -= NU * NX;
+  if (q < NU * NU) {  // Quu = R (+reg) + B'P B
+    const int a = q % NU, b = q / NU;
+    return {short(F::R + q), short(F::BtP + a), NU, short(F::B + b * NX), 1, short(F::Quu + q), a == b};
   }
-#pragma unroll
-  for (int r = 0; r < RicDesc<NX, NU, TS>::R4; ++r) {
-    const int q = lane + r * TS;
-    DotSlot a = idle, b = idle;
-    short g = -1;
-    if (q < NX * NX) {  // P(i,j) = sym(Qxx + Qux' K)
-      const int i = q % NX, j = q / NX;
-      a = {short(F::Qxx + q), short(F::Qux + i * NU), 1, short(F::K + j * NU), 1, short(F::P + q), false};
-      b = {short(F::Qxx + j + i * NX), short(F::Qux + j * NU), 1, short(F::K + i * NU), 1, short(F::P + q), false};
-      g = short(ValueLayout<NX>::P + q);
-    } else if (q < F::n4) {  // p = qx + Qux' k
-      const int i = q - NX * NX;
-      a = {short(F::qx + i), short(F::Qux + i * NU), 1, short(F::k), 1, short(F::p + i), false};
-      b = a;
-      g = short(ValueLayout<NX>::p + i);
-    }
-    d.s4a[r] = a;
-    d.s4b[r] = b;
-    d.g4[r] = g;
-  }
+  q -= NU * NU;
+  if (q < NX) return {short(F::q + q), short(F::A + q * NX), 1, F::psh, 1, short(F::qx + q), false};  // qx
+  q -= NX;
+  if (q < NU) return {short(F::r + q), short(F::B + q * NX), 1, F::psh, 1, short(F::qu + q), false};  // qu
+  return {F::ZERO, F::ZERO, 0, F::ZERO, 0, F::DUMMY, false};
 }
 
 template <int LEN>
@@ -765,24 +717,45 @@ __device__ __forceinline__ double dot_slot(const double* Fm, const DotSlot& s, d
 // Overwrites P, p; writes value / policy records. Returns kIndefinite when
 // R + B'PB is not positive definite (lqr_scan.hpp:150, riccati.hpp:31-35).
 template <int NX, int NU, int TS>
-__device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, const RicDesc<NX, NU, TS>& d, double* V_g,
-                                   double* pol_g) {
+__device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int lane, double* V_g, double* pol_g) {
   using F = RicFlat<NX, NU>;
-  using D = RicDesc<NX, NU, TS>;
+  constexpr int R1 = (F::n1 + TS - 1) / TS, R2 = (F::n2 + TS - 1) / TS, R4 = (F::n4 + TS - 1) / TS;
   __syncwarp(mask);
-  double o1[D::R1];
+  {
+    double o[R1];
+    short oo[R1];
 #pragma unroll
-  for (int r = 0; r < D::R1; ++r) o1[r] = dot_slot<NX>(Fm, d.s1[r], 0.0);
+    for (int r = 0; r < R1; ++r) {
+      const DotSlot sl = ric_slot1<NX, NU>(lane + r * TS);
+      o[r] = dot_slot<NX>(Fm, sl, 0.0);
+      oo[r] = sl.oo;
+    }
 #pragma unroll
-  for (int r = 0; r < D::R1; ++r) Fm[d.s1[r].oo] = o1[r];
+    for (int r = 0; r < R1; ++r) Fm[oo[r]] = o[r];
+  }
   __syncwarp(mask);
-  double o2[D::R2];
+  {
+    double o[R2];
+    short oo[R2];
 #pragma unroll
-  for (int r = 0; r < D::R2; ++r) o2[r] = dot_slot<NX>(Fm, d.s2[r], reg);
+    for (int r = 0; r < R2; ++r) {
+      const DotSlot sl = ric_slot2<NX, NU>(lane + r * TS);
+      o[r] = dot_slot<NX>(Fm, sl, reg);
+      oo[r] = sl.oo;
+    }
 #pragma unroll
-  for (int r = 0; r < D::R2; ++r) Fm[d.s2[r].oo] = o2[r];
+    for (int r = 0; r < R2; ++r) Fm[oo[r]] = o[r];
+  }
   __syncwarp(mask);
   // Huu = sym(Quu); every lane factors it and forms its row of Huu^-1.
+  int a3, v3, o3, g3;
+  if (lane < NU * NX) {  // K(a, j) = -Hinv(a,:) Qux(:, j)
+    a3 = lane % NU, v3 = F::Qux + (lane / NU) * NU, o3 = F::K + lane, g3 = PolicyLayout<NX, NU>::K + lane;
+  } else if (lane < NU * NX + NU) {  // k(a) = -Hinv(a,:) qu
+    a3 = lane - NU * NX, v3 = F::qu, o3 = F::k + a3, g3 = PolicyLayout<NX, NU>::k + a3;
+  } else {
+    a3 = 0, v3 = F::ZERO, o3 = F::DUMMY, g3 = -1;
+  }
   double H[NU * NU];
 #pragma unroll
   for (int t = 0; t < NU * NU; ++t) H[t] = Fm[F::Quu + t];
@@ -800,30 +773,54 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, const 
     for (int b = 0; b < NU; ++b) {
       double v = inv[0 + b * NU];
 #pragma unroll
-      for (int a = 1; a < NU; ++a) v = (a == d.a3) ? inv[a + b * NU] : v;
+      for (int a = 1; a < NU; ++a) v = (a == a3) ? inv[a + b * NU] : v;
       row[b] = v;
     }
   }
   {
     double v = 0.0;
 #pragma unroll
-    for (int b = 0; b < NU; ++b) v = fma(row[b], Fm[d.v3 + b], v);
-    Fm[d.o3] = -v;
-    if (pol_g && d.g3 >= 0) pol_g[d.g3] = -v;
+    for (int b = 0; b < NU; ++b) v = fma(row[b], Fm[v3 + b], v);
+    Fm[o3] = -v;
+    if (pol_g && g3 >= 0) pol_g[g3] = -v;
   }
   __syncwarp(mask);
-  double o4[D::R4];
+  double o4[R4];
+  short oo4[R4], g4[R4];
 #pragma unroll
-  for (int r = 0; r < D::R4; ++r) {
-    const double a = dot_slot<NU>(Fm, d.s4a[r], 0.0);
-    const double b = dot_slot<NU>(Fm, d.s4b[r], 0.0);
+  for (int r = 0; r < R4; ++r) {
+    const int q = lane + r * TS;
+    double a = 0.0, b = 0.0;
+    if (q < NX * NX) {  // P(i,j) = sym(Qxx + Qux' K)
+      const int i = q % NX, j = q / NX;
+      a = Fm[F::Qxx + q];
+      b = Fm[F::Qxx + j + i * NX];
+#pragma unroll
+      for (int t = 0; t < NU; ++t) {
+        a = fma(Fm[F::Qux + t + i * NU], Fm[F::K + t + j * NU], a);
+        b = fma(Fm[F::Qux + t + j * NU], Fm[F::K + t + i * NU], b);
+      }
+      oo4[r] = short(F::P + q);
+      g4[r] = short(ValueLayout<NX>::P + q);
+    } else if (q < F::n4) {  // p = qx + Qux' k
+      const int i = q - NX * NX;
+      a = Fm[F::qx + i];
+#pragma unroll
+      for (int t = 0; t < NU; ++t) a = fma(Fm[F::Qux + t + i * NU], Fm[F::k + t], a);
+      b = a;
+      oo4[r] = short(F::p + i);
+      g4[r] = short(ValueLayout<NX>::p + i);
+    } else {
+      oo4[r] = F::DUMMY;
+      g4[r] = -1;
+    }
     o4[r] = 0.5 * (a + b);
   }
   __syncwarp(mask);
 #pragma unroll
-  for (int r = 0; r < D::R4; ++r) {
-    Fm[d.s4a[r].oo] = o4[r];
-    if (V_g && d.g4[r] >= 0) V_g[d.g4[r]] = o4[r];
+  for (int r = 0; r < R4; ++r) {
+    Fm[oo4[r]] = o4[r];
+    if (V_g && g4[r] >= 0) V_g[g4[r]] = o4[r];
   }
   const unsigned bad = __ballot_sync(mask, !pos);
   return bad ? kIndefinite : kBwdOk;

@@ -151,7 +151,10 @@ __device__ __forceinline__ void red_put(RedSmem* sm, int k, double v, bool is_su
 }
 
 // ------------------------------------------------------------------ solver
-template <int NX, int NU, class G>
+// kSeqOnly: every segment takes the team Riccati sweep / walk; the scan path
+// (and its register footprint) is compiled out — used for batches of trees
+// whose segments are all short (e.g. cfg0/cfg4).
+template <int NX, int NU, class G, bool kSeqOnly = false>
 struct Solver {
   using SL = StageLayout<NX, NU>;
   using BL = BwdLayout<NX>;
@@ -197,7 +200,7 @@ struct Solver {
   }
   __device__ double* val(int i) const { return w.value + static_cast<size_t>(i) * VL::stride; }
   // Segments of at most seq_max_len nodes take the team Riccati sweep.
-  __device__ bool seq_len(int L) const { return kTS > 0 && L <= o.seq_max_len; }
+  __device__ bool seq_len(int L) const { return kSeqOnly || (kTS > 0 && L <= o.seq_max_len); }
   // (P, p) of node i after the backward pass (either path); P at +0, p at +NX*NX.
   __device__ const double* value_ptr(int i) const {
     const int s = t.node_seg[i];
@@ -486,8 +489,6 @@ struct Solver {
       const int team = g.rank() / kTS, nteams = g.size() / kTS, lane = threadIdx.x % kTS;
       const unsigned mask = team_mask();
       double* Fm = reinterpret_cast<double*>(&ric_smem());
-      RicDesc<NX, NU, kTS> desc;
-      ric_desc_init<NX, NU, kTS>(lane, desc);
       constexpr int PRE = (SL::size + kTS - 1) / kTS;
       for (int s = sb + team; s < se; s += nteams) {
         const SegIdx sq = seg_idx(s);
@@ -526,7 +527,7 @@ struct Solver {
           }
           for (int k = lane; k < SL::size; k += kTS) Fm[F::S + k] = stage(b)[k];
           if (lane < NX) Fm[F::c + lane] = 0.0;
-          const int e = team_riccati_step_u<NX, NU, kTS>(reg, mask, Fm, desc, val(b), pol(b));
+          const int e = team_riccati_step_u<NX, NU, kTS>(reg, mask, Fm, lane, val(b), pol(b));
           err = err ? err : e;
         }
         // Chain nodes tail -> head; the next node's stage record and edge
@@ -550,7 +551,7 @@ struct Solver {
             }
             if (lane < NX) prec = w.defect[i * NX + lane];
           }
-          const int e = team_riccati_step_u<NX, NU, kTS>(reg, mask, Fm, desc, val(i), pol(i));
+          const int e = team_riccati_step_u<NX, NU, kTS>(reg, mask, Fm, lane, val(i), pol(i));
           err = err ? err : e;
           if (k >= 1) {
             __syncwarp(mask);
@@ -582,6 +583,7 @@ struct Solver {
         mark(2);
         continue;
       }
+      if constexpr (!kSeqOnly) {
       // Terminal of each segment: regularized leaf cost or the branch-node
       // Bellman step over the summed children (riccati.hpp:107-120).
       for_depth_items(d, 1, [&](int s, int) {
@@ -629,6 +631,7 @@ struct Solver {
       const int e = scan_bwd_depth(d);
       mark(2);
       err = err ? err : e;
+      }
     }
     // Policies of scanned chain nodes from their successor's value
     // (feedback_from_values, lqr_scan.hpp:146); max_feedforward.
@@ -636,12 +639,14 @@ struct Solver {
     for (int i = g.rank(); i < t.n; i += g.size()) {
       if (is_leaf(i)) continue;
       const int s = t.node_seg[i], k = t.node_pos[i];
-      if (!seq_len(seg_len(s)) && k + 1 < seg_len(s)) {
-        const int nxt = seg_node(s, k + 1);
-        const double* v = value_of(nxt);
-        const int e = feedback<NX, NU>(stage(i), reg, w.defect + nxt * NX, v + BL::P, v + BL::p, pol(i) + PL::K,
-                                       pol(i) + PL::k);
-        err = err ? err : e;
+      if constexpr (!kSeqOnly) {
+        if (!seq_len(seg_len(s)) && k + 1 < seg_len(s)) {
+          const int nxt = seg_node(s, k + 1);
+          const double* v = value_of(nxt);
+          const int e = feedback<NX, NU>(stage(i), reg, w.defect + nxt * NX, v + BL::P, v + BL::p,
+                                         pol(i) + PL::K, pol(i) + PL::k);
+          err = err ? err : e;
+        }
       }
       double m = 0.0;
 #pragma unroll
@@ -682,6 +687,7 @@ struct Solver {
   // short segments: a team walk dx_{k+1} = A dx + B du + d. Returns (a1, a2).
   __device__ void forward(double* a1_out, double* a2_out) {
     auto scan_E = [&](int d) { return seq_len(t.depth_len[d]) ? 0 : t.depth_len[d] - 1; };
+    if constexpr (!kSeqOnly) {
     for_multi_depth_items([&](int d) { return scan_E(d); }, [&](int d, int s, int k) {
       const int i = seg_node(s, k), nxt = seg_node(s, k + 1);
       init_fwd_element<NX, NU>(stage(i), w.defect + nxt * NX, pol(i) + PL::K, pol(i) + PL::k,
@@ -724,6 +730,7 @@ struct Solver {
           });
       g.sync();
     }
+    }
     mark(5);
     // Depth sweep.
     for (int d = 0; d < t.ndepth; ++d) {
@@ -732,6 +739,7 @@ struct Solver {
         forward_walk_depth(d);
         continue;
       }
+      if constexpr (!kSeqOnly) {
       for_depth_items(d, L, [&](int s, int k) {
         const int head = seg_node(s, 0);
         double h[NX];
@@ -756,6 +764,7 @@ struct Solver {
         }
       });
       g.sync();
+      }
     }
     // EC terms per node (solver.hpp:416-428).
     double a1 = 0.0, a2 = 0.0;
@@ -804,93 +813,68 @@ struct Solver {
     for (int j = 0; j < NX; ++j) h[j] = (t1[j] + Bk[j]) + w.defect[head * NX + j];
   }
 
-  // Team walk of every short segment at depth d: du_k = K dx_k + k,
-  // dx_{k+1} = (A + B K) dx_k + B k + d (lane r owns state row r). The next
-  // node's rows / policy / offset are prefetched into registers.
-  struct WalkPre {
-    double A[NX], B[NU], K[NU * NX], k[NU], d;
+  // Walk of every short segment at depth d, one thread per segment with the
+  // state in registers: du_k = K dx_k + k, dx_{k+1} = (A + B K) dx_k + B k + d
+  // (solver.hpp:341-350 closed loop). The next node's A, B, K, k, d are
+  // prefetched while the current step computes.
+  struct WalkNode {
+    double A[NX * NX], B[NX * NU], K[NU * NX], k[NU], d[NX];
   };
-  static constexpr int kRows = NX > NU ? NX : NU;  // lanes < NX own state rows, < NU inputs
-  __device__ void walk_load(int i, int nxt, int lane, WalkPre& p) const {
-    if (lane < kRows) {
-      const double* si = stage(i);
-      const double* po = pol(i);
-      const int r = lane < NX ? lane : 0;
+  __device__ void walk_fetch(int i, int nxt, WalkNode& p) const {
+    const double* si = stage(i);
+    const double* po = pol(i);
 #pragma unroll
-      for (int l = 0; l < NX; ++l) p.A[l] = si[SL::A + r + l * NX];
+    for (int q = 0; q < NX * NX; ++q) p.A[q] = si[SL::A + q];
 #pragma unroll
-      for (int t2 = 0; t2 < NU; ++t2) p.B[t2] = si[SL::B + r + t2 * NX];
+    for (int q = 0; q < NX * NU; ++q) p.B[q] = si[SL::B + q];
 #pragma unroll
-      for (int q = 0; q < NU * NX; ++q) p.K[q] = po[PL::K + q];
+    for (int q = 0; q < NU * NX; ++q) p.K[q] = po[PL::K + q];
 #pragma unroll
-      for (int t2 = 0; t2 < NU; ++t2) p.k[t2] = po[PL::k + t2];
-      p.d = nxt >= 0 ? w.defect[nxt * NX + r] : 0.0;
-    }
+    for (int q = 0; q < NU; ++q) p.k[q] = po[PL::k + q];
+#pragma unroll
+    for (int q = 0; q < NX; ++q) p.d[q] = nxt >= 0 ? w.defect[nxt * NX + q] : 0.0;
   }
 
   __device__ void forward_walk_depth(int d) {
-    if constexpr (kTS > 0) {
-      const int L = t.depth_len[d];
-      const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
-      const int team = g.rank() / kTS, nteams = g.size() / kTS, lane = threadIdx.x % kTS;
-      const unsigned mask = team_mask();
-      RicSmem<NX, NU>& sm = ric_smem();
-      double* dx = sm.psh;  // reuse team scratch
-      for (int s = sb + team; s < se; s += nteams) {
-        const SegIdx sq = seg_idx(s);
-        const int head = sq.head;
-        const int last = is_leaf(node_at(sq, L - 1)) ? L - 1 : L;  // nodes with an input
-        WalkPre cur, nxp;
-        if (last > 0) walk_load(head, L > 1 ? node_at(sq, 1) : -1, lane, cur);
-        __syncwarp(mask);
-        if (lane == 0) {
-          double h[NX];
-          head_dx(head, h);
+    const int L = t.depth_len[d];
+    const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
+    for (int s = sb + g.rank(); s < se; s += g.size()) {
+      const SegIdx sq = seg_idx(s);
+      const int head = sq.head;
+      const int last = is_leaf(node_at(sq, L - 1)) ? L - 1 : L;  // nodes with an input
+      double dx[NX];
+      head_dx(head, dx);
 #pragma unroll
-          for (int j = 0; j < NX; ++j) {
-            dx[j] = h[j];
-            w.dx[head * NX + j] = h[j];
-          }
+      for (int j = 0; j < NX; ++j) w.dx[head * NX + j] = dx[j];
+      if (last == 0) continue;
+      WalkNode cur, nx;
+      walk_fetch(head, L > 1 ? node_at(sq, 1) : -1, cur);
+      for (int k = 0; k < last; ++k) {
+        const int i = node_at(sq, k);
+        const int nxt = k + 1 < L ? node_at(sq, k + 1) : -1;
+        if (k + 1 < last) walk_fetch(nxt, k + 2 < L ? node_at(sq, k + 2) : -1, nx);
+        double du[NU];
+        mv<NU, NX>(cur.K, dx, du);
+#pragma unroll
+        for (int j = 0; j < NU; ++j) {
+          du[j] += cur.k[j];
+          w.du[i * NU + j] = du[j];
         }
-        __syncwarp(mask);
-        for (int k = 0; k < last; ++k) {
-          const int i = node_at(sq, k);
-          const int nxt = k + 1 < L ? node_at(sq, k + 1) : -1;
-          if (k + 1 < last) walk_load(nxt, k + 2 < L ? node_at(sq, k + 2) : -1, lane, nxp);
-          double xr = 0.0;
-          if (lane < kRows) {
-            double dxl[NX];
+        if (nxt < 0) break;
+        // (A + B K) dx + B k + d, in the reference's closed-loop order.
+        double BK[NX * NX], Acl[NX * NX], Bk[NX], t1[NX];
+        mm<NX, NU, NX>(cur.B, cur.K, BK);
 #pragma unroll
-            for (int l = 0; l < NX; ++l) dxl[l] = dx[l];
-            if (lane < NU) {
-              double a = 0.0;
+        for (int q = 0; q < NX * NX; ++q) Acl[q] = cur.A[q] + BK[q];
+        mv<NX, NU>(cur.B, cur.k, Bk);
+        mv<NX, NX>(Acl, dx, t1);
 #pragma unroll
-              for (int l = 0; l < NX; ++l) a = fma(cur.K[lane + l * NU], dxl[l], a);
-              w.du[i * NU + lane] = a + cur.k[lane];
-            }
-            if (nxt >= 0 && lane < NX) {
-              double acl = 0.0, bk = 0.0;
-#pragma unroll
-              for (int l = 0; l < NX; ++l) {
-                double av = cur.A[l];
-#pragma unroll
-                for (int t2 = 0; t2 < NU; ++t2) av = fma(cur.B[t2], cur.K[t2 + l * NU], av);
-                acl = fma(av, dxl[l], acl);
-              }
-#pragma unroll
-              for (int t2 = 0; t2 < NU; ++t2) bk = fma(cur.B[t2], cur.k[t2], bk);
-              xr = (acl + bk) + cur.d;
-            }
-          }
-          if (nxt < 0 || k + 1 == L) break;
-          __syncwarp(mask);
-          if (lane < NX) {
-            dx[lane] = xr;
-            w.dx[nxt * NX + lane] = xr;
-          }
-          __syncwarp(mask);
-          cur = nxp;
+        for (int j = 0; j < NX; ++j) {
+          dx[j] = (t1[j] + Bk[j]) + cur.d[j];
+          w.dx[nxt * NX + j] = dx[j];
         }
+        if (k + 1 == L) break;
+        cur = nx;
       }
     }
     g.sync();

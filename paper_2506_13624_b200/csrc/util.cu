@@ -124,8 +124,6 @@ __global__ void ric_bench_kernel(const double* stages, const double* defects, do
   __shared__ double Fm[F::size];
   const int lane = threadIdx.x;
   const unsigned mask = 0xffffu;
-  RicDesc<NX, NU, TS> desc;
-  ric_desc_init<NX, NU, TS>(lane, desc);
   for (int k = lane; k < F::size; k += TS) Fm[k] = 0.0;
   __syncwarp(mask);
   for (int k = lane; k < NX * NX; k += TS) Fm[F::P + k] = (k % 5 == 0) ? 1.0 : 0.0;
@@ -146,7 +144,7 @@ __global__ void ric_bench_kernel(const double* stages, const double* defects, do
       pre[j] = idx < SL::size ? sp[idx] : 0.0;
     }
     if (lane < NX) prec = defects[((k + 1) % steps) * NX + lane];
-    err |= team_riccati_step_u<NX, NU, TS>(0.0, mask, Fm, desc, vals + static_cast<size_t>(k) * 20,
+    err |= team_riccati_step_u<NX, NU, TS>(0.0, mask, Fm, lane, vals + static_cast<size_t>(k) * 20,
                                            pols + static_cast<size_t>(k) * 10);
     __syncwarp(mask);
 #pragma unroll
@@ -188,6 +186,50 @@ double ric_step_cycles(int steps, int prefetch, cudaStream_t stream) {
   cudaStreamSynchronize(stream);
   cudaFree(ds), cudaFree(dd), cudaFree(dv), cudaFree(dp), cudaFree(dc);
   return static_cast<double>(hc[0]) / steps;
+}
+
+}  // namespace bmpc_b200
+
+namespace bmpc_b200 {
+
+// Dependent-latency probes (diagnostic): one thread, `n` dependent ops.
+__global__ void lat_probe_kernel(double* io, int n, unsigned long long* out) {
+  __shared__ double sm[64];
+  double a = io[0], b = io[1];
+  if (threadIdx.x < 64) sm[threadIdx.x] = io[threadIdx.x % 4];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  unsigned long long t0 = clock64();
+  for (int i = 0; i < n; ++i) a = fma(a, b, 1e-9);
+  unsigned long long t1 = clock64();
+  int idx = static_cast<int>(a) & 3;
+  for (int i = 0; i < n; ++i) idx = static_cast<int>(sm[idx]) & 3;  // dependent LDS chain
+  unsigned long long t2 = clock64();
+  double c = a;
+  for (int i = 0; i < n; ++i) c = 1.0 / (c + 1.5);  // dependent FP64 division chain
+  unsigned long long t3 = clock64();
+  io[2] = a + idx + c;
+  out[0] = t1 - t0;
+  out[1] = t2 - t1;
+  out[2] = t3 - t2;
+}
+
+void latency_probe(double* cyc3, cudaStream_t stream) {
+  double h[4] = {1.0000001, 0.9999999, 0, 0};
+  double* d;
+  unsigned long long* o;
+  cudaMalloc(&d, sizeof h);
+  cudaMalloc(&o, 3 * sizeof(unsigned long long));
+  cudaMemcpy(d, h, sizeof h, cudaMemcpyHostToDevice);
+  const int n = 4096;
+  lat_probe_kernel<<<1, 64, 0, stream>>>(d, n, o);
+  lat_probe_kernel<<<1, 64, 0, stream>>>(d, n, o);
+  unsigned long long ho[3];
+  cudaMemcpyAsync(ho, o, sizeof ho, cudaMemcpyDeviceToHost, stream);
+  cudaStreamSynchronize(stream);
+  for (int k = 0; k < 3; ++k) cyc3[k] = static_cast<double>(ho[k]) / n;
+  cudaFree(d);
+  cudaFree(o);
 }
 
 }  // namespace bmpc_b200
