@@ -44,6 +44,8 @@ __global__ void __launch_bounds__(THREADS, MINB) solve_cta_kernel(const Topo* __
   __syncthreads();
   Solver<NX, NU, CtaGroup, SEQ> s(CtaGroup{&red}, ctx.topo, ctx.mp, ctx.work, opts);
   s.tsm = dyn_smem + red_smem_bytes(blockDim.x);
+  s.wbuf = reinterpret_cast<double*>(s.tsm);
+  s.wcap = blockDim.x;
   s.solve();
 }
 
@@ -65,6 +67,8 @@ __global__ void __launch_bounds__(256) solve_grid_kernel(const Topo* __restrict_
   __syncthreads();
   Solver<NX, NU, GridGroup> s(GridGroup{&red, red_scratch, nullptr}, ctx.topo, ctx.mp, ctx.work, opts);
   s.tsm = dyn_smem + red_smem_bytes(blockDim.x);
+  s.wbuf = reinterpret_cast<double*>(s.tsm);
+  s.wcap = blockDim.x;
   s.solve();
 }
 
@@ -76,6 +80,8 @@ __device__ void lqr_tree_body(G g, BlockCtx& ctx, double reg, double* scalars, i
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   Solver<NX, NU, G> s(g, ctx.topo, dummy, ctx.work, o);
   s.tsm = dyn_smem + red_smem_bytes(blockDim.x);
+  s.wbuf = reinterpret_cast<double*>(s.tsm);
+  s.wcap = blockDim.x;
   s.lqr_tree(reg, scalars);
 }
 
@@ -117,7 +123,9 @@ __global__ void __launch_bounds__(256) lqr_tree_grid_kernel(const Topo* topo, co
 template <int NX, int NU>
 static size_t team_smem_bytes(int threads) {
   constexpr int ts = team_size<NX, NU>();
-  return red_smem_bytes(threads) + (ts > 0 ? static_cast<size_t>(threads / ts) * Solver<NX, NU, CtaGroup>::slot_bytes() : 16);
+  const size_t team = ts > 0 ? static_cast<size_t>(threads / ts) * Solver<NX, NU, CtaGroup>::slot_bytes() : 16;
+  const size_t walk = static_cast<size_t>(threads) * Solver<NX, NU, CtaGroup>::kWE * sizeof(double);
+  return red_smem_bytes(threads) + (team > walk ? team : walk);
 }
 
 template <class K>

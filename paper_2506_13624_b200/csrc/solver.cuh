@@ -89,6 +89,8 @@ struct CtaGroup {
   RedSmem* sm;
   __device__ int rank() const { return threadIdx.x; }
   __device__ int size() const { return blockDim.x; }
+  __device__ int block() const { return 0; }
+  __device__ int nblocks() const { return 1; }
   __device__ bool leader() const { return threadIdx.x == 0; }
   __device__ void sync() const { __syncthreads(); }
   // Fold warp partials sm->part[0..nslot) into sm->total (all threads see it).
@@ -111,6 +113,8 @@ struct GridGroup {
   int* parity;      // per-block private counter lives in smem via sm->flag
   __device__ int rank() const { return blockIdx.x * blockDim.x + threadIdx.x; }
   __device__ int size() const { return gridDim.x * blockDim.x; }
+  __device__ int block() const { return blockIdx.x; }
+  __device__ int nblocks() const { return gridDim.x; }
   __device__ bool leader() const { return blockIdx.x == 0 && threadIdx.x == 0; }
   __device__ void sync() const { cg::this_grid().sync(); }
   __device__ void finish(int nslot, int nsum) const {
@@ -168,6 +172,8 @@ struct Solver {
   Work& w;
   const DevOptions& o;
   double g_rho{0.0};  // current AL penalty (uniform across the group)
+  double* wbuf{nullptr};  // forward-walk elements (aliases tsm; wcap elements of kWE doubles)
+  int wcap{0};
   void* tsm{nullptr};  // [blockDim / kTS] team scratch slots of slot_bytes() (kernel-provided)
 
   __device__ Solver(G g_, const Topo& t_, const ModelParams& mp_, Work& w_, const DevOptions& o_)
@@ -777,7 +783,14 @@ struct Solver {
         a1 += dot<NX>(si + SL::q, dxi);
         a2 += 0.5 * dot<NX>(dxi, Qdx);
       } else {
-        const double* dui = w.du + i * NU;
+        double* dui = w.du + i * NU;
+        if (seq_len(seg_len(t.node_seg[i]))) {  // walked segment: du = K dx + k
+          const double* po = pol(i);
+          double du[NU];
+          mv<NU, NX>(po + PL::K, dxi, du);
+#pragma unroll
+          for (int j = 0; j < NU; ++j) dui[j] = du[j] + po[PL::k + j];
+        }
         double Mdx[NU], Rdu[NU];
         mv<NU, NX>(si + SL::M, dxi, Mdx);
         mv<NU, NU>(si + SL::R, dui, Rdu);
@@ -813,68 +826,71 @@ struct Solver {
     for (int j = 0; j < NX; ++j) h[j] = (t1[j] + Bk[j]) + w.defect[head * NX + j];
   }
 
-  // Walk of every short segment at depth d, one thread per segment with the
-  // state in registers: du_k = K dx_k + k, dx_{k+1} = (A + B K) dx_k + B k + d
-  // (solver.hpp:341-350 closed loop). The next node's A, B, K, k, d are
-  // prefetched while the current step computes.
-  struct WalkNode {
-    double A[NX * NX], B[NX * NU], K[NU * NX], k[NU], d[NX];
-  };
-  __device__ void walk_fetch(int i, int nxt, WalkNode& p) const {
+  // Walk of every short segment at depth d (solver.hpp:341-350 closed loop):
+  // dx_{k+1} = (A_k + B_k K_k) dx_k + B_k k_k + d_{k+1}. The per-step affine
+  // maps do not depend on dx, so the whole block first builds them in shared
+  // memory (one element per thread, a chunk of every segment at once); one
+  // thread per segment then runs the dependent chain out of shared memory.
+  // du = K dx + k is formed per node in the EC phase. Block-local: under a
+  // GridGroup each block walks its own share of the depth's segments.
+  static constexpr int kWE = NX * NX + 2 * NX;  // walk element: Acl, B k, defect of the next node
+  __device__ void walk_element(int i, int nxt, double* e) const {
     const double* si = stage(i);
     const double* po = pol(i);
+    double BK[NX * NX], Bk[NX];
+    mm<NX, NU, NX>(si + SL::B, po + PL::K, BK);
 #pragma unroll
-    for (int q = 0; q < NX * NX; ++q) p.A[q] = si[SL::A + q];
+    for (int q = 0; q < NX * NX; ++q) e[q] = si[SL::A + q] + BK[q];
+    mv<NX, NU>(si + SL::B, po + PL::k, Bk);
 #pragma unroll
-    for (int q = 0; q < NX * NU; ++q) p.B[q] = si[SL::B + q];
-#pragma unroll
-    for (int q = 0; q < NU * NX; ++q) p.K[q] = po[PL::K + q];
-#pragma unroll
-    for (int q = 0; q < NU; ++q) p.k[q] = po[PL::k + q];
-#pragma unroll
-    for (int q = 0; q < NX; ++q) p.d[q] = nxt >= 0 ? w.defect[nxt * NX + q] : 0.0;
+    for (int j = 0; j < NX; ++j) {
+      e[NX * NX + j] = Bk[j];
+      e[NX * NX + NX + j] = w.defect[nxt * NX + j];
+    }
   }
 
   __device__ void forward_walk_depth(int d) {
     const int L = t.depth_len[d];
     const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
-    for (int s = sb + g.rank(); s < se; s += g.size()) {
-      const SegIdx sq = seg_idx(s);
-      const int head = sq.head;
-      const int last = is_leaf(node_at(sq, L - 1)) ? L - 1 : L;  // nodes with an input
+    const int nb = g.nblocks(), b = g.block();
+    const int T = L - 1;  // transitions inside a segment
+    const int lr = threadIdx.x, ls = blockDim.x;
+    const int nmine = se - sb > b ? (se - sb - b + nb - 1) / nb : 0;
+    const int grp = min(ls, wcap);
+    for (int j0 = 0; j0 < nmine; j0 += grp) {
+      const int ng = min(grp, nmine - j0);
+      const int C = max(1, wcap / ng);
+      const bool walker = lr < ng;
+      SegIdx sq{0, 0, 0};
       double dx[NX];
-      head_dx(head, dx);
+      if (walker) {
+        sq = seg_idx(sb + b + (j0 + lr) * nb);
+        head_dx(sq.head, dx);
 #pragma unroll
-      for (int j = 0; j < NX; ++j) w.dx[head * NX + j] = dx[j];
-      if (last == 0) continue;
-      WalkNode cur, nx;
-      walk_fetch(head, L > 1 ? node_at(sq, 1) : -1, cur);
-      for (int k = 0; k < last; ++k) {
-        const int i = node_at(sq, k);
-        const int nxt = k + 1 < L ? node_at(sq, k + 1) : -1;
-        if (k + 1 < last) walk_fetch(nxt, k + 2 < L ? node_at(sq, k + 2) : -1, nx);
-        double du[NU];
-        mv<NU, NX>(cur.K, dx, du);
-#pragma unroll
-        for (int j = 0; j < NU; ++j) {
-          du[j] += cur.k[j];
-          w.du[i * NU + j] = du[j];
+        for (int j = 0; j < NX; ++j) w.dx[sq.head * NX + j] = dx[j];
+      }
+      for (int c0 = 0; c0 < T; c0 += C) {
+        const int cn = min(C, T - c0);
+        for (int q = lr; q < ng * cn; q += ls) {
+          const int r = q / cn, kk = q - r * cn;
+          const SegIdx qs = seg_idx(sb + b + (j0 + r) * nb);
+          walk_element(node_at(qs, c0 + kk), node_at(qs, c0 + kk + 1), wbuf + (r * C + kk) * kWE);
         }
-        if (nxt < 0) break;
-        // (A + B K) dx + B k + d, in the reference's closed-loop order.
-        double BK[NX * NX], Acl[NX * NX], Bk[NX], t1[NX];
-        mm<NX, NU, NX>(cur.B, cur.K, BK);
+        __syncthreads();
+        if (walker) {
+          const double* e = wbuf + lr * C * kWE;
+          for (int kk = 0; kk < cn; ++kk, e += kWE) {
+            const int nxt = node_at(sq, c0 + kk + 1);
+            double t1[NX];
+            mv<NX, NX>(e, dx, t1);
 #pragma unroll
-        for (int q = 0; q < NX * NX; ++q) Acl[q] = cur.A[q] + BK[q];
-        mv<NX, NU>(cur.B, cur.k, Bk);
-        mv<NX, NX>(Acl, dx, t1);
-#pragma unroll
-        for (int j = 0; j < NX; ++j) {
-          dx[j] = (t1[j] + Bk[j]) + cur.d[j];
-          w.dx[nxt * NX + j] = dx[j];
+            for (int j = 0; j < NX; ++j) {
+              dx[j] = (t1[j] + e[NX * NX + j]) + e[NX * NX + NX + j];
+              w.dx[nxt * NX + j] = dx[j];
+            }
+          }
         }
-        if (k + 1 == L) break;
-        cur = nx;
+        __syncthreads();
       }
     }
     g.sync();
