@@ -536,7 +536,10 @@ def batch_phase_profile(batch: "Batch", instance: int = 0) -> dict:
     """Per-phase device time (ms) of one instance after a profiled solve."""
     out = np.zeros(16)
     _check(lib().bmpc_batch_phase_profile(batch._h, int(instance), _ptr(out), 16))
-    return {name: out[i] * 1e-6 for i, name in enumerate(PHASES)}
+    res = {name: out[i] * 1e-6 for i, name in enumerate(PHASES)}
+    if out[13] > 0:  # diagnostic counters, not times
+        res["sweep_cycles_per_step"] = out[12] / out[13]
+    return res
 
 
 def batch_set_profiling(batch: "Batch", on: bool = True):

@@ -154,6 +154,15 @@ __device__ __forceinline__ void red_put(RedSmem* sm, int k, double v, bool is_su
   if ((threadIdx.x & 31) == 0) sm->part[k * (blockDim.x >> 5) + (threadIdx.x >> 5)] = v;
 }
 
+// Like red_put, but accumulates into the warp's slot (first: overwrite).
+__device__ __forceinline__ void red_acc(RedSmem* sm, int k, double v, bool is_sum, bool first) {
+  v = is_sum ? warp_sum(v) : warp_max(v);
+  if ((threadIdx.x & 31) == 0) {
+    double* slot = sm->part + k * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    *slot = first ? v : (is_sum ? *slot + v : fmax(*slot, v));
+  }
+}
+
 // ------------------------------------------------------------------ solver
 // kSeqOnly: every segment takes the team Riccati sweep / walk; the scan path
 // (and its register footprint) is compiled out — used for batches of trees
@@ -544,20 +553,29 @@ struct Solver {
           for (int k = lane; k < SL::size; k += kTS) Fm[F::S + k] = s0[k];
           if (lane < NX) Fm[F::c + lane] = w.defect[b * NX + lane];
         }
+        long long tc0 = 0;
+        if (w.prof && threadIdx.x == 0) tc0 = clock64();
+        // Base pointers in registers: the step's generic stores could alias the
+        // shared-memory Work struct, which would force a reload every step.
+        const double* const stg = w.stage;
+        const double* const dfc = w.defect;
+        double* const vbase = w.value;
+        double* const pbase = w.policy;
         for (int k = L - 2; k >= 0; --k) {
           const int i = node_at(sq, k);
           double pre[PRE];
           double prec = 0.0;
           if (k >= 1) {
-            const double* sp = stage(node_at(sq, k - 1));
+            const double* sp = stg + static_cast<size_t>(node_at(sq, k - 1)) * SL::stride;
 #pragma unroll
             for (int j = 0; j < PRE; ++j) {
               const int idx = lane + j * kTS;
               pre[j] = idx < SL::size ? sp[idx] : 0.0;
             }
-            if (lane < NX) prec = w.defect[i * NX + lane];
+            if (lane < NX) prec = dfc[i * NX + lane];
           }
-          const int e = team_riccati_step_u<NX, NU, kTS>(reg, mask, Fm, lane, val(i), pol(i));
+          const int e = team_riccati_step_u<NX, NU, kTS>(reg, mask, Fm, lane, vbase + static_cast<size_t>(i) * VL::stride,
+                                                         pbase + static_cast<size_t>(i) * PL::stride);
           err = err ? err : e;
           if (k >= 1) {
             __syncwarp(mask);
@@ -568,6 +586,10 @@ struct Solver {
             }
             if (lane < NX) Fm[F::c + lane] = prec;
           }
+        }
+        if (w.prof && threadIdx.x == 0 && L >= 2) {  // diagnostic: cycles per chain step
+          w.prof[12] += static_cast<double>(clock64() - tc0);
+          w.prof[13] += L - 1;
         }
       }
     }
@@ -901,21 +923,67 @@ struct Solver {
   // slots [4l .. 4l+3]; returns the first accepted level or -1.
   __device__ int line_search(int levels, double merit0, double a1, double a2, double mu, double dl1_nom,
                              Eval* chosen, double* merit_chosen, double* decrease_chosen) {
-    for (int l = 0; l < levels; ++l) {
-      const double alpha = ldexp(1.0, -l);
-      double c = 0, cal = 0, dl = 0, vm = -INFINITY;
-      for (int i = g.rank(); i < t.n; i += g.size()) {
-        double a, b, d, v;
-        node_eval(i, alpha, &a, &b, &d, &v);
-        c += a;
-        cal += b;
-        dl += d;
-        vm = fmax(vm, v);
+    // One node per thread per chunk; the node's and its parent's x, dx, u, du
+    // are loaded once and every alpha is evaluated from registers. Per-alpha
+    // sums are butterfly-reduced per chunk into the warp slots (fixed order,
+    // deterministic), so no per-alpha accumulators stay live.
+    const int gsz = g.size();
+    for (int base = 0; base < t.n; base += gsz) {
+      const int i = base + g.rank();
+      const bool valid = i < t.n;
+      const bool leaf = valid ? is_leaf(i) : true;
+      const int p = valid ? t.parent[i] : -1;
+      double x[NX], dx[NX], u[NU], du[NU], xp[NX], dxp[NX], up[NU], dup[NU];
+#pragma unroll
+      for (int j = 0; j < NX; ++j) {
+        x[j] = valid ? w.x[i * NX + j] : 0.0;
+        dx[j] = valid ? w.dx[i * NX + j] : 0.0;
+        xp[j] = p >= 0 ? w.x[p * NX + j] : 0.0;
+        dxp[j] = p >= 0 ? w.dx[p * NX + j] : 0.0;
       }
-      red_put(g.sm, 3 * l + 0, c, true);
-      red_put(g.sm, 3 * l + 1, cal, true);
-      red_put(g.sm, 3 * l + 2, dl, true);
-      red_put(g.sm, 3 * levels + l, vm, false);
+#pragma unroll
+      for (int j = 0; j < NU; ++j) {
+        u[j] = valid && !leaf ? w.u[i * NU + j] : 0.0;
+        du[j] = valid && !leaf ? w.du[i * NU + j] : 0.0;
+        up[j] = p >= 0 ? w.u[p * NU + j] : 0.0;
+        dup[j] = p >= 0 ? w.du[p * NU + j] : 0.0;
+      }
+      const double wi = valid ? t.weight[i] : 0.0;
+      const double* eta = w.eta + static_cast<size_t>(valid ? i : 0) * t.max_con;
+#pragma unroll 1
+      for (int l = 0; l < levels; ++l) {
+        const double alpha = ldexp(1.0, -l);
+        double c = 0.0, cal = 0.0, dl = 0.0, vm = -INFINITY;
+        if (valid) {
+          double xt[NX], ut[NU];
+#pragma unroll
+          for (int j = 0; j < NX; ++j) xt[j] = fma(alpha, dx[j], x[j]);
+#pragma unroll
+          for (int j = 0; j < NU; ++j) ut[j] = leaf ? 0.0 : fma(alpha, du[j], u[j]);
+          double nc, pen, gm;
+          node_cost<NX, NU>(mp, i, leaf, xt, ut, eta, g_rho, &nc, &pen, &gm);
+          c = wi * nc;
+          cal = wi * (nc + pen);
+          vm = gm;
+          if (p >= 0) {
+            double xpt[NX], upt[NU], f[NX];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) xpt[j] = fma(alpha, dxp[j], xp[j]);
+#pragma unroll
+            for (int j = 0; j < NU; ++j) upt[j] = fma(alpha, dup[j], up[j]);
+            node_dynamics<NX, NU>(mp, p, xpt, upt, f);
+            double sd = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) sd += fabs(f[j] - xt[j]);
+            dl = sd;
+          }
+        }
+        const bool first = base == 0;
+        red_acc(g.sm, 3 * l + 0, c, true, first);
+        red_acc(g.sm, 3 * l + 1, cal, true, first);
+        red_acc(g.sm, 3 * l + 2, dl, true, first);
+        red_acc(g.sm, 3 * levels + l, vm, false, first);
+      }
     }
     g.finish(4 * levels, 3 * levels);
     for (int l = 0; l < levels; ++l) {

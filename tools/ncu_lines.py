@@ -9,6 +9,7 @@ cur_file = None
 hdr = None
 agg = defaultdict(float)
 inst = defaultdict(float)
+reasons = defaultdict(lambda: defaultdict(float))
 src_text = {}
 line_key = None
 for r in rows:
@@ -31,9 +32,14 @@ for r in rows:
     try:
         agg[line_key] += float(d.get("Warp Stall Sampling (All Samples)", 0) or 0)
         inst[line_key] += float(d.get("Instructions Executed", 0) or 0)
+        for kk, vv in d.items():
+            if kk.startswith("stall_") and "Not Issued" not in kk and vv:
+                reasons[line_key][kk[6:]] += float(vv)
     except ValueError:
         pass
 tot = sum(agg.values()) or 1
 top = sorted(agg.items(), key=lambda kv: -kv[1])[: int(sys.argv[2]) if len(sys.argv) > 2 else 40]
 for k, v in top:
-    print("%6.2f%% %10.0f inst  %s:%d  %s" % (100 * v / tot, inst[k], k[0], k[1], src_text.get(k, "")))
+    rs = sorted(reasons[k].items(), key=lambda kv: -kv[1])[:3]
+    why = " ".join("%s=%.0f%%" % (a, 100 * b / v) for a, b in rs) if v else ""
+    print("%6.2f%% %10.0f inst  %s:%d  [%s]  %s" % (100 * v / tot, inst[k], k[0], k[1], why, src_text.get(k, "")[:60]))

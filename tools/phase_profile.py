@@ -20,7 +20,10 @@ for name, p in cases:
     r = reps[0]
     prof = B.batch_phase_profile(bt)
     passes = r.n_records + r.outer_iterations
+    cps = prof.pop("sweep_cycles_per_step", None)
     tot = sum(prof.values())
+    if cps:
+        print(f"   team sweep: {cps:.0f} cycles per chain step (thread 0's team)")
     print(f"{name}: nodes={p.tree.node_count} passes~{passes} total={r.times['total_s']*1e3:.2f}ms profiled={tot:.2f}ms")
     for k, v in prof.items():
         print(f"   {k:24s} {v:8.2f} ms  {1e3*v/passes:8.1f} us/pass  {100*v/tot:5.1f}%")
