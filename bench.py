@@ -39,7 +39,12 @@ PER_GPU = 4096
 # Algorithmic work per non-leaf node per inner iteration:
 # linearize 1.575 + init 0.4 + 2 combines 3.0 + feedback 0.35 + fwd 0.482
 # + EC 0.086 + evaluate x2 0.4 + line search 11 x 0.212 = 8.6 kflop.
+# The line search stops at the first round holding an accepted step size
+# (same result), so its share is counted per step size actually evaluated:
+# F_PASS per pass + F_ALPHA per evaluated alpha.
 F_NODE = 8.6e3
+F_ALPHA = 0.212e3
+F_PASS = F_NODE - 11 * F_ALPHA
 
 
 def parse():
@@ -224,7 +229,8 @@ def main():
     status = np.array([r.status for r in reps])
     passes = np.array([r.n_records + r.outer_iterations for r in reps])
     nl = int((probs[0].tree.child_count > 0).sum())
-    flops_per_launch = F_NODE * nl * float(passes.sum())
+    alpha_evals = float(sum(r.alpha_evals for r in reps))
+    flops_per_launch = nl * (F_PASS * float(passes.sum()) + F_ALPHA * alpha_evals)
 
     # e2e: public API with host buffers, copies inside the timed region.
     xh = np.empty((count, n, nx))

@@ -144,6 +144,9 @@ typedef struct bmpc_report {
   double times[6];
   double final_penalty, final_mu, final_reg;
   char message[160];
+  /* Work counter (not a SolveReport field): step sizes the line search
+   * evaluated over all passes (see bmpc_ctx_set_line_search_block). */
+  double alpha_evals;
 } bmpc_report;
 
 /* ------------------------------------------------------------- context */
@@ -156,6 +159,12 @@ int bmpc_ctx_synchronize(bmpc_ctx* ctx);
  * nodes use the team-cooperative sequential Riccati sweep, longer ones the
  * associative scan (0 = scan everywhere; default 64, env BMPC_SEQ_MAX). */
 int bmpc_ctx_set_seq_max_len(bmpc_ctx* ctx, int len);
+/* Line search (solver.hpp:459-518) in rounds of `alphas` step sizes: a round
+ * evaluates its alphas for every node and stops at the first accepted one, so
+ * the chosen alpha and every reported value equal the all-at-once parallel
+ * search; later rounds run only when a whole round is rejected
+ * (0 = all alpha_levels in one round; default 2, env BMPC_LS_BLOCK). */
+int bmpc_ctx_set_line_search_block(bmpc_ctx* ctx, int alphas);
 /* Number of kernels this ctx launched since creation (evidence counter). */
 long long bmpc_ctx_launch_count(const bmpc_ctx* ctx);
 

@@ -86,7 +86,7 @@ class _Report(C.Structure):
                [(n, C.c_double) for n in ("final_cost", "final_violation", "final_defect_l1")] + \
                [("times", C.c_double * 6)] + \
                [(n, C.c_double) for n in ("final_penalty", "final_mu", "final_reg")] + \
-               [("message", C.c_char * 160)]
+               [("message", C.c_char * 160), ("alpha_evals", C.c_double)]
 
 
 _lib_handle = None
@@ -340,6 +340,7 @@ class SolveReport:
     times: dict
     iterations: dict
     n_records: int
+    alpha_evals: float = 0.0  # work counter: step sizes evaluated by the line search
 
     @property
     def status_name(self) -> str:
@@ -365,7 +366,8 @@ def _report(r: _Report, recs=None, nrec=0) -> SolveReport:
         its = {f: np.array([getattr(recs[i], f) for i in range(k)]) for f in RECORD_FIELDS}
     names = ("setup_s", "backward_p1_s", "backward_p2_s", "forward_s", "line_search_s", "total_s")
     return SolveReport(r.status, r.message.decode(), r.inner_iterations, r.outer_iterations, r.final_cost,
-                       r.final_violation, r.final_defect_l1, dict(zip(names, list(r.times))), its, r.n_records)
+                       r.final_violation, r.final_defect_l1, dict(zip(names, list(r.times))), its, r.n_records,
+                       r.alpha_evals)
 
 
 # ------------------------------------------------------------------ context
@@ -550,6 +552,12 @@ def set_seq_max_len(ctx: Context, length: int):
     """Segments of <= length nodes use the team Riccati sweep, longer ones the
     associative scan (0 = scan everywhere)."""
     _check(lib().bmpc_ctx_set_seq_max_len(ctx._h, int(length)))
+
+
+def set_line_search_block(ctx: Context, alphas: int):
+    """Step sizes per line-search round (0 = all levels at once, the reference's
+    parallel search); the accepted alpha and all reported values are the same."""
+    _check(lib().bmpc_ctx_set_line_search_block(ctx._h, int(alphas)))
 
 
 def debug_ric_step_cycles(steps: int = 512, prefetch: bool = True, ctx: Optional[Context] = None) -> float:

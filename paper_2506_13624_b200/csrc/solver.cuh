@@ -921,84 +921,98 @@ struct Solver {
   // ------------------------------------------------- line search (S)
   // Parallel line search (solver.hpp:459-518): every alpha evaluated, sums in
   // slots [4l .. 4l+3]; returns the first accepted level or -1.
+  // Parallel line search (solver.hpp:459-518) with the reference's
+  // first-accepted-alpha semantics, evaluated in rounds of o.ls_block step
+  // sizes: a round evaluates its alphas for every node, reduces them, and
+  // stops at the first accepted one. The chosen alpha and every reported
+  // value are identical to evaluating all levels at once (each alpha's sums
+  // are independent of the rounds); later rounds only run when every alpha of
+  // the earlier ones was rejected.
+  // One node per thread per chunk; the node's and its parent's x, dx, u, du
+  // are loaded once per round and the round's alphas evaluated from
+  // registers. Per-alpha sums are butterfly-reduced per chunk into the warp
+  // slots (fixed order, deterministic). Returns the accepted level or -1.
   __device__ int line_search(int levels, double merit0, double a1, double a2, double mu, double dl1_nom,
-                             Eval* chosen, double* merit_chosen, double* decrease_chosen) {
-    // One node per thread per chunk; the node's and its parent's x, dx, u, du
-    // are loaded once and every alpha is evaluated from registers. Per-alpha
-    // sums are butterfly-reduced per chunk into the warp slots (fixed order,
-    // deterministic), so no per-alpha accumulators stay live.
+                             Eval* chosen, double* merit_chosen, double* decrease_chosen, int* evals) {
+    const int blk = o.ls_block > 0 ? min(o.ls_block, kMaxAlpha) : levels;
     const int gsz = g.size();
-    for (int base = 0; base < t.n; base += gsz) {
-      const int i = base + g.rank();
-      const bool valid = i < t.n;
-      const bool leaf = valid ? is_leaf(i) : true;
-      const int p = valid ? t.parent[i] : -1;
-      double x[NX], dx[NX], u[NU], du[NU], xp[NX], dxp[NX], up[NU], dup[NU];
+    for (int l0 = 0; l0 < levels; l0 += blk) {
+      const int nl = min(blk, levels - l0);
+      *evals += nl;
+      for (int base = 0; base < t.n; base += gsz) {
+        const int i = base + g.rank();
+        const bool valid = i < t.n;
+        const bool leaf = valid ? is_leaf(i) : true;
+        const int p = valid ? t.parent[i] : -1;
+        double x[NX], dx[NX], u[NU], du[NU], xp[NX], dxp[NX], up[NU], dup[NU];
 #pragma unroll
-      for (int j = 0; j < NX; ++j) {
-        x[j] = valid ? w.x[i * NX + j] : 0.0;
-        dx[j] = valid ? w.dx[i * NX + j] : 0.0;
-        xp[j] = p >= 0 ? w.x[p * NX + j] : 0.0;
-        dxp[j] = p >= 0 ? w.dx[p * NX + j] : 0.0;
-      }
-#pragma unroll
-      for (int j = 0; j < NU; ++j) {
-        u[j] = valid && !leaf ? w.u[i * NU + j] : 0.0;
-        du[j] = valid && !leaf ? w.du[i * NU + j] : 0.0;
-        up[j] = p >= 0 ? w.u[p * NU + j] : 0.0;
-        dup[j] = p >= 0 ? w.du[p * NU + j] : 0.0;
-      }
-      const double wi = valid ? t.weight[i] : 0.0;
-      const double* eta = w.eta + static_cast<size_t>(valid ? i : 0) * t.max_con;
-#pragma unroll 1
-      for (int l = 0; l < levels; ++l) {
-        const double alpha = ldexp(1.0, -l);
-        double c = 0.0, cal = 0.0, dl = 0.0, vm = -INFINITY;
-        if (valid) {
-          double xt[NX], ut[NU];
-#pragma unroll
-          for (int j = 0; j < NX; ++j) xt[j] = fma(alpha, dx[j], x[j]);
-#pragma unroll
-          for (int j = 0; j < NU; ++j) ut[j] = leaf ? 0.0 : fma(alpha, du[j], u[j]);
-          double nc, pen, gm;
-          node_cost<NX, NU>(mp, i, leaf, xt, ut, eta, g_rho, &nc, &pen, &gm);
-          c = wi * nc;
-          cal = wi * (nc + pen);
-          vm = gm;
-          if (p >= 0) {
-            double xpt[NX], upt[NU], f[NX];
-#pragma unroll
-            for (int j = 0; j < NX; ++j) xpt[j] = fma(alpha, dxp[j], xp[j]);
-#pragma unroll
-            for (int j = 0; j < NU; ++j) upt[j] = fma(alpha, dup[j], up[j]);
-            node_dynamics<NX, NU>(mp, p, xpt, upt, f);
-            double sd = 0.0;
-#pragma unroll
-            for (int j = 0; j < NX; ++j) sd += fabs(f[j] - xt[j]);
-            dl = sd;
-          }
+        for (int j = 0; j < NX; ++j) {
+          x[j] = valid ? w.x[i * NX + j] : 0.0;
+          dx[j] = valid ? w.dx[i * NX + j] : 0.0;
+          xp[j] = p >= 0 ? w.x[p * NX + j] : 0.0;
+          dxp[j] = p >= 0 ? w.dx[p * NX + j] : 0.0;
         }
-        const bool first = base == 0;
-        red_acc(g.sm, 3 * l + 0, c, true, first);
-        red_acc(g.sm, 3 * l + 1, cal, true, first);
-        red_acc(g.sm, 3 * l + 2, dl, true, first);
-        red_acc(g.sm, 3 * levels + l, vm, false, first);
+#pragma unroll
+        for (int j = 0; j < NU; ++j) {
+          u[j] = valid && !leaf ? w.u[i * NU + j] : 0.0;
+          du[j] = valid && !leaf ? w.du[i * NU + j] : 0.0;
+          up[j] = p >= 0 ? w.u[p * NU + j] : 0.0;
+          dup[j] = p >= 0 ? w.du[p * NU + j] : 0.0;
+        }
+        const double wi = valid ? t.weight[i] : 0.0;
+        const double* eta = w.eta + static_cast<size_t>(valid ? i : 0) * t.max_con;
+#pragma unroll 1
+        for (int q = 0; q < nl; ++q) {
+          const double alpha = ldexp(1.0, -(l0 + q));
+          double c = 0.0, cal = 0.0, dl = 0.0, vm = -INFINITY;
+          if (valid) {
+            double xt[NX], ut[NU];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) xt[j] = fma(alpha, dx[j], x[j]);
+#pragma unroll
+            for (int j = 0; j < NU; ++j) ut[j] = leaf ? 0.0 : fma(alpha, du[j], u[j]);
+            double nc, pen, gm;
+            node_cost<NX, NU>(mp, i, leaf, xt, ut, eta, g_rho, &nc, &pen, &gm);
+            c = wi * nc;
+            cal = wi * (nc + pen);
+            vm = gm;
+            if (p >= 0) {
+              double xpt[NX], upt[NU], f[NX];
+#pragma unroll
+              for (int j = 0; j < NX; ++j) xpt[j] = fma(alpha, dxp[j], xp[j]);
+#pragma unroll
+              for (int j = 0; j < NU; ++j) upt[j] = fma(alpha, dup[j], up[j]);
+              node_dynamics<NX, NU>(mp, p, xpt, upt, f);
+              double sd = 0.0;
+#pragma unroll
+              for (int j = 0; j < NX; ++j) sd += fabs(f[j] - xt[j]);
+              dl = sd;
+            }
+          }
+          const bool first = base == 0;
+          red_acc(g.sm, 3 * q + 0, c, true, first);
+          red_acc(g.sm, 3 * q + 1, cal, true, first);
+          red_acc(g.sm, 3 * q + 2, dl, true, first);
+          red_acc(g.sm, 3 * nl + q, vm, false, first);
+        }
       }
-    }
-    g.finish(4 * levels, 3 * levels);
-    for (int l = 0; l < levels; ++l) {
-      const double alpha = ldexp(1.0, -l);
-      const double cal = g.sm->total[3 * l + 1], dl = g.sm->total[3 * l + 2];
-      const bool finite = isfinite(cal) && isfinite(dl);
-      const double m = finite ? cal + mu * dl : INFINITY;
-      const double ec = a1 * alpha + a2 * alpha * alpha;
-      const double dec = o.armijo_beta * (ec - alpha * mu * dl1_nom);
-      if (isfinite(m) && m <= merit0 + dec) {
-        *chosen = {g.sm->total[3 * l + 0], cal, dl, fmax(g.sm->total[3 * levels + l], 0.0)};
-        *merit_chosen = m;
-        *decrease_chosen = dec;
-        return l;
+      g.finish(4 * nl, 3 * nl);
+      for (int q = 0; q < nl; ++q) {
+        const double alpha = ldexp(1.0, -(l0 + q));
+        const double cal = g.sm->total[3 * q + 1], dl = g.sm->total[3 * q + 2];
+        const bool finite = isfinite(cal) && isfinite(dl);
+        const double m = finite ? cal + mu * dl : INFINITY;
+        const double ec = a1 * alpha + a2 * alpha * alpha;
+        const double dec = o.armijo_beta * (ec - alpha * mu * dl1_nom);
+        if (isfinite(m) && m <= merit0 + dec) {
+          *chosen = {g.sm->total[3 * q + 0], cal, dl, fmax(g.sm->total[3 * nl + q], 0.0)};
+          *merit_chosen = m;
+          *decrease_chosen = dec;
+          return l0 + q;
+        }
       }
+      // (finish() opens with a barrier, so the next round cannot overwrite
+      // the totals while a thread still reads them.)
     }
     return -1;
   }
@@ -1072,7 +1086,7 @@ struct Solver {
     double reg = o.reg_init;
     bool inner_converged = false, failed = false;
     int status = kError, err_code = kErrNone, err_node = -1;
-    int inner = 0, outer_count = 0, nrec = 0;
+    int inner = 0, outer_count = 0, nrec = 0, alpha_evals = 0;
 
     for (int outer = 0; outer < o.max_outer_iterations; ++outer) {
       ++outer_count;
@@ -1124,7 +1138,8 @@ struct Solver {
         Eval after;
         double merit_after = 0.0, dec = 0.0;
         mark(8);
-        const int lvl = line_search(o.alpha_levels, merit0, a1, a2, mu, ev.defect_l1, &after, &merit_after, &dec);
+        const int lvl =
+            line_search(o.alpha_levels, merit0, a1, a2, mu, ev.defect_l1, &after, &merit_after, &dec, &alpha_evals);
         mark(7);
         double t4 = now_s();
         times[4] += t4 - t3;
@@ -1195,6 +1210,7 @@ struct Solver {
       res->final_defect_l1 = fin.defect_l1;
       for (int k = 0; k < 6; ++k) res->times[k] = times[k];
       res->final_penalty = g_rho;
+      res->alpha_evals = alpha_evals;
       res->final_mu = mu;
       res->final_reg = reg;
     }

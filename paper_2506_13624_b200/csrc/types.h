@@ -35,6 +35,7 @@ struct DevOptions {  // SolverOptions (solver.hpp:28-58), device copy
   double reg_init, reg_min, reg_growth, reg_decay, reg_max;
   int zero_inputs;  // 1: initial inputs are zero (solver.hpp:604-609), skip the H2D
   int seq_max_len;  // segments of <= this many nodes use the team Riccati sweep, longer ones the scan
+  int ls_block;     // step sizes evaluated per line-search round (<= 0: all alpha_levels at once)
 };
 
 // IterationRecord (solver.hpp:547-561).
@@ -60,6 +61,7 @@ struct DevResult {  // SolveReport (solver.hpp:572-582) minus the records
   double final_cost, final_violation, final_defect_l1;
   double times[6];  // setup, backward (all), 0, forward, line search, total [s]
   double final_penalty, final_mu, final_reg;
+  double alpha_evals;  // step sizes evaluated by the line search (all passes)
 };
 
 // ------------------------------------------------------------------ topology

@@ -243,6 +243,40 @@ def test_deterministic_and_launch_shapes_agree(ctx):
         assert _gen.rel_err(x, outs[0][0]) <= 1e-10
 
 
+def test_line_search_rounds_do_not_change_results():
+    """Evaluating the step sizes in rounds (stop at the first round holding an
+    accepted alpha) returns exactly what the all-at-once parallel search does."""
+    probs = [B.build_intersection_case(B.intersection_spec(63, 10.0, 0.1), 2, 2, perturb_seed=s)
+             for s in (601, 622, 3409, 4035)]  # 3409 / 4035: long AL runs with rejected steps
+    outs = {}
+    for blk in (0, 1, 2, 3, 11):
+        c = B.Context(0)
+        B.set_line_search_block(c, blk)
+        bt = B.Batch(c, probs, max_records=1000)
+        bt.set_models()
+        bt.solve()
+        x = np.zeros((len(probs), bt.n, bt.nx))
+        u = np.zeros((len(probs), bt.n, bt.nu))
+        reps, _ = bt.results(x, u)
+        recs = [bt.records(i) for i in range(len(probs))]
+        outs[blk] = (x, u, reps, recs)
+    x0, u0, r0, rec0 = outs[0]
+    assert all(r.alpha_evals == 11 * r.n_records for r in r0)
+    for blk, (x, u, reps, recs) in outs.items():
+        np.testing.assert_array_equal(x, x0)
+        np.testing.assert_array_equal(u, u0)
+        for a, b, ra, rb in zip(reps, r0, recs, rec0):
+            assert (a.status, a.inner_iterations, a.outer_iterations, a.n_records) == \
+                (b.status, b.inner_iterations, b.outer_iterations, b.n_records)
+            assert a.final_cost == b.final_cost
+            for k in ra:
+                np.testing.assert_array_equal(ra[k], rb[k])
+        if blk == 1:  # one alpha per round: evaluations = accepted level + 1 (all 11 when rejected)
+            for a, ra in zip(reps, recs):
+                lv = np.where(ra["accepted"] > 0, -np.log2(np.where(ra["alpha"] > 0, ra["alpha"], 1.0)), 10)
+                assert a.alpha_evals == float((lv + 1).sum())
+
+
 def test_native_library_loaded(ctx):
     """The CUDA path is the one that ran: the in-tree .so is mapped and
     launched kernels."""

@@ -11,7 +11,7 @@ import paper_2506_13624_b200 as B
 cnt = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 ctx = B.Context(0)
 probs = [B.build_intersection_case(B.intersection_spec(63, 10.0, 0.1), 2, 2, perturb_seed=42 + i) for i in range(cnt)]
-bt = B.Batch(ctx, probs)
+bt = B.Batch(ctx, probs, max_records=1000)
 bt.set_models()
 bt.solve()
 reps, _ = bt.results()
@@ -19,11 +19,13 @@ out = {"passes": np.array([r.n_records + r.outer_iterations for r in reps]),
        "outer": np.array([r.outer_iterations for r in reps]),
        "status": np.array([r.status for r in reps]),
        "x0": np.array([p.initial_state for p in probs])}
-first = {k: [] for k in ("cost", "violation", "defect_l1", "regularization", "alpha", "accepted")}
+K = 60  # first K records of every instance (zero-padded)
+first = {k: [] for k in ("outer", "cost", "violation", "defect_l1", "regularization", "alpha", "accepted")}
 for i in range(cnt):
     rec = bt.records(i, 1000)
     for k in first:
-        first[k].append(rec[k][:3] if len(rec[k]) >= 3 else np.pad(rec[k], (0, 3 - len(rec[k]))))
+        v = np.asarray(rec[k], dtype=float)[:K]
+        first[k].append(np.pad(v, (0, K - len(v))))
 for k, v in first.items():
     out["rec_" + k] = np.array(v)
 os.makedirs("gpurun_out", exist_ok=True)
