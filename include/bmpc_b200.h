@@ -223,6 +223,7 @@ int bmpc_batch_phase_profile(bmpc_batch* batch, int instance, double* out, int n
 /* Diagnostic: dependent-latency probe {DFMA, LDS, FP64 division} in SM cycles. */
 int bmpc_debug_latency_probe(bmpc_ctx* ctx, double* cycles3);
 /* Diagnostic: SM cycles per team-cooperative Riccati step on a chain. */
+/* prefetch == 2: stage-stamped run, cycles[0..5] = total, then per-stage cycles per step. */
 int bmpc_debug_ric_step_cycles(bmpc_ctx* ctx, int steps, int prefetch, double* cycles);
 /* Diagnostic: microseconds per cooperative grid barrier at this launch shape. */
 int bmpc_debug_grid_sync_us(bmpc_ctx* ctx, int blocks, int threads, int iters, double* us);

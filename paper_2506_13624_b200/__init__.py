@@ -560,8 +560,9 @@ def set_line_search_block(ctx: Context, alphas: int):
     _check(lib().bmpc_ctx_set_line_search_block(ctx._h, int(alphas)))
 
 
-def debug_ric_step_cycles(steps: int = 512, prefetch: bool = True, ctx: Optional[Context] = None) -> float:
+def debug_ric_step_cycles(steps: int = 512, prefetch: int = 1, ctx: Optional[Context] = None):
+    """Cycles per isolated team Riccati step; prefetch=2 returns (total, [5 stage cycles])."""
     ctx = ctx or default_context()
-    v = C.c_double()
-    _check(lib().bmpc_debug_ric_step_cycles(ctx._h, int(steps), int(prefetch), C.byref(v)))
-    return v.value
+    v = (C.c_double * 6)()
+    _check(lib().bmpc_debug_ric_step_cycles(ctx._h, int(steps), int(prefetch), v))
+    return (v[0], list(v[1:])) if prefetch == 2 else v[0]

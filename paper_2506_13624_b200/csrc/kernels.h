@@ -81,7 +81,7 @@ cudaError_t launch_pack_results(const Work* d_works, int count, int n, int nx, i
                                 cudaStream_t stream);
 double measure_fp64_peak_tflops(cudaStream_t stream);
 double grid_sync_us(int blocks, int threads, int iters, cudaStream_t stream);
-double ric_step_cycles(int steps, int prefetch, cudaStream_t stream);
+double ric_step_cycles(int steps, int prefetch, cudaStream_t stream, double* stages = nullptr);
 void latency_probe(double* cyc3, cudaStream_t stream);
 
 }  // namespace bmpc_b200

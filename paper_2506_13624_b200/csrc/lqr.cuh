@@ -716,10 +716,21 @@ __device__ __forceinline__ double dot_slot(const double* Fm, const DotSlot& s, d
 // One Bellman step on the team's flat array (stage, c, P, p staged).
 // Overwrites P, p; writes value / policy records. Returns kIndefinite when
 // R + B'PB is not positive definite (lqr_scan.hpp:150, riccati.hpp:31-35).
-template <int NX, int NU, int TS>
-__device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int lane, double* V_g, double* pol_g) {
+// kStamp (diagnostic): lane 0 accumulates clock64 deltas per stage into st[0..4].
+template <int NX, int NU, int TS, bool kStamp = false>
+__device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int lane, double* V_g, double* pol_g,
+                                   unsigned long long* st = nullptr) {
   using F = RicFlat<NX, NU>;
   constexpr int R1 = (F::n1 + TS - 1) / TS, R2 = (F::n2 + TS - 1) / TS, R4 = (F::n4 + TS - 1) / TS;
+  long long ck = 0;
+  auto stamp = [&](int k) {
+    if constexpr (kStamp) {
+      const long long now = clock64();
+      if (lane == 0 && k > 0) st[k - 1] += now - ck;
+      ck = now;
+    }
+  };
+  stamp(0);
   __syncwarp(mask);
   {
     double o[R1];
@@ -734,6 +745,7 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
     for (int r = 0; r < R1; ++r) Fm[oo[r]] = o[r];
   }
   __syncwarp(mask);
+  stamp(1);
   {
     double o[R2];
     short oo[R2];
@@ -747,6 +759,7 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
     for (int r = 0; r < R2; ++r) Fm[oo[r]] = o[r];
   }
   __syncwarp(mask);
+  stamp(2);
   // Huu = sym(Quu); every lane factors it and forms its row of Huu^-1.
   int a3, v3, o3, g3;
   if (lane < NU * NX) {  // K(a, j) = -Hinv(a,:) Qux(:, j)
@@ -785,6 +798,7 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
     if (pol_g && g3 >= 0) pol_g[g3] = -v;
   }
   __syncwarp(mask);
+  stamp(3);
   double o4[R4];
   short oo4[R4], g4[R4];
 #pragma unroll
@@ -817,12 +831,14 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
     o4[r] = 0.5 * (a + b);
   }
   __syncwarp(mask);
+  stamp(4);
 #pragma unroll
   for (int r = 0; r < R4; ++r) {
     Fm[oo4[r]] = o4[r];
     if (V_g && g4[r] >= 0) V_g[g4[r]] = o4[r];
   }
   const unsigned bad = __ballot_sync(mask, !pos);
+  stamp(5);
   return bad ? kIndefinite : kBwdOk;
 }
 

@@ -116,6 +116,7 @@ double grid_sync_us(int blocks, int threads, int iters, cudaStream_t stream) {
 
 namespace bmpc_b200 {
 
+template <bool kStamp>
 __global__ void ric_bench_kernel(const double* stages, const double* defects, double* vals, double* pols, int steps,
                                  int prefetch, unsigned long long* cycles) {
   constexpr int NX = 4, NU = 2, TS = 16;
@@ -131,6 +132,8 @@ __global__ void ric_bench_kernel(const double* stages, const double* defects, do
   for (int k = lane; k < SL::size; k += TS) Fm[F::S + k] = stages[k];
   if (lane < NX) Fm[F::c + lane] = defects[lane];
   __syncwarp(mask);
+  unsigned long long st[5] = {0, 0, 0, 0, 0};
+
   unsigned long long t0 = clock64();
   int err = 0;
   for (int k = 0; k < steps; ++k) {
@@ -144,8 +147,8 @@ __global__ void ric_bench_kernel(const double* stages, const double* defects, do
       pre[j] = idx < SL::size ? sp[idx] : 0.0;
     }
     if (lane < NX) prec = defects[((k + 1) % steps) * NX + lane];
-    err |= team_riccati_step_u<NX, NU, TS>(0.0, mask, Fm, lane, vals + static_cast<size_t>(k) * 20,
-                                           pols + static_cast<size_t>(k) * 10);
+    err |= team_riccati_step_u<NX, NU, TS, kStamp>(0.0, mask, Fm, lane, vals + static_cast<size_t>(k) * 20,
+                                                   pols + static_cast<size_t>(k) * 10, st);
     __syncwarp(mask);
 #pragma unroll
     for (int j = 0; j < PRE; ++j) {
@@ -158,11 +161,14 @@ __global__ void ric_bench_kernel(const double* stages, const double* defects, do
   if (lane == 0) {
     cycles[0] = t1 - t0;
     cycles[1] = err;
+    for (int q = 0; q < 5; ++q) cycles[2 + q] = st[q];
   }
   (void)prefetch;
 }
 
-double ric_step_cycles(int steps, int prefetch, cudaStream_t stream) {
+// Cycles per isolated team Riccati step; prefetch == 2: stage-stamped run,
+// out[1..5] = cycles per step of each stage (diagnostic).
+double ric_step_cycles(int steps, int prefetch, cudaStream_t stream, double* stages) {
   using SL = StageLayout<4, 2>;
   std::vector<double> hs(static_cast<size_t>(steps) * SL::stride, 0.0), hd(static_cast<size_t>(steps) * 4, 0.01);
   for (int k = 0; k < steps; ++k) {
@@ -176,15 +182,21 @@ double ric_step_cycles(int steps, int prefetch, cudaStream_t stream) {
   cudaMalloc(&dd, hd.size() * 8);
   cudaMalloc(&dv, static_cast<size_t>(steps) * 20 * 8);
   cudaMalloc(&dp, static_cast<size_t>(steps) * 10 * 8);
-  cudaMalloc(&dc, 16);
+  cudaMalloc(&dc, 7 * sizeof(unsigned long long));
   cudaMemcpy(ds, hs.data(), hs.size() * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(dd, hd.data(), hd.size() * 8, cudaMemcpyHostToDevice);
-  ric_bench_kernel<<<1, 16, 0, stream>>>(ds, dd, dv, dp, steps, prefetch, dc);
-  ric_bench_kernel<<<1, 16, 0, stream>>>(ds, dd, dv, dp, steps, prefetch, dc);
-  unsigned long long hc[2];
-  cudaMemcpyAsync(hc, dc, 16, cudaMemcpyDeviceToHost, stream);
+  for (int r = 0; r < 2; ++r) {
+    if (prefetch == 2)
+      ric_bench_kernel<true><<<1, 16, 0, stream>>>(ds, dd, dv, dp, steps, prefetch, dc);
+    else
+      ric_bench_kernel<false><<<1, 16, 0, stream>>>(ds, dd, dv, dp, steps, prefetch, dc);
+  }
+  unsigned long long hc[7];
+  cudaMemcpyAsync(hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, stream);
   cudaStreamSynchronize(stream);
   cudaFree(ds), cudaFree(dd), cudaFree(dv), cudaFree(dp), cudaFree(dc);
+  if (stages)
+    for (int q = 0; q < 5; ++q) stages[q] = static_cast<double>(hc[2 + q]) / steps;
   return static_cast<double>(hc[0]) / steps;
 }
 
