@@ -579,6 +579,14 @@ DevOptions to_dev(const bmpc_options& o) {
   return d;
 }
 
+// Column-major n x n with exact zeros off the diagonal.
+bool is_diag(const double* w, int n) {
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i)
+      if (i != j && w[i + n * j] != 0.0) return false;
+  return true;
+}
+
 void fill_report(const DevResult& r, bmpc_report* out) {
   out->status = r.status;
   out->error_code = r.error_code;
@@ -999,6 +1007,8 @@ int bmpc_batch_set_models(bmpc_batch* b, const bmpc_model_desc* models, size_t* 
         mp.a_max = m.accel_limit;
         mp.w_max = m.yaw_rate_limit;
         mp.radius = m.safety_radius;
+        // BMPC_DENSE_MODEL=1 forces the dense expansion (tests compare both bitwise).
+        mp.w_diag = is_diag(mp.Wx, 4) && is_diag(mp.Wu, 2) && is_diag(mp.Wf, 4) && !std::getenv("BMPC_DENSE_MODEL");
         std::memcpy(md, m.reference, n * 4 * sizeof(double));
         if (b->nv > 0) std::memcpy(md + align2(n * 4), m.vehicle_position, n * static_cast<size_t>(b->nv) * 2 * sizeof(double));
       } else {
@@ -1032,6 +1042,7 @@ int bmpc_batch_replicate(bmpc_batch* b) {
       b->h_mps[static_cast<size_t>(i)].a_max = b->h_mps[0].a_max;
       b->h_mps[static_cast<size_t>(i)].w_max = b->h_mps[0].w_max;
       b->h_mps[static_cast<size_t>(i)].radius = b->h_mps[0].radius;
+      b->h_mps[static_cast<size_t>(i)].w_diag = b->h_mps[0].w_diag;
       ck(cudaMemcpyAsync(b->model_data.as<double>() + static_cast<size_t>(i) * b->node_data_doubles,
                          b->model_data.as<double>(), b->node_data_doubles * sizeof(double), cudaMemcpyDeviceToDevice,
                          s),

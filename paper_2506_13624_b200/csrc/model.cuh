@@ -38,17 +38,26 @@ __device__ __forceinline__ void unicycle_derivative(const double* x, const doubl
   dx[3] = u[0];
 }
 
-// unicycle::step (unicycle.hpp:36-42).
+// unicycle::step (unicycle.hpp:36-42). The heading at stages 2 and 3 is the
+// same expression psi + dt/2 * u1 (psi' = u1), so its sincos is shared.
 __device__ __forceinline__ void unicycle_step(const double* x, const double* u, double dt, double* xn) {
   double k1[4], k2[4], k3[4], k4[4], t[4];
   unicycle_derivative(x, u, k1);
   const double hdt = 0.5 * dt;
 #pragma unroll
   for (int i = 0; i < 4; ++i) t[i] = x[i] + hdt * k1[i];
-  unicycle_derivative(t, u, k2);
+  double s2, c2;
+  sincos(t[2], &s2, &c2);
+  k2[0] = t[3] * c2;
+  k2[1] = t[3] * s2;
+  k2[2] = u[1];
+  k2[3] = u[0];
 #pragma unroll
   for (int i = 0; i < 4; ++i) t[i] = x[i] + hdt * k2[i];
-  unicycle_derivative(t, u, k3);
+  k3[0] = t[3] * c2;  // t[2] == x[2] + hdt * u[1] again
+  k3[1] = t[3] * s2;
+  k3[2] = u[1];
+  k3[3] = u[0];
 #pragma unroll
   for (int i = 0; i < 4; ++i) t[i] = x[i] + dt * k3[i];
   unicycle_derivative(t, u, k4);
@@ -140,6 +149,55 @@ __device__ __forceinline__ void unicycle_step_jacobians(const double* x, const d
   for (int i = 0; i < 8; ++i) B[i] = s6 * (((dk1u[i] + 2.0 * dk2u[i]) + 2.0 * dk3u[i]) + dk4u[i]);
 }
 
+// unicycle_step_jacobians on its sparsity, bit-identical to the dense chain
+// rule above for finite inputs: the stage Jacobians J only couple (px, py) to
+// (psi, v), whose own dynamics are trivial, so dk_s/dx = J_s exactly, the
+// stage-3 point has the stage-2 heading and speed (J_3 = J_2), and every
+// dropped term of the dense products is an exact zero. Three sincos instead
+// of seven, no 4x4 products.
+__device__ __forceinline__ void unicycle_step_jacobians_sparse(const double* x, const double* u, double dt,
+                                                               double* A, double* B) {
+  const double hdt = 0.5 * dt;
+  const double psi2 = x[2] + hdt * u[1], v2 = x[3] + hdt * u[0];  // stages 2 and 3
+  const double psi4 = x[2] + dt * u[1], v4 = x[3] + dt * u[0];
+  double s1, c1, s2, c2, s4, c4;
+  sincos(x[2], &s1, &c1);
+  sincos(psi2, &s2, &c2);
+  sincos(psi4, &s4, &c4);
+  // J(0,2) = -v s, J(0,3) = c, J(1,2) = v c, J(1,3) = s at each stage point.
+  const double j1[4] = {-x[3] * s1, c1, x[3] * c1, s1};
+  const double j2[4] = {-v2 * s2, c2, v2 * c2, s2};
+  const double j4[4] = {-v4 * s4, c4, v4 * c4, s4};
+  const double s6 = dt / 6.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) A[i] = (i % 5 == 0) ? 1.0 : 0.0;
+  // A(r, c) for r in {0,1}, c in {2,3}: entry e = 2r + (c - 2).
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+#pragma unroll
+    for (int c = 2; c < 4; ++c) {
+      const int e = 2 * r + (c - 2);
+      A[r + 4 * c] = 0.0 + s6 * (((j1[e] + 2.0 * j2[e]) + 2.0 * j2[e]) + j4[e]);
+    }
+  }
+  // B rows 0,1: dk_s u(r, 0) = J_s(r,3) h_s, dk_s u(r, 1) = J_s(r,2) h_s (h = dt/2, dt/2, dt);
+  // rows 2,3: the selector Ju, B(2,1) = B(3,0) = s6 * 6.
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+#pragma unroll
+    for (int cu = 0; cu < 2; ++cu) {
+      const int e = 2 * r + (cu == 0 ? 1 : 0);
+      const double d2 = j2[e] * hdt, d3 = j2[e] * hdt, d4 = j4[e] * dt;
+      B[r + 4 * cu] = s6 * (((0.0 + 2.0 * d2) + 2.0 * d3) + d4);
+    }
+  }
+  const double sel = s6 * (((1.0 + 2.0 * 1.0) + 2.0 * 1.0) + 1.0);
+  B[2 + 4 * 0] = s6 * (((0.0 + 2.0 * 0.0) + 2.0 * 0.0) + 0.0);
+  B[3 + 4 * 0] = sel;
+  B[2 + 4 * 1] = sel;
+  B[3 + 4 * 1] = B[2 + 4 * 0];
+}
+
 // ego_constraints (scenarios.hpp:206-248) values and, optionally, Jacobians.
 // Rows: [a-amax, -a-amax, w-wmax, -w-wmax] (non-leaf) then r - sqrt(d^2+eps).
 template <bool kJac>
@@ -200,6 +258,14 @@ __device__ __forceinline__ double quad_form(const double* W, const double* e) {
   mv<N, N>(W, e, We);
   return 0.5 * dot<N>(e, We);
 }
+// Same value for a diagonal W (the dropped terms of mv are exact zeros).
+template <int N>
+__device__ __forceinline__ double quad_form_diag(const double* W, const double* e) {
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) s = fma(e[i], W[(N + 1) * i] * e[i], s);
+  return 0.5 * s;
+}
 
 // ----------------------------------------------------------- generic node API
 // Dynamics f(x, u) of non-leaf `node`.
@@ -235,7 +301,9 @@ __device__ __forceinline__ void node_cost(const ModelParams& mp, int node, bool 
       double e[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) e[i] = x[i] - ref[i];
-      if (leaf) {
+      if (mp.w_diag) {
+        *cost = leaf ? quad_form_diag<4>(mp.Wf, e) : quad_form_diag<4>(mp.Wx, e) + quad_form_diag<2>(mp.Wu, u);
+      } else if (leaf) {
         *cost = quad_form<4>(mp.Wf, e);
       } else {
         *cost = quad_form<4>(mp.Wx, e) + quad_form<2>(mp.Wu, u);
@@ -268,6 +336,88 @@ __device__ __forceinline__ void node_cost(const ModelParams& mp, int node, bool 
   }
 }
 
+// Structured form of the unicycle expansion below for diagonal weights: the
+// same operations on the non-zero pattern (box rows have Ju = +-1 and Jx = 0,
+// distance rows Jx in columns 0-1 only, M = 0), so the stage record is
+// bit-identical to the dense path for finite inputs at a fraction of the work
+// and registers.
+__device__ __forceinline__ bool unicycle_linearize_structured(const ModelParams& mp, int node, bool leaf, double w,
+                                                              const double* x, const double* u, const double* eta,
+                                                              double rho, double* rec) {
+  using L = StageLayout<4, 2>;
+  const double* ref = mp.reference + static_cast<long long>(node) * 4;
+  const double* W = leaf ? mp.Wf : mp.Wx;
+  double q[4], Q[4];  // diagonal of Q
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    Q[i] = W[5 * i];
+    q[i] = W[5 * i] * (x[i] - ref[i]);
+  }
+  // Distance rows: Jx(m, 0..1) = -(dx, dy) / dist; q += Jx' lam, Q(0..1, 0..1) += Jx' diag(as) Jx.
+  const int nb = leaf ? 0 : 4;
+  const double* vp = mp.vehicles + static_cast<long long>(node) * mp.nv * 2;
+  double sq0 = 0.0, sq1 = 0.0, s00 = 0.0, s10 = 0.0, s01 = 0.0, s11 = 0.0;
+#pragma unroll
+  for (int v = 0; v < kMaxVehicles; ++v) {
+    if (v < mp.nv) {
+      const double dx = x[0] - vp[2 * v + 0];
+      const double dy = x[1] - vp[2 * v + 1];
+      const double dist = sqrt(dx * dx + dy * dy + 1e-6);
+      const double g = mp.radius - dist;
+      const double e = eta[nb + v];
+      const double as = (g >= 0.0 || e > 0.0) ? rho : 0.0;
+      const double lam = e + as * g;
+      const double j0 = -dx / dist, j1 = -dy / dist;
+      sq0 = fma(j0, lam, sq0);
+      sq1 = fma(j1, lam, sq1);
+      s00 = fma(j0 * as, j0, s00);
+      s10 = fma(j1 * as, j0, s10);
+      s01 = fma(j0 * as, j1, s01);
+      s11 = fma(j1 * as, j1, s11);
+    }
+  }
+  double Qf[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) Qf[i] = (i % 5 == 0) ? Q[i / 5] + 0.0 : 0.0 + 0.0;
+  Qf[0] = Q[0] + s00;
+  Qf[1] = 0.0 + s10;
+  Qf[4] = 0.0 + s01;
+  Qf[5] = Q[1] + s11;
+  q[0] += sq0;
+  q[1] += sq1;
+  q[2] += 0.0;
+  q[3] += 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) rec[L::Q + i] = w * Qf[i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) rec[L::q + i] = w * q[i];
+  if (leaf) return all_finite<16>(rec + L::Q) && all_finite<4>(rec + L::q);
+  // Box rows [a - amax, -a - amax, w - wmax, -w - wmax]: Ju = (+1, -1) on u0, u1.
+  double as[4], lam[4];
+  {
+    const double g[4] = {u[0] - mp.a_max, -u[0] - mp.a_max, u[1] - mp.w_max, -u[1] - mp.w_max};
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      as[m] = (g[m] >= 0.0 || eta[m] > 0.0) ? rho : 0.0;
+      lam[m] = eta[m] + as[m] * g[m];
+    }
+  }
+  double r0 = mp.Wu[0] * u[0], r1 = mp.Wu[3] * u[1];
+  r0 += fma(-1.0, lam[1], fma(1.0, lam[0], 0.0));
+  r1 += fma(-1.0, lam[3], fma(1.0, lam[2], 0.0));
+  rec[L::R + 0] = w * (mp.Wu[0] + fma(-as[1], -1.0, fma(as[0], 1.0, 0.0)));
+  rec[L::R + 1] = w * (0.0 + 0.0);
+  rec[L::R + 2] = w * (0.0 + 0.0);
+  rec[L::R + 3] = w * (mp.Wu[3] + fma(-as[3], -1.0, fma(as[2], 1.0, 0.0)));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) rec[L::M + i] = w * (0.0 + 0.0);
+  rec[L::r + 0] = w * r0;
+  rec[L::r + 1] = w * r1;
+  unicycle_step_jacobians_sparse(x, u, mp.dt, rec + L::A, rec + L::B);
+  return all_finite<16>(rec + L::A) && all_finite<8>(rec + L::B) && all_finite<16>(rec + L::Q) &&
+         all_finite<4>(rec + L::R) && all_finite<4>(rec + L::q) && all_finite<2>(rec + L::r);
+}
+
 // linearize (solver.hpp:76-136) of one node: weighted, AL-augmented
 // Gauss-Newton stage record (non-leaf) or terminal (P, p) in the Q/q slots.
 // Returns false on a non-finite expansion.
@@ -276,6 +426,7 @@ __device__ __forceinline__ bool node_linearize(const ModelParams& mp, int node, 
                                                const double* u, const double* eta, double rho, double* rec) {
   using L = StageLayout<NX, NU>;
   if constexpr (NX == 4 && NU == 2) {
+    if (mp.kind == kModelUnicycle && mp.w_diag) return unicycle_linearize_structured(mp, node, leaf, w, x, u, eta, rho, rec);
     if (mp.kind == kModelUnicycle) {
       const double* ref = mp.reference + static_cast<long long>(node) * 4;
       double e[4];
@@ -352,7 +503,7 @@ __device__ __forceinline__ bool node_linearize(const ModelParams& mp, int node, 
           M[i + 2 * j] += s;
         }
       }
-      unicycle_step_jacobians(x, u, mp.dt, rec + L::A, rec + L::B);
+      unicycle_step_jacobians_sparse(x, u, mp.dt, rec + L::A, rec + L::B);
 #pragma unroll
       for (int i = 0; i < 16; ++i) rec[L::Q + i] = w * Q[i];
 #pragma unroll

@@ -16,6 +16,7 @@ struct ModelParams {
   double dt;
   double Wx[16], Wu[4], Wf[16];
   double a_max, w_max, radius;
+  int w_diag;               // Wx, Wu, Wf all diagonal: structured (zero-skipping) expansion, same bits
   const double* reference;  // [node][4]
   const double* vehicles;   // [node][nv][2]
   // affine-quadratic

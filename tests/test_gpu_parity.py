@@ -277,6 +277,37 @@ def test_line_search_rounds_do_not_change_results():
                 assert a.alpha_evals == float((lv + 1).sum())
 
 
+def test_structured_expansion_matches_dense(ctx, monkeypatch):
+    """Diagonal weights take the zero-skipping unicycle expansion; it must be
+    bit-identical to the dense chain rule."""
+    probs = [B.build_intersection_case(B.intersection_spec(63, 10.0, 0.1), 2, 2, perturb_seed=s)
+             for s in (7, 601, 3409)]
+    probs.append(B.build_latency_case(B.latency_spec(0.5)))
+    outs = []
+    for dense in (False, True):
+        if dense:
+            monkeypatch.setenv("BMPC_DENSE_MODEL", "1")
+        else:
+            monkeypatch.delenv("BMPC_DENSE_MODEL", raising=False)
+        res = []
+        for p in probs:
+            bt = B.Batch(ctx, [p], max_records=1000)
+            bt.set_models()
+            bt.solve()
+            x = np.zeros((1, bt.n, bt.nx))
+            u = np.zeros((1, bt.n, bt.nu))
+            reps, _ = bt.results(x, u)
+            res.append((x, u, reps[0], bt.records(0)))
+        outs.append(res)
+    for (xa, ua, ra, reca), (xb, ub, rb, recb) in zip(*outs):
+        np.testing.assert_array_equal(xa, xb)
+        np.testing.assert_array_equal(ua, ub)
+        assert (ra.inner_iterations, ra.outer_iterations, ra.final_cost) == \
+            (rb.inner_iterations, rb.outer_iterations, rb.final_cost)
+        for k in reca:
+            np.testing.assert_array_equal(reca[k], recb[k])
+
+
 def test_native_library_loaded(ctx):
     """The CUDA path is the one that ran: the in-tree .so is mapped and
     launched kernels."""
