@@ -17,7 +17,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libbmpc_b200.so")
+LIB_PATH = os.environ.get("BMPC_LIB") or os.path.join(_HERE, "_lib", "libbmpc_b200.so")  # BMPC_LIB: A/B builds
 
 CONVERGED, MAX_ITERATIONS, ERROR = 0, 1, 2
 STATUS_NAMES = {CONVERGED: "converged", MAX_ITERATIONS: "max-iter", ERROR: "error"}  # solver.hpp:538-545
@@ -531,7 +531,7 @@ def debug_grid_sync_us(blocks: int, threads: int, iters: int = 2000, ctx: Option
 
 
 PHASES = ("linearize", "bwd_terminal_elements", "bwd_scan", "feedback", "fwd_elements", "fwd_scan", "fwd_sweep",
-          "line_search", "merit", "step_al")
+          "line_search", "merit", "step_al", "ec_du")
 
 
 def batch_phase_profile(batch: "Batch", instance: int = 0) -> dict:

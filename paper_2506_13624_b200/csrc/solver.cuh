@@ -794,6 +794,7 @@ struct Solver {
       g.sync();
       }
     }
+    mark(6);
     // EC terms per node (solver.hpp:416-428).
     double a1 = 0.0, a2 = 0.0;
     for (int i = g.rank(); i < t.n; i += g.size()) {
@@ -823,7 +824,7 @@ struct Solver {
     red_put(g.sm, 0, a1, true);
     red_put(g.sm, 1, a2, true);
     g.finish(2, 2);
-    mark(6);
+    mark(10);
     *a1_out = g.sm->total[0];
     *a2_out = g.sm->total[1];
   }
