@@ -165,6 +165,12 @@ int bmpc_ctx_set_seq_max_len(bmpc_ctx* ctx, int len);
  * search; later rounds run only when a whole round is rejected
  * (0 = all alpha_levels in one round; default 2, env BMPC_LS_BLOCK). */
 int bmpc_ctx_set_line_search_block(bmpc_ctx* ctx, int alphas);
+/* Batch schedule for batches larger than one resident wave: a probe launch
+ * runs every instance for `probe_passes` inner passes and suspends it, the
+ * instances are ordered by their last constraint violation (largest first),
+ * and a second launch resumes them; results are bit-identical to one launch
+ * (0 = one FIFO launch; default 10, env BMPC_PROBE). */
+int bmpc_ctx_set_schedule(bmpc_ctx* ctx, int probe_passes);
 /* Number of kernels this ctx launched since creation (evidence counter). */
 long long bmpc_ctx_launch_count(const bmpc_ctx* ctx);
 

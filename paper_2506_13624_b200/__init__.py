@@ -560,6 +560,12 @@ def set_line_search_block(ctx: Context, alphas: int):
     _check(lib().bmpc_ctx_set_line_search_block(ctx._h, int(alphas)))
 
 
+def set_schedule(ctx: Context, probe_passes: int):
+    """Batch schedule: probe passes before ordering instances by their last
+    constraint violation (0 = one FIFO launch). Results are identical."""
+    _check(lib().bmpc_ctx_set_schedule(ctx._h, int(probe_passes)))
+
+
 def debug_ric_step_cycles(steps: int = 512, prefetch: int = 1, ctx: Optional[Context] = None):
     """Cycles per isolated team Riccati step; prefetch=2 returns (total, [5 stage cycles])."""
     ctx = ctx or default_context()

@@ -628,6 +628,7 @@ void fill_report(const DevResult& r, bmpc_report* out) {
 struct bmpc_ctx {
   int seq_max_len{-1};  // segments <= this length use the team Riccati sweep (-1: default)
   int ls_block{-1};     // step sizes per line-search round (-1: default, 0: all levels at once)
+  int probe{-1};        // batch schedule: probe passes before ordering (-1: default, 0: one FIFO launch)
   int device{0};
   cudaStream_t stream{nullptr};
   bool own_stream{false};
@@ -652,6 +653,19 @@ static int ls_block_for(const bmpc_ctx* c) {
   return 2;
 }
 
+// Batch schedule. Pass counts of perturbed instances are heavy-tailed (cfg4:
+// mean 85, max 856), so a FIFO launch ends with a tail of long solves that
+// started late. When the batch exceeds one wave, a probe launch runs every
+// instance for `probe` passes and suspends it (bit-identical resume), the
+// instances are ordered by their last constraint violation (the best cheap
+// predictor of a long AL run measured on cfg4), and the main launch resumes
+// them longest-expected first.
+static int probe_for(const bmpc_ctx* c) {
+  if (c && c->probe >= 0) return c->probe;
+  if (const char* env = std::getenv("BMPC_PROBE")) return std::atoi(env);
+  return 10;
+}
+
 // Device-resident instances sharing one plan.
 struct bmpc_batch {
   bmpc_ctx* ctx{nullptr};
@@ -659,7 +673,7 @@ struct bmpc_batch {
   int count{0}, nx{0}, nu{0}, kind{0}, nv{0}, max_records{0};
   size_t node_data_doubles{0};  // per instance: reference+vehicles or lq stage+leaf
   Strides st{};
-  DevBuf model_data, x0, state, records, results, mps, works, red, prof;
+  DevBuf model_data, x0, state, records, results, mps, works, red, prof, resume, order;
   std::vector<ModelParams> h_mps;
   std::vector<Work> h_works;
   size_t per_state_doubles{0};
@@ -862,6 +876,12 @@ int bmpc_ctx_set_seq_max_len(bmpc_ctx* c, int len) {
   return BMPC_OK;
 }
 
+int bmpc_ctx_set_schedule(bmpc_ctx* c, int probe_passes) {
+  if (!c) return fail(BMPC_ERR_INVALID, "null ctx");
+  c->probe = probe_passes;
+  return BMPC_OK;
+}
+
 int bmpc_ctx_set_line_search_block(bmpc_ctx* c, int alphas) {
   if (!c) return fail(BMPC_ERR_INVALID, "null ctx");
   c->ls_block = alphas;
@@ -918,6 +938,8 @@ int bmpc_batch_create(bmpc_ctx* ctx, const bmpc_tree* tree, int count, const bmp
     b->results = DevBuf(C * sizeof(DevResult));
     b->mps = DevBuf(C * sizeof(ModelParams));
     b->works = DevBuf(C * sizeof(Work));
+    b->resume = DevBuf(C * sizeof(DevResume));
+    b->order = DevBuf(C * sizeof(int));
     // Grid mode for a single large tree: all SMs on one instance.
     b->grid_mode = count == 1 && tree->node_count > 1024;
     if (b->grid_mode) {
@@ -958,6 +980,7 @@ int bmpc_batch_create(bmpc_ctx* ctx, const bmpc_tree* tree, int count, const bmp
       w.value = s + off[10];
       w.records = b->records.as<DevRecord>() + i * static_cast<size_t>(std::max(b->max_records, 1));
       w.max_records = b->max_records;
+      w.resume = b->grid_mode ? nullptr : b->resume.as<DevResume>() + i;
       w.result = b->results.as<DevResult>() + i;
       w.prof = nullptr;
     }
@@ -1108,11 +1131,32 @@ static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_input
     e = launch_solve_grid(b->nx, b->nu, b->plan->d_topo.as<Topo>(), b->mps.as<ModelParams>(), b->works.as<Work>(), d,
                           b->red.as<double>(), b->grid_blocks, b->threads, b->ctx->stream);
   } else {
-    e = launch_solve_cta(b->nx, b->nu, b->plan->d_topo.as<Topo>(), b->mps.as<ModelParams>(), b->works.as<Work>(), d,
-                         b->count, b->cta_threads, b->cta_min_blocks, seq_only(b, d.seq_max_len), b->ctx->stream);
+    cudaStream_t s = b->ctx->stream;
+    const bool so = seq_only(b, d.seq_max_len);
+    auto launch = [&]() {
+      ++b->ctx->launches;
+      return launch_solve_cta(b->nx, b->nu, b->plan->d_topo.as<Topo>(), b->mps.as<ModelParams>(),
+                              b->works.as<Work>(), d, b->count, b->cta_threads, b->cta_min_blocks, so, s);
+    };
+    e = cudaMemsetAsync(b->resume.p, 0, static_cast<size_t>(b->count) * sizeof(DevResume), s);
+    const int probe = probe_for(b->ctx);
+    const int wave = std::max(1, b->ctx->sms * b->cta_min_blocks);
+    if (e == cudaSuccess && probe > 0 && b->count > wave) {
+      d.pass_budget = probe;
+      e = launch();
+      if (e == cudaSuccess) {
+        ++b->ctx->launches;
+        e = launch_order_by_key(b->resume.as<DevResume>(), b->count, b->order.as<int>(), s);
+      }
+      d.pass_budget = 0;
+      d.order = b->order.as<int>();
+      if (e == cudaSuccess) e = launch();
+    } else if (e == cudaSuccess) {
+      e = launch();
+    }
   }
   if (e != cudaSuccess) return fail(BMPC_ERR_CUDA, std::string("solve launch: ") + cudaGetErrorString(e));
-  ++b->ctx->launches;
+  if (b->grid_mode) ++b->ctx->launches;
   return BMPC_OK;
 }
 

@@ -13,6 +13,7 @@ struct Topo;
 struct ModelParams;
 struct Work;
 struct DevOptions;
+struct DevResume;
 
 // Per-node / per-slot strides (doubles) of the device layouts for (nx, nu).
 struct Strides {
@@ -77,6 +78,7 @@ size_t sizeof_dev_record();
 constexpr int kRedSlotsHost = 64;
 
 // util.cu
+cudaError_t launch_order_by_key(const DevResume* d_resume, int count, int* d_order, cudaStream_t stream);
 cudaError_t launch_pack_results(const Work* d_works, int count, int n, int nx, int nu, double* dst,
                                 cudaStream_t stream);
 double measure_fp64_peak_tflops(cudaStream_t stream);

@@ -31,8 +31,8 @@ __global__ void __launch_bounds__(THREADS, MINB) solve_cta_kernel(const Topo* __
                                                         int count) {
   __shared__ RedSmem red;
   __shared__ BlockCtx ctx;
-  const int b = blockIdx.x;
-  if (b >= count) return;
+  if (static_cast<int>(blockIdx.x) >= count) return;
+  const int b = opts.order ? opts.order[blockIdx.x] : static_cast<int>(blockIdx.x);
   if (threadIdx.x == 0) {
     ctx.topo = *topo;
     ctx.mp = mps[b];

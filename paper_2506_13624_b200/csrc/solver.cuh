@@ -1061,38 +1061,90 @@ struct Solver {
 
   // ------------------------------------------------------------- solve
   __device__ void solve() {
-    const double t_start = now_s();
+    double t_start = now_s();
     double times[6] = {0, 0, 0, 0, 0, 0};
     DevResult* res = w.result;
-    if (g.leader()) {
-      res->status = kError;
-      res->error_code = kErrNone;
-      res->error_node = -1;
-      res->inner_iterations = 0;
-      res->outer_iterations = 0;
-      res->n_records = 0;
-    }
-    if (o.alpha_levels < 1 || o.alpha_levels > kMaxAlpha) {
-      if (g.leader()) res->error_code = kErrAlphaLevels;
-      return;
-    }
-    // eta = 0; the caller filled w.u with the initial inputs.
-    for (int i = g.rank(); i < t.n * t.max_con; i += g.size()) w.eta[i] = 0.0;
-    g_rho = o.penalty_init;
-    if (!rollout()) {
-      if (g.leader()) res->error_code = kErrRolloutNonfinite;
-      return;
-    }
-    double mu = o.merit_mu_init;
-    double reg = o.reg_init;
+    DevResume* rs = w.resume;
+    const int rstate = rs ? rs->state : 0;
+    if (rstate == 2) return;  // finished in an earlier launch
+    double mu, reg, last_viol = 0.0;
     bool inner_converged = false, failed = false;
     int status = kError, err_code = kErrNone, err_node = -1;
-    int inner = 0, outer_count = 0, nrec = 0, alpha_evals = 0;
+    int inner = 0, outer_count = 0, nrec = 0, alpha_evals = 0, outer0 = 0, pass0 = 0;
+    if (rstate == 1) {  // resume at the top of inner pass (outer0, pass0)
+      outer0 = rs->outer;
+      pass0 = rs->pass;
+      outer_count = rs->outer_count;
+      inner = rs->inner;
+      nrec = rs->nrec;
+      alpha_evals = rs->alpha_evals;
+      mu = rs->mu;
+      reg = rs->reg;
+      g_rho = rs->rho;
+      last_viol = rs->key;
+      t_start -= rs->elapsed;
+      for (int k = 0; k < 6; ++k) times[k] = rs->times[k];
+    } else {
+      if (g.leader()) {
+        res->status = kError;
+        res->error_code = kErrNone;
+        res->error_node = -1;
+        res->inner_iterations = 0;
+        res->outer_iterations = 0;
+        res->n_records = 0;
+      }
+      if (o.alpha_levels < 1 || o.alpha_levels > kMaxAlpha) {
+        if (g.leader()) {
+          res->error_code = kErrAlphaLevels;
+          if (rs) rs->state = 2;
+        }
+        return;
+      }
+      // eta = 0; the caller filled w.u with the initial inputs.
+      for (int i = g.rank(); i < t.n * t.max_con; i += g.size()) w.eta[i] = 0.0;
+      g_rho = o.penalty_init;
+      if (!rollout()) {
+        if (g.leader()) {
+          res->error_code = kErrRolloutNonfinite;
+          if (rs) rs->state = 2;
+        }
+        return;
+      }
+      mu = o.merit_mu_init;
+      reg = o.reg_init;
+    }
+    int budget_used = 0;
+    bool resumed = rstate == 1;
 
-    for (int outer = 0; outer < o.max_outer_iterations; ++outer) {
-      ++outer_count;
-      inner_converged = false;
-      for (int pass = 0; pass < o.max_inner_iterations; ++pass) {
+    for (int outer = outer0; outer < o.max_outer_iterations; ++outer) {
+      int pass_start = 0;
+      if (resumed) {
+        pass_start = pass0;
+        resumed = false;
+      } else {
+        ++outer_count;
+        inner_converged = false;
+      }
+      for (int pass = pass_start; pass < o.max_inner_iterations; ++pass) {
+        if (rs && o.pass_budget > 0 && budget_used++ >= o.pass_budget) {
+          // Suspend: everything the loop carries lives in (x, u, eta, records) or here.
+          if (g.leader()) {
+            rs->state = 1;
+            rs->outer = outer;
+            rs->pass = pass;
+            rs->outer_count = outer_count;
+            rs->inner = inner;
+            rs->nrec = nrec;
+            rs->alpha_evals = alpha_evals;
+            rs->mu = mu;
+            rs->reg = reg;
+            rs->rho = g_rho;
+            rs->key = last_viol;
+            rs->elapsed = now_s() - t_start;
+            for (int k = 0; k < 6; ++k) rs->times[k] = times[k];
+          }
+          return;
+        }
         double t0 = now_s();
         int bad = 0;
         mark(9);
@@ -1162,6 +1214,7 @@ struct Solver {
           rec.violation = ev.max_violation;
           if (g.leader() && nrec < w.max_records) w.records[nrec] = rec;
           ++nrec;
+          last_viol = rec.violation;
           if (reg > o.reg_max) {
             err_code = kErrLineSearch;
             failed = true;
@@ -1179,6 +1232,7 @@ struct Solver {
         rec.violation = after.max_violation;
         if (g.leader() && nrec < w.max_records) w.records[nrec] = rec;
         ++nrec;
+        last_viol = rec.violation;
       }
       if (failed) break;
       const Eval ev = evaluate_current();
@@ -1211,6 +1265,7 @@ struct Solver {
       res->final_defect_l1 = fin.defect_l1;
       for (int k = 0; k < 6; ++k) res->times[k] = times[k];
       res->final_penalty = g_rho;
+      if (rs) rs->state = 2;
       res->alpha_evals = alpha_evals;
       res->final_mu = mu;
       res->final_reg = reg;

@@ -37,6 +37,17 @@ struct DevOptions {  // SolverOptions (solver.hpp:28-58), device copy
   int zero_inputs;  // 1: initial inputs are zero (solver.hpp:604-609), skip the H2D
   int seq_max_len;  // segments of <= this many nodes use the team Riccati sweep, longer ones the scan
   int ls_block;     // step sizes evaluated per line-search round (<= 0: all alpha_levels at once)
+  int pass_budget;  // > 0: suspend a solve after this many inner passes in this launch (Work::resume)
+  const int* order; // optional block -> instance map of a batch launch (nullptr: identity)
+};
+
+// Suspended solve() loop state (batch scheduling): a solve can stop at the top
+// of an inner pass and continue in a later launch with bit-identical results.
+struct DevResume {
+  int state;  // 0 fresh, 1 suspended, 2 finished
+  int outer, pass, outer_count, inner, nrec, alpha_evals, pad;
+  double mu, reg, rho, elapsed, key;  // key: last recorded constraint violation (scheduling priority)
+  double times[6];
 };
 
 // IterationRecord (solver.hpp:547-561).
@@ -104,6 +115,7 @@ struct Work {
   int max_records;
   DevResult* result;
   double* prof;  // optional [kProfSlots] per-phase device time (ns), leader-accumulated
+  DevResume* resume;  // optional suspend / resume state
 };
 
 }  // namespace bmpc_b200

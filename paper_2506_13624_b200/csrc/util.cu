@@ -25,6 +25,66 @@ __global__ void pack_results_kernel(const Work* __restrict__ works, int count, i
   }
 }
 
+// Batch scheduling: order instances by their suspended-solve key (descending:
+// the largest constraint violation after the probe launch first; finished
+// instances last), ties by index. One block, bitonic sort in shared memory;
+// beyond kMaxSortCount the identity order is used.
+constexpr int kMaxSortCount = 8192;
+
+__global__ void order_by_key_kernel(const DevResume* __restrict__ rs, int count, int npow2, int* __restrict__ order) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  double* key = reinterpret_cast<double*>(sm);
+  int* idx = reinterpret_cast<int*>(key + npow2);
+  for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+    double k = -INFINITY;
+    if (i < count && rs[i].state == 1 && !isnan(rs[i].key)) k = rs[i].key;
+    key[i] = k;
+    idx[i] = i < count ? i : 0x7fffffff;
+  }
+  __syncthreads();
+  for (int k = 2; k <= npow2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool before = key[i] > key[l] || (key[i] == key[l] && idx[i] < idx[l]);
+          if (((i & k) == 0) != before) {
+            const double tk = key[i];
+            key[i] = key[l];
+            key[l] = tk;
+            const int ti = idx[i];
+            idx[i] = idx[l];
+            idx[l] = ti;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < count; i += blockDim.x) order[i] = idx[i];
+}
+
+__global__ void identity_order_kernel(int count, int* __restrict__ order) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) order[i] = i;
+}
+
+cudaError_t launch_order_by_key(const DevResume* d_resume, int count, int* d_order, cudaStream_t stream) {
+  if (count > kMaxSortCount) {
+    identity_order_kernel<<<64, 256, 0, stream>>>(count, d_order);
+    return cudaGetLastError();
+  }
+  int npow2 = 1;
+  while (npow2 < count) npow2 <<= 1;
+  const size_t smem = static_cast<size_t>(npow2) * (sizeof(double) + sizeof(int));
+  static bool once = (cudaFuncSetAttribute(reinterpret_cast<const void*>(order_by_key_kernel),
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(kMaxSortCount * (sizeof(double) + sizeof(int)))),
+                      true);
+  (void)once;
+  order_by_key_kernel<<<1, 1024, smem, stream>>>(d_resume, count, npow2, d_order);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pack_results(const Work* d_works, int count, int n, int nx, int nu, double* dst,
                                 cudaStream_t stream) {
   pack_results_kernel<<<1184, 256, 0, stream>>>(d_works, count, n, nx, nu, dst);
@@ -133,6 +193,7 @@ __global__ void ric_bench_kernel(const double* stages, const double* defects, do
   if (lane < NX) Fm[F::c + lane] = defects[lane];
   __syncwarp(mask);
   unsigned long long st[5] = {0, 0, 0, 0, 0};
+
 
   unsigned long long t0 = clock64();
   int err = 0;

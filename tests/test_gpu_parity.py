@@ -308,6 +308,39 @@ def test_structured_expansion_matches_dense(ctx, monkeypatch):
             np.testing.assert_array_equal(reca[k], recb[k])
 
 
+def test_probe_schedule_is_bit_identical():
+    """Suspending every solve after a few passes, reordering and resuming it
+    in a second launch gives exactly the single-launch results."""
+    probs = [B.build_intersection_case(B.intersection_spec(63, 10.0, 0.1), 2, 2, perturb_seed=9000 + s)
+             for s in range(200)]
+    outs = {}
+    for probe in (0, 1, 3, 10):
+        c = B.Context(0)
+        B.set_schedule(c, probe)
+        bt = B.Batch(c, probs, max_records=600)
+        bt.set_models()
+        bt.set_launch(256, 1)  # one wave = 148 instances < 200: the schedule engages
+        n0 = c.launches
+        bt.solve()
+        launches = c.launches - n0
+        x = np.zeros((len(probs), bt.n, bt.nx))
+        u = np.zeros((len(probs), bt.n, bt.nu))
+        reps, _ = bt.results(x, u)
+        outs[probe] = (x, u, reps, [bt.records(i, 600) for i in (0, 17, 199)], launches)
+    assert outs[0][4] == 1 and outs[3][4] == 3
+    x0, u0, r0, rec0, _ = outs[0]
+    for probe, (x, u, reps, recs, _) in outs.items():
+        np.testing.assert_array_equal(x, x0)
+        np.testing.assert_array_equal(u, u0)
+        for a, b in zip(reps, r0):
+            assert (a.status, a.inner_iterations, a.outer_iterations, a.n_records, a.alpha_evals) == \
+                (b.status, b.inner_iterations, b.outer_iterations, b.n_records, b.alpha_evals)
+            assert a.final_cost == b.final_cost and a.final_violation == b.final_violation
+        for ra, rb in zip(recs, rec0):
+            for k in ra:
+                np.testing.assert_array_equal(ra[k], rb[k])
+
+
 def test_native_library_loaded(ctx):
     """The CUDA path is the one that ran: the in-tree .so is mapped and
     launched kernels."""
