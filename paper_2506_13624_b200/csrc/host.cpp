@@ -1133,26 +1133,32 @@ static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_input
   } else {
     cudaStream_t s = b->ctx->stream;
     const bool so = seq_only(b, d.seq_max_len);
-    auto launch = [&]() {
+    auto launch = [&](int threads, int min_blocks, int count, cudaStream_t st) {
       ++b->ctx->launches;
       return launch_solve_cta(b->nx, b->nu, b->plan->d_topo.as<Topo>(), b->mps.as<ModelParams>(),
-                              b->works.as<Work>(), d, b->count, b->cta_threads, b->cta_min_blocks, so, s);
+                              b->works.as<Work>(), d, count, threads, min_blocks, so, st);
     };
+    // Experiment knob (tools/): shape "TxM" of the probe launch.
+    int pt = b->cta_threads, pm = b->cta_min_blocks;
+    if (const char* env = std::getenv("BMPC_SHAPE_PROBE")) {
+      int et = 0, em = 0;
+      if (std::sscanf(env, "%dx%d", &et, &em) == 2 && cta_variant_supported(b->nx, b->nu, et, em)) pt = et, pm = em;
+    }
     e = cudaMemsetAsync(b->resume.p, 0, static_cast<size_t>(b->count) * sizeof(DevResume), s);
     const int probe = probe_for(b->ctx);
     const int wave = std::max(1, b->ctx->sms * b->cta_min_blocks);
     if (e == cudaSuccess && probe > 0 && b->count > wave) {
       d.pass_budget = probe;
-      e = launch();
+      e = launch(pt, pm, b->count, s);
       if (e == cudaSuccess) {
         ++b->ctx->launches;
         e = launch_order_by_key(b->resume.as<DevResume>(), b->count, b->order.as<int>(), s);
       }
       d.pass_budget = 0;
       d.order = b->order.as<int>();
-      if (e == cudaSuccess) e = launch();
+      if (e == cudaSuccess) e = launch(b->cta_threads, b->cta_min_blocks, b->count, s);
     } else if (e == cudaSuccess) {
-      e = launch();
+      e = launch(b->cta_threads, b->cta_min_blocks, b->count, s);
     }
   }
   if (e != cudaSuccess) return fail(BMPC_ERR_CUDA, std::string("solve launch: ") + cudaGetErrorString(e));
