@@ -77,6 +77,7 @@ __device__ void lqr_tree_body(G g, BlockCtx& ctx, double reg, double* scalars, i
   ModelParams dummy{};
   DevOptions o{};
   o.seq_max_len = seq_max;
+  o.keep_values = 1;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   Solver<NX, NU, G> s(g, ctx.topo, dummy, ctx.work, o);
   s.tsm = dyn_smem + red_smem_bytes(blockDim.x);

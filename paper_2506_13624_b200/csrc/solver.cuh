@@ -511,15 +511,18 @@ struct Solver {
         __syncwarp(mask);
         if (lane == 0) Fm[F::ZERO] = 0.0;
         if (is_leaf(b)) {
+          // Values are read back only at segment heads (the parent's branch
+          // step); the kernel-level API keeps every node's.
+          const bool keep = o.keep_values || L == 1;
           for (int k = lane; k < NX * NX; k += kTS) {
             const double v = stage(b)[SL::Q + k] + ((k % (NX + 1)) == 0 ? reg : 0.0);
             Fm[F::P + k] = v;
-            val(b)[VL::P + k] = v;
+            if (keep) val(b)[VL::P + k] = v;
           }
           for (int k = lane; k < NX; k += kTS) {
             const double v = stage(b)[SL::q + k];
             Fm[F::p + k] = v;
-            val(b)[VL::p + k] = v;
+            if (keep) val(b)[VL::p + k] = v;
           }
         } else {
           // riccati_tree_from (riccati.hpp:112-116): children in index order.
@@ -542,7 +545,8 @@ struct Solver {
           }
           for (int k = lane; k < SL::size; k += kTS) Fm[F::S + k] = stage(b)[k];
           if (lane < NX) Fm[F::c + lane] = 0.0;
-          const int e = team_riccati_step_u<NX, NU, kTS>(reg, mask, Fm, lane, val(b), pol(b));
+          const int e = team_riccati_step_u<NX, NU, kTS>(reg, mask, Fm, lane,
+                                                         (o.keep_values || L == 1) ? val(b) : nullptr, pol(b));
           err = err ? err : e;
         }
         // Chain nodes tail -> head; the next node's stage record and edge
@@ -574,7 +578,8 @@ struct Solver {
             }
             if (lane < NX) prec = dfc[i * NX + lane];
           }
-          const int e = team_riccati_step_u<NX, NU, kTS>(reg, mask, Fm, lane, vbase + static_cast<size_t>(i) * VL::stride,
+          double* const vi = (k == 0 || o.keep_values) ? vbase + static_cast<size_t>(i) * VL::stride : nullptr;
+          const int e = team_riccati_step_u<NX, NU, kTS>(reg, mask, Fm, lane, vi,
                                                          pbase + static_cast<size_t>(i) * PL::stride);
           err = err ? err : e;
           if (k >= 1) {

@@ -39,6 +39,7 @@ struct DevOptions {  // SolverOptions (solver.hpp:28-58), device copy
   int ls_block;     // step sizes evaluated per line-search round (<= 0: all alpha_levels at once)
   int pass_budget;  // > 0: suspend a solve after this many inner passes in this launch (Work::resume)
   const int* order; // optional block -> instance map of a batch launch (nullptr: identity)
+  int keep_values;  // 1: store (P, p) of every node (kernel-level API); 0: segment heads only
 };
 
 // Suspended solve() loop state (batch scheduling): a solve can stop at the top
