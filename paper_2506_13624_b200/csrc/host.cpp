@@ -687,6 +687,10 @@ struct bmpc_batch {
     if (h_pack) cudaFreeHost(h_pack);
   }
   int cta_min_blocks{1};
+  // Schedule of batches with more instances than SMs (see probe_for):
+  // probe launch shape, main-launch pass budget (0: to completion) and the
+  // low-latency shape that finishes the survivors.
+  int probe_threads{256}, probe_min_blocks{1}, main_budget{0}, fin_threads{256}, fin_min_blocks{1};
   bool grid_mode{false};
   int grid_blocks{0};
 };
@@ -698,24 +702,34 @@ size_t align2(size_t v) { return (v + 1) & ~size_t{1}; }
 // Per-instance block shape: env BMPC_CTA="<threads>x<min_blocks>" overrides
 // the tuned default.
 void default_launch_shape(bmpc_batch* b) {
-  int t = 256, m = 1;
-  if (b->nx == 4 && b->nu == 2 && b->count > 1) {  // batches: more resident instances per SM
-    t = 128;
-    m = 4;
-  }
-  if (const char* env = std::getenv("BMPC_CTA")) {
+  auto env_shape = [&](const char* name, int* t, int* m) {
+    const char* env = std::getenv(name);
     int et = 0, em = 0;
-    if (std::sscanf(env, "%dx%d", &et, &em) == 2 && cta_variant_supported(b->nx, b->nu, et, em)) {
-      t = et;
-      m = em;
-    }
+    if (env && std::sscanf(env, "%dx%d", &et, &em) == 2 && cta_variant_supported(b->nx, b->nu, et, em)) *t = et, *m = em;
+  };
+  // One instance per SM or fewer: 256 threads each (lowest latency). More:
+  // (4,2) batches take the measured cfg4 schedule (tools/probe_exp.sh):
+  // 64x8 probe and main launches (highest pass throughput) with a 150-pass
+  // budget, survivors finished by 256-thread blocks that run nearly alone.
+  int t = 256, m = 1;
+  if (b->nx == 4 && b->nu == 2 && b->count > std::max(1, b->ctx->sms)) {
+    t = 64;
+    m = 8;
+    b->main_budget = 150;
   }
+  env_shape("BMPC_CTA", &t, &m);
   if (!cta_variant_supported(b->nx, b->nu, t, m)) {
     t = 256;
     m = 1;
   }
   b->cta_threads = t;
   b->cta_min_blocks = m;
+  b->probe_threads = t;
+  b->probe_min_blocks = m;
+  env_shape("BMPC_SHAPE_PROBE", &b->probe_threads, &b->probe_min_blocks);
+  if (!cta_variant_supported(b->nx, b->nu, b->fin_threads, b->fin_min_blocks)) b->main_budget = 0;
+  env_shape("BMPC_SHAPE_FINISH", &b->fin_threads, &b->fin_min_blocks);
+  if (const char* env = std::getenv("BMPC_MAIN_BUDGET")) b->main_budget = std::atoi(env);
 }
 
 // Lays out every per-instance array; returns doubles per instance.
@@ -1089,6 +1103,10 @@ int bmpc_batch_set_launch(bmpc_batch* b, int threads, int min_blocks) {
                                           " not compiled for these dims");
   b->cta_threads = threads;
   b->cta_min_blocks = min_blocks;
+  if (!std::getenv("BMPC_SHAPE_PROBE")) {
+    b->probe_threads = threads;
+    b->probe_min_blocks = min_blocks;
+  }
   return BMPC_OK;
 }
 
@@ -1138,27 +1156,26 @@ static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_input
       return launch_solve_cta(b->nx, b->nu, b->plan->d_topo.as<Topo>(), b->mps.as<ModelParams>(),
                               b->works.as<Work>(), d, count, threads, min_blocks, so, st);
     };
-    // Experiment knob (tools/): shape "TxM" of the probe launch.
-    int pt = b->cta_threads, pm = b->cta_min_blocks;
-    if (const char* env = std::getenv("BMPC_SHAPE_PROBE")) {
-      int et = 0, em = 0;
-      if (std::sscanf(env, "%dx%d", &et, &em) == 2 && cta_variant_supported(b->nx, b->nu, et, em)) pt = et, pm = em;
-    }
+    const int pt = b->probe_threads, pm = b->probe_min_blocks, mt = b->cta_threads, mm = b->cta_min_blocks;
+    const int ft = b->fin_threads, fm = b->fin_min_blocks, main_budget = b->main_budget;
     e = cudaMemsetAsync(b->resume.p, 0, static_cast<size_t>(b->count) * sizeof(DevResume), s);
     const int probe = probe_for(b->ctx);
-    const int wave = std::max(1, b->ctx->sms * b->cta_min_blocks);
-    if (e == cudaSuccess && probe > 0 && b->count > wave) {
+    if (e == cudaSuccess && probe > 0 && b->count > std::max(1, b->ctx->sms)) {
       d.pass_budget = probe;
       e = launch(pt, pm, b->count, s);
       if (e == cudaSuccess) {
         ++b->ctx->launches;
         e = launch_order_by_key(b->resume.as<DevResume>(), b->count, b->order.as<int>(), s);
       }
-      d.pass_budget = 0;
+      d.pass_budget = main_budget;
       d.order = b->order.as<int>();
-      if (e == cudaSuccess) e = launch(b->cta_threads, b->cta_min_blocks, b->count, s);
+      if (e == cudaSuccess) e = launch(mt, mm, b->count, s);
+      if (e == cudaSuccess && main_budget > 0) {
+        d.pass_budget = 0;
+        e = launch(ft, fm, b->count, s);
+      }
     } else if (e == cudaSuccess) {
-      e = launch(b->cta_threads, b->cta_min_blocks, b->count, s);
+      e = launch(mt, mm, b->count, s);
     }
   }
   if (e != cudaSuccess) return fail(BMPC_ERR_CUDA, std::string("solve launch: ") + cudaGetErrorString(e));

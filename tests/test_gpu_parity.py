@@ -327,7 +327,7 @@ def test_probe_schedule_is_bit_identical():
         u = np.zeros((len(probs), bt.n, bt.nu))
         reps, _ = bt.results(x, u)
         outs[probe] = (x, u, reps, [bt.records(i, 600) for i in (0, 17, 199)], launches)
-    assert outs[0][4] == 1 and outs[3][4] == 3
+    assert outs[0][4] == 1 and outs[3][4] == 4  # probe, order, main (150-pass budget), finish
     x0, u0, r0, rec0, _ = outs[0]
     for probe, (x, u, reps, recs, _) in outs.items():
         np.testing.assert_array_equal(x, x0)

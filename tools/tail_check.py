@@ -13,14 +13,15 @@ s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
 ctx = B.Context(0, stream=s.cuda_stream)
 cnt = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
-shape = sys.argv[2] if len(sys.argv) > 2 else "128x4"
-t, m = (int(v) for v in shape.split("x"))
+shape = sys.argv[2] if len(sys.argv) > 2 else "default"
+t, m = (int(v) for v in shape.split("x")) if shape != "default" else (0, 8)
 same = len(sys.argv) > 3 and sys.argv[3] == "same"  # identical instances: no tail, steady-state throughput
 probs = [B.build_intersection_case(B.intersection_spec(63, 10.0, 0.1), 2, 2, perturb_seed=None if same else 42 + i)
          for i in range(cnt)]
 bt = B.Batch(ctx, probs)
 bt.set_models()
-bt.set_launch(t, m)
+if shape != "default":
+    bt.set_launch(t, m)
 bt.solve()
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
