@@ -641,26 +641,41 @@ __device__ int team_riccati_step(double reg, int lane, unsigned mask, RicSmem<NX
 
 // ---------------------------------------------------------------------------
 // Divergence-free team Riccati step. Every small product of riccati_step is a
-// "dot slot" out = base (+ reg on a diagonal) + sum_l X[xo + l xs] Y[yo + l ys]
-// over one flat shared array; each lane owns fixed slots, described once per
-// sweep, so all lanes run one instruction stream per stage (4 stages + the
-// redundant NU x NU LDLT).
+// "dot slot" out = base (+ reg on a diagonal) + sum_l X[xo + l] Y[yo + l] over
+// one flat shared array; each lane owns fixed slots, so all lanes run one
+// instruction stream per stage (4 stages + the redundant NU x NU LDLT).
+// Every operand is laid out contiguous (P also as its transpose PT, B'P and
+// A'P row-major), so both operands stream with unit stride and, for even NX,
+// as 16-byte vector loads at even offsets. The products and their order are
+// those of the reference's dense riccati_step.
 template <int NX, int NU>
 struct RicFlat {  // offsets into the team's flat shared array
   using L = StageLayout<NX, NU>;
+  static constexpr int ev(int v) { return (v + 1) & ~1; }
   static constexpr int S = 0, A = L::A, B = L::B, Q = L::Q, R = L::R, M = L::M, q = L::q, r = L::r;
-  static constexpr int P = L::size, p = P + NX * NX, c = p + NX, psh = c + NX, BtP = psh + NX,
-                       AtP = BtP + NU * NX, Qxx = AtP + NX * NX, Qux = Qxx + NX * NX, Quu = Qux + NU * NX,
-                       qx = Quu + NU * NU, qu = qx + NX, K = qu + NU, k = K + NU * NX, ZERO = k + NU,
-                       DUMMY = ZERO + 1, size = DUMMY + 8;
+  static constexpr int P = ev(L::size), PT = P + NX * NX, p = ev(PT + NX * NX), c = ev(p + NX), psh = ev(c + NX),
+                       BtP = ev(psh + NX),         // row-major NU x NX: BtP[a * NX + l] = (B'P)(a, l)
+                       AtP = ev(BtP + NU * NX),    // row-major NX x NX: AtP[i * NX + l] = (A'P)(i, l)
+                       Qxx = ev(AtP + NX * NX), Qux = ev(Qxx + NX * NX), Quu = ev(Qux + NU * NX),
+                       qx = ev(Quu + NU * NU), qu = ev(qx + NX), K = ev(qu + NU), k = ev(K + NU * NX),
+                       ZERO = ev(k + NU), DUMMY = ZERO + ev(NX), size = DUMMY + 8;
   static constexpr int n1 = NX + NU * NX + NX * NX;                  // psh, B'P, A'P
   static constexpr int n2 = NX * NX + NU * NX + NU * NU + NX + NU;   // Qxx, Qux, Quu, qx, qu
   static constexpr int n3 = NU * NX + NU;                            // K, k
   static constexpr int n4 = NX * NX + NX;                            // P, p
+  static constexpr bool kVec = NX % 2 == 0;  // all X / Y operand offsets even
 };
 
+// P(i, j) (column-major index k = i + NX j) and its transposed copy.
+template <int NX, int NU>
+__device__ __forceinline__ void ric_put_P(double* Fm, int k, double v) {
+  using F = RicFlat<NX, NU>;
+  Fm[F::P + k] = v;
+  Fm[F::PT + (k % NX) * NX + k / NX] = v;
+}
+
 struct DotSlot {
-  short bo, xo, xs, yo, ys, oo;
+  short bo, xo, yo, oo;
   bool diag;  // add the Levenberg shift (Quu diagonal)
 };
 
@@ -669,16 +684,16 @@ struct DotSlot {
 template <int NX, int NU>
 __device__ __forceinline__ DotSlot ric_slot1(int q) {
   using F = RicFlat<NX, NU>;
-  if (q < NX) return {short(F::p + q), short(F::P + q), NX, F::c, 1, short(F::psh + q), false};  // psh = p + P c
-  if (q < NX + NU * NX) {  // B'P (a, j)
-    const int t = q - NX, a = t % NU, j = t / NU;
-    return {F::ZERO, short(F::B + a * NX), 1, short(F::P + j * NX), 1, short(F::BtP + t), false};
+  if (q < NX) return {short(F::p + q), short(F::PT + q * NX), F::c, short(F::psh + q), false};  // psh = p + P c
+  if (q < NX + NU * NX) {  // B'P (a, j) = B(:, a) . P(:, j)
+    const int t = q - NX, a = t / NX, j = t % NX;
+    return {F::ZERO, short(F::B + a * NX), short(F::P + j * NX), short(F::BtP + t), false};
   }
-  if (q < F::n1) {  // A'P (i, j)
-    const int t = q - NX - NU * NX, i = t % NX, j = t / NX;
-    return {F::ZERO, short(F::A + i * NX), 1, short(F::P + j * NX), 1, short(F::AtP + t), false};
+  if (q < F::n1) {  // A'P (i, j) = A(:, i) . P(:, j)
+    const int t = q - NX - NU * NX, i = t / NX, j = t % NX;
+    return {F::ZERO, short(F::A + i * NX), short(F::P + j * NX), short(F::AtP + t), false};
   }
-  return {F::ZERO, F::ZERO, 0, F::ZERO, 0, F::DUMMY, false};
+  return {F::ZERO, F::ZERO, F::ZERO, F::DUMMY, false};
 }
 
 template <int NX, int NU>
@@ -686,30 +701,41 @@ __device__ __forceinline__ DotSlot ric_slot2(int q) {
   using F = RicFlat<NX, NU>;
   if (q < NX * NX) {  // Qxx = Q + A'P A
     const int i = q % NX, j = q / NX;
-    return {short(F::Q + q), short(F::AtP + i), NX, short(F::A + j * NX), 1, short(F::Qxx + q), false};
+    return {short(F::Q + q), short(F::AtP + i * NX), short(F::A + j * NX), short(F::Qxx + q), false};
   }
   q -= NX * NX;
   if (q < NU * NX) {  // Qux = M + B'P A
     const int a = q % NU, j = q / NU;
-    return {short(F::M + q), short(F::BtP + a), NU, short(F::A + j * NX), 1, short(F::Qux + q), false};
+    return {short(F::M + q), short(F::BtP + a * NX), short(F::A + j * NX), short(F::Qux + q), false};
   }
   q -= NU * NX;
   if (q < NU * NU) {  // Quu = R (+reg) + B'P B
     const int a = q % NU, b = q / NU;
-    return {short(F::R + q), short(F::BtP + a), NU, short(F::B + b * NX), 1, short(F::Quu + q), a == b};
+    return {short(F::R + q), short(F::BtP + a * NX), short(F::B + b * NX), short(F::Quu + q), a == b};
   }
   q -= NU * NU;
-  if (q < NX) return {short(F::q + q), short(F::A + q * NX), 1, F::psh, 1, short(F::qx + q), false};  // qx
+  if (q < NX) return {short(F::q + q), short(F::A + q * NX), F::psh, short(F::qx + q), false};  // qx
   q -= NX;
-  if (q < NU) return {short(F::r + q), short(F::B + q * NX), 1, F::psh, 1, short(F::qu + q), false};  // qu
-  return {F::ZERO, F::ZERO, 0, F::ZERO, 0, F::DUMMY, false};
+  if (q < NU) return {short(F::r + q), short(F::B + q * NX), F::psh, short(F::qu + q), false};  // qu
+  return {F::ZERO, F::ZERO, F::ZERO, F::DUMMY, false};
 }
 
-template <int LEN>
+template <int LEN, bool kVec>
 __device__ __forceinline__ double dot_slot(const double* Fm, const DotSlot& s, double reg) {
   double a = Fm[s.bo] + (s.diag ? reg : 0.0);
+  if constexpr (kVec && LEN % 2 == 0) {
+    const double2* X = reinterpret_cast<const double2*>(Fm + s.xo);
+    const double2* Y = reinterpret_cast<const double2*>(Fm + s.yo);
 #pragma unroll
-  for (int l = 0; l < LEN; ++l) a = fma(Fm[s.xo + l * s.xs], Fm[s.yo + l * s.ys], a);
+    for (int l = 0; l < LEN / 2; ++l) {
+      const double2 x = X[l], y = Y[l];
+      a = fma(x.x, y.x, a);
+      a = fma(x.y, y.y, a);
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < LEN; ++l) a = fma(Fm[s.xo + l], Fm[s.yo + l], a);
+  }
   return a;
 }
 
@@ -738,7 +764,7 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
 #pragma unroll
     for (int r = 0; r < R1; ++r) {
       const DotSlot sl = ric_slot1<NX, NU>(lane + r * TS);
-      o[r] = dot_slot<NX>(Fm, sl, 0.0);
+      o[r] = dot_slot<NX, F::kVec>(Fm, sl, 0.0);
       oo[r] = sl.oo;
     }
 #pragma unroll
@@ -752,7 +778,7 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
 #pragma unroll
     for (int r = 0; r < R2; ++r) {
       const DotSlot sl = ric_slot2<NX, NU>(lane + r * TS);
-      o[r] = dot_slot<NX>(Fm, sl, reg);
+      o[r] = dot_slot<NX, F::kVec>(Fm, sl, reg);
       oo[r] = sl.oo;
     }
 #pragma unroll
@@ -800,13 +826,15 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
   __syncwarp(mask);
   stamp(3);
   double o4[R4];
-  short oo4[R4], g4[R4];
+  short oo4[R4], ot4[R4], g4[R4];
 #pragma unroll
   for (int r = 0; r < R4; ++r) {
     const int q = lane + r * TS;
     double a = 0.0, b = 0.0;
+    ot4[r] = F::DUMMY;
     if (q < NX * NX) {  // P(i,j) = sym(Qxx + Qux' K)
       const int i = q % NX, j = q / NX;
+      ot4[r] = short(F::PT + i * NX + j);
       a = Fm[F::Qxx + q];
       b = Fm[F::Qxx + j + i * NX];
 #pragma unroll
@@ -835,6 +863,7 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
 #pragma unroll
   for (int r = 0; r < R4; ++r) {
     Fm[oo4[r]] = o4[r];
+    Fm[ot4[r]] = o4[r];
     if (V_g && g4[r] >= 0) V_g[g4[r]] = o4[r];
   }
   const unsigned bad = __ballot_sync(mask, !pos);

@@ -489,7 +489,7 @@ struct Solver {
   __host__ __device__ static constexpr size_t slot_bytes() {
     constexpr size_t a = sizeof(TeamSmem<NX>) > sizeof(RicSmem<NX, NU>) ? sizeof(TeamSmem<NX>) : sizeof(RicSmem<NX, NU>);
     constexpr size_t b = sizeof(double) * RicFlat<NX, NU>::size;
-    return a > b ? a : b;
+    return ((a > b ? a : b) + 15) / 16 * 16;  // 16-byte aligned slots (vector loads)
   }
 
   // Team Riccati sweep of every (short) segment at depth d: terminal (leaf
@@ -509,14 +509,14 @@ struct Solver {
         const SegIdx sq = seg_idx(s);
         const int b = node_at(sq, L - 1);
         __syncwarp(mask);
-        if (lane == 0) Fm[F::ZERO] = 0.0;
+        if (lane < NX) Fm[F::ZERO + lane] = 0.0;
         if (is_leaf(b)) {
           // Values are read back only at segment heads (the parent's branch
           // step); the kernel-level API keeps every node's.
           const bool keep = o.keep_values || L == 1;
           for (int k = lane; k < NX * NX; k += kTS) {
             const double v = stage(b)[SL::Q + k] + ((k % (NX + 1)) == 0 ? reg : 0.0);
-            Fm[F::P + k] = v;
+            ric_put_P<NX, NU>(Fm, k, v);
             if (keep) val(b)[VL::P + k] = v;
           }
           for (int k = lane; k < NX; k += kTS) {
@@ -530,7 +530,7 @@ struct Solver {
           for (int k = lane; k < NX * NX; k += kTS) {
             double a = 0.0;
             for (int ch = c0; ch < c0 + nc; ++ch) a += value_ptr(ch)[k];
-            Fm[F::P + k] = a;
+            ric_put_P<NX, NU>(Fm, k, a);
           }
           for (int k = lane; k < NX; k += kTS) {
             double a = 0.0;

@@ -182,12 +182,12 @@ __global__ void ric_bench_kernel(const double* stages, const double* defects, do
   constexpr int NX = 4, NU = 2, TS = 16;
   using SL = StageLayout<NX, NU>;
   using F = RicFlat<NX, NU>;
-  __shared__ double Fm[F::size];
+  __shared__ __align__(16) double Fm[F::size];
   const int lane = threadIdx.x;
   const unsigned mask = 0xffffu;
   for (int k = lane; k < F::size; k += TS) Fm[k] = 0.0;
   __syncwarp(mask);
-  for (int k = lane; k < NX * NX; k += TS) Fm[F::P + k] = (k % 5 == 0) ? 1.0 : 0.0;
+  for (int k = lane; k < NX * NX; k += TS) ric_put_P<NX, NU>(Fm, k, (k % 5 == 0) ? 1.0 : 0.0);
   if (lane < NX) Fm[F::p + lane] = 0.1;
   for (int k = lane; k < SL::size; k += TS) Fm[F::S + k] = stages[k];
   if (lane < NX) Fm[F::c + lane] = defects[lane];
