@@ -42,10 +42,10 @@ __global__ void __launch_bounds__(THREADS, MINB) solve_cta_kernel(const Topo* __
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   red.part = reinterpret_cast<double*>(dyn_smem);
   __syncthreads();
-  Solver<NX, NU, CtaGroup, SEQ> s(CtaGroup{&red}, ctx.topo, ctx.mp, ctx.work, opts);
-  s.tsm = dyn_smem + red_smem_bytes(blockDim.x);
+  Solver<NX, NU, CtaGroupT<THREADS>, SEQ> s(CtaGroupT<THREADS>{&red}, ctx.topo, ctx.mp, ctx.work, opts);
+  s.tsm = dyn_smem + red_smem_bytes(THREADS);
   s.wbuf = reinterpret_cast<double*>(s.tsm);
-  s.wcap = blockDim.x;
+  s.wcap = THREADS;
   s.solve();
 }
 

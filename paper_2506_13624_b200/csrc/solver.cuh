@@ -85,10 +85,14 @@ struct RedSmem {
 // Reductions are two-stage and deterministic: warps butterfly-reduce (every
 // lane ends with the same bits) into per-warp slots; slots are then folded
 // in a fixed order. Slot k < nsum are sums, the rest maxima.
-struct CtaGroup {
+// kBlock > 0: block size known at compile time (per-instance kernels), so
+// strides, warp counts and slot offsets fold to immediates.
+template <int kBlock = 0>
+struct CtaGroupT {
   RedSmem* sm;
+  __device__ static int bdim() { return kBlock > 0 ? kBlock : static_cast<int>(blockDim.x); }
   __device__ int rank() const { return threadIdx.x; }
-  __device__ int size() const { return blockDim.x; }
+  __device__ int size() const { return bdim(); }
   __device__ int block() const { return 0; }
   __device__ int nblocks() const { return 1; }
   __device__ bool leader() const { return threadIdx.x == 0; }
@@ -96,8 +100,8 @@ struct CtaGroup {
   // Fold warp partials sm->part[0..nslot) into sm->total (all threads see it).
   __device__ void finish(int nslot, int nsum) const {
     __syncthreads();
-    const int nw = (blockDim.x + 31) >> 5;
-    for (int k = threadIdx.x; k < nslot; k += blockDim.x) {
+    const int nw = (bdim() + 31) >> 5;
+    for (int k = threadIdx.x; k < nslot; k += bdim()) {
       const double* pk = sm->part + k * nw;
       double a = pk[0];
       for (int w = 1; w < nw; ++w) a = k < nsum ? a + pk[w] : fmax(a, pk[w]);
@@ -106,9 +110,11 @@ struct CtaGroup {
     __syncthreads();
   }
 };
+using CtaGroup = CtaGroupT<0>;
 
 struct GridGroup {
   RedSmem* sm;
+  __device__ static int bdim() { return blockDim.x; }
   double* scratch;  // [2][gridDim.x][kRedSlots] global partials (double-buffered)
   int* parity;      // per-block private counter lives in smem via sm->flag
   __device__ int rank() const { return blockIdx.x * blockDim.x + threadIdx.x; }
@@ -149,16 +155,18 @@ struct GridGroup {
 };
 
 // Contribute this thread's value to slot k (every thread of the block must call).
-__device__ __forceinline__ void red_put(RedSmem* sm, int k, double v, bool is_sum) {
+template <class G>
+__device__ __forceinline__ void red_put(const G& g, int k, double v, bool is_sum) {
   v = is_sum ? warp_sum(v) : warp_max(v);
-  if ((threadIdx.x & 31) == 0) sm->part[k * (blockDim.x >> 5) + (threadIdx.x >> 5)] = v;
+  if ((threadIdx.x & 31) == 0) g.sm->part[k * (G::bdim() >> 5) + (threadIdx.x >> 5)] = v;
 }
 
 // Like red_put, but accumulates into the warp's slot (first: overwrite).
-__device__ __forceinline__ void red_acc(RedSmem* sm, int k, double v, bool is_sum, bool first) {
+template <class G>
+__device__ __forceinline__ void red_acc(const G& g, int k, double v, bool is_sum, bool first) {
   v = is_sum ? warp_sum(v) : warp_max(v);
   if ((threadIdx.x & 31) == 0) {
-    double* slot = sm->part + k * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    double* slot = g.sm->part + k * (G::bdim() >> 5) + (threadIdx.x >> 5);
     *slot = first ? v : (is_sum ? *slot + v : fmax(*slot, v));
   }
 }
@@ -257,7 +265,7 @@ struct Solver {
       }
       g.sync();
     }
-    red_put(g.sm, 0, bad, false);
+    red_put(g, 0, bad, false);
     g.finish(1, 0);
     if (g.sm->total[0] > 0.0) {
       if (g.leader()) w.result->error_node = static_cast<int>(g.sm->total[0]) - 1;
@@ -328,10 +336,10 @@ struct Solver {
       dl += d;
       vm = fmax(vm, v);
     }
-    red_put(g.sm, 0, c, true);
-    red_put(g.sm, 1, cal, true);
-    red_put(g.sm, 2, dl, true);
-    red_put(g.sm, 3, vm, false);
+    red_put(g, 0, c, true);
+    red_put(g, 1, cal, true);
+    red_put(g, 2, dl, true);
+    red_put(g, 3, vm, false);
     g.finish(4, 3);
     return {g.sm->total[0], g.sm->total[1], g.sm->total[2], fmax(g.sm->total[3], 0.0)};
   }
@@ -357,11 +365,11 @@ struct Solver {
       const bool dok = all_finite<NX>(w.defect + i * NX);
       if (!(ok && dok) && bad == 0) bad = i + 1;
     }
-    red_put(g.sm, 0, c, true);
-    red_put(g.sm, 1, cal, true);
-    red_put(g.sm, 2, dl, true);
-    red_put(g.sm, 3, vm, false);
-    red_put(g.sm, 4, bad, false);
+    red_put(g, 0, c, true);
+    red_put(g, 1, cal, true);
+    red_put(g, 2, dl, true);
+    red_put(g, 3, vm, false);
+    red_put(g, 4, bad, false);
     g.finish(5, 3);
     *bad_node = static_cast<int>(g.sm->total[4]);
     return {g.sm->total[0], g.sm->total[1], g.sm->total[2], fmax(g.sm->total[3], 0.0)};
@@ -686,8 +694,8 @@ struct Solver {
       for (int j = 0; j < NU; ++j) m = fmax(m, fabs(pol(i)[PL::k + j]));
       mff = fmax(mff, m);
     }
-    red_put(g.sm, 0, mff, false);
-    red_put(g.sm, 1, static_cast<double>(err), false);
+    red_put(g, 0, mff, false);
+    red_put(g, 1, static_cast<double>(err), false);
     g.finish(2, 0);
     mark(3);
     *max_ff = g.sm->total[0];
@@ -826,8 +834,8 @@ struct Solver {
         a2 += (0.5 * dot<NX>(dxi, Qdx) + dot<NU>(dui, Mdx)) + 0.5 * dot<NU>(dui, Rdu);
       }
     }
-    red_put(g.sm, 0, a1, true);
-    red_put(g.sm, 1, a2, true);
+    red_put(g, 0, a1, true);
+    red_put(g, 1, a2, true);
     g.finish(2, 2);
     mark(10);
     *a1_out = g.sm->total[0];
@@ -882,7 +890,7 @@ struct Solver {
     const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
     const int nb = g.nblocks(), b = g.block();
     const int T = L - 1;  // transitions inside a segment
-    const int lr = threadIdx.x, ls = blockDim.x;
+    const int lr = threadIdx.x, ls = G::bdim();
     const int nmine = se - sb > b ? (se - sb - b + nb - 1) / nb : 0;
     const int grp = min(ls, wcap);
     for (int j0 = 0; j0 < nmine; j0 += grp) {
@@ -996,10 +1004,10 @@ struct Solver {
             }
           }
           const bool first = base == 0;
-          red_acc(g.sm, 3 * q + 0, c, true, first);
-          red_acc(g.sm, 3 * q + 1, cal, true, first);
-          red_acc(g.sm, 3 * q + 2, dl, true, first);
-          red_acc(g.sm, 3 * nl + q, vm, false, first);
+          red_acc(g, 3 * q + 0, c, true, first);
+          red_acc(g, 3 * q + 1, cal, true, first);
+          red_acc(g, 3 * q + 2, dl, true, first);
+          red_acc(g, 3 * nl + q, vm, false, first);
         }
       }
       g.finish(4 * nl, 3 * nl);
