@@ -536,11 +536,13 @@ PHASES = ("linearize", "bwd_terminal_elements", "bwd_scan", "feedback", "fwd_ele
 
 def batch_phase_profile(batch: "Batch", instance: int = 0) -> dict:
     """Per-phase device time (ms) of one instance after a profiled solve."""
-    out = np.zeros(16)
-    _check(lib().bmpc_batch_phase_profile(batch._h, int(instance), _ptr(out), 16))
+    out = np.zeros(24)
+    _check(lib().bmpc_batch_phase_profile(batch._h, int(instance), _ptr(out), 24))
     res = {name: out[i] * 1e-6 for i, name in enumerate(PHASES)}
     if out[13] > 0:  # diagnostic counters, not times
         res["sweep_cycles_per_step"] = out[12] / out[13]
+    res["walk_cycles"] = (out[14], out[15], out[11], out[18])  # head_dx, chunk loop, depth walks, walks ns
+    res["sm_mhz"] = 1e3 * out[16] / out[17] if out[17] > 0 else 0.0  # effective SM clock of the solve
     return res
 
 

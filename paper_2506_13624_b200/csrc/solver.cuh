@@ -79,6 +79,7 @@ __device__ __forceinline__ double warp_max(double v) {
 struct RedSmem {
   double* part;  // [kRedSlots][nwarps] warp partials (dynamic shared memory)
   double total[kRedSlots];
+  double prof[kProfSlots];  // profiling accumulators (leader), flushed to Work::prof once per launch
   int flag;
 };
 
@@ -601,8 +602,8 @@ struct Solver {
           }
         }
         if (w.prof && threadIdx.x == 0 && L >= 2) {  // diagnostic: cycles per chain step
-          w.prof[12] += static_cast<double>(clock64() - tc0);
-          w.prof[13] += L - 1;
+          g.sm->prof[12] += static_cast<double>(clock64() - tc0);
+          g.sm->prof[13] += L - 1;
         }
       }
     }
@@ -777,7 +778,18 @@ struct Solver {
     for (int d = 0; d < t.ndepth; ++d) {
       const int L = t.depth_len[d];
       if (seq_len(L)) {
+        long long tf0 = 0, nf0 = 0;
+        if (w.prof && threadIdx.x == 0) {
+          tf0 = clock64();
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(nf0));
+        }
         forward_walk_depth(d);
+        if (w.prof && threadIdx.x == 0) {
+          long long nf1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(nf1));
+          g.sm->prof[11] += static_cast<double>(clock64() - tf0);
+          g.sm->prof[18] += static_cast<double>(nf1 - nf0);
+        }
         continue;
       }
       if constexpr (!kSeqOnly) {
@@ -899,11 +911,18 @@ struct Solver {
       const bool walker = lr < ng;
       SegIdx sq{0, 0, 0};
       double dx[NX];
+      long long th0 = 0;
+      if (w.prof && lr == 0) th0 = clock64();
       if (walker) {
         sq = seg_idx(sb + b + (j0 + lr) * nb);
         head_dx(sq.head, dx);
 #pragma unroll
         for (int j = 0; j < NX; ++j) w.dx[sq.head * NX + j] = dx[j];
+      }
+      if (w.prof && lr == 0) {  // diagnostic (shared-memory accumulators)
+        const long long now = clock64();
+        g.sm->prof[14] += static_cast<double>(now - th0);
+        th0 = now;
       }
       for (int c0 = 0; c0 < T; c0 += C) {
         const int cn = min(C, T - c0);
@@ -928,6 +947,7 @@ struct Solver {
         }
         __syncthreads();
       }
+      if (w.prof && lr == 0) g.sm->prof[15] += static_cast<double>(clock64() - th0);
     }
     g.sync();
   }
@@ -1061,7 +1081,7 @@ struct Solver {
     if (w.prof && g.leader()) {
       unsigned long long ns;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
-      if (prof_last) w.prof[id] += static_cast<double>(ns - prof_last);
+      if (prof_last) g.sm->prof[id] += static_cast<double>(ns - prof_last);
       prof_last = ns;
     }
   }
@@ -1074,6 +1094,24 @@ struct Solver {
 
   // ------------------------------------------------------------- solve
   __device__ void solve() {
+    long long c0 = 0, n0 = 0;
+    if (w.prof && g.leader()) {
+      for (int k = 0; k < kProfSlots; ++k) g.sm->prof[k] = 0.0;
+      c0 = clock64();
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(n0));
+    }
+    solve_body();
+    if (w.prof && g.leader()) {  // SM clock check: cycles and ns of this launch
+      long long n1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(n1));
+      g.sm->prof[16] += static_cast<double>(clock64() - c0);
+      g.sm->prof[17] += static_cast<double>(n1 - n0);
+    }
+    if (w.prof && g.leader())  // one flush per launch (a global RMW per mark costs ~1 us)
+      for (int k = 0; k < kProfSlots; ++k) w.prof[k] += g.sm->prof[k];
+  }
+
+  __device__ void solve_body() {
     double t_start = now_s();
     double times[6] = {0, 0, 0, 0, 0, 0};
     DevResult* res = w.result;

@@ -25,7 +25,7 @@ struct ModelParams {
 };
 
 constexpr int kMaxAlpha = 16;
-constexpr int kProfSlots = 16;
+constexpr int kProfSlots = 24;
 
 // ------------------------------------------------------------------ options
 struct DevOptions {  // SolverOptions (solver.hpp:28-58), device copy
