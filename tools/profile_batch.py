@@ -8,12 +8,13 @@ import numpy as np
 import paper_2506_13624_b200 as B
 
 cnt = int(sys.argv[1]) if len(sys.argv) > 1 else 592
-t, m = (int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else "256x2").split("x"))
+shape = sys.argv[2] if len(sys.argv) > 2 else "default"
 ctx = B.Context(0)
 probs = [B.build_intersection_case(B.intersection_spec(63, 10.0, 0.1), 2, 2, perturb_seed=42 + i) for i in range(cnt)]
 bt = B.Batch(ctx, probs)
 bt.set_models()
-bt.set_launch(t, m)
+if shape != "default":
+    bt.set_launch(*(int(v) for v in shape.split("x")))
 bt.solve()
 reps, _ = bt.results()
 p = np.array([r.n_records + r.outer_iterations for r in reps])
