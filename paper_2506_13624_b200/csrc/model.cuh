@@ -340,11 +340,50 @@ __device__ __forceinline__ void node_cost(const ModelParams& mp, int node, bool 
 // same operations on the non-zero pattern (box rows have Ju = +-1 and Jx = 0,
 // distance rows Jx in columns 0-1 only, M = 0), so the stage record is
 // bit-identical to the dense path for finite inputs at a fraction of the work
-// and registers.
+// and registers. Only the kVar variable entries change between passes; the
+// constant remainder (identity / zero blocks, the input selector of B) is
+// written once per solve by unicycle_stage_constants.
+struct UniRec {
+  using L = StageLayout<4, 2>;
+  static constexpr int kVar = 22;
+  // Dense StageLayout offsets of the variable entries: A(0..1, 2..3), B(0..1, :),
+  // Q(0..1, 0..1) Q22 Q33, R00 R11, q, r. Leaves use the Q / q ones (8..13, 16..19).
+  __host__ __device__ static constexpr int pos(int e) {
+    constexpr int t[kVar] = {L::A + 8,  L::A + 12, L::A + 9, L::A + 13, L::B + 0, L::B + 4, L::B + 1, L::B + 5,
+                             L::Q + 0,  L::Q + 1,  L::Q + 4, L::Q + 5,  L::Q + 10, L::Q + 15, L::R + 0, L::R + 3,
+                             L::q + 0,  L::q + 1,  L::q + 2, L::q + 3,  L::r + 0,  L::r + 1};
+    return t[e];
+  }
+  __host__ __device__ static constexpr bool is_var(int k) {
+    for (int e = 0; e < kVar; ++e)
+      if (pos(e) == k) return true;
+    return false;
+  }
+};
+
+// The constant entries of a structured record (exactly what the dense path writes there).
+__device__ __forceinline__ void unicycle_stage_constants(double dt, bool leaf, double* rec) {
+  using L = StageLayout<4, 2>;
+  const double s6 = dt / 6.0;
+  const double sel = s6 * (((1.0 + 2.0 * 1.0) + 2.0 * 1.0) + 1.0);
+  const double bz = s6 * (((0.0 + 2.0 * 0.0) + 2.0 * 0.0) + 0.0);
+#pragma unroll
+  for (int k = 0; k < L::size; ++k) {
+    if (UniRec::is_var(k)) continue;
+    if (leaf && (k < L::Q || k >= L::R) && !(k >= L::q && k < L::r)) continue;  // leaves: Q, q only
+    double v = 0.0;
+    if (k < L::B) v = ((k - L::A) % 5 == 0) ? 1.0 : 0.0;
+    else if (k == L::B + 3 || k == L::B + 6) v = sel;
+    else if (k == L::B + 2 || k == L::B + 7) v = bz;
+    rec[k] = v;
+  }
+}
+
+// Variable entries v[UniRec::kVar] of a node's structured record; returns false
+// on a non-finite expansion (the constants are finite).
 __device__ __forceinline__ bool unicycle_linearize_structured(const ModelParams& mp, int node, bool leaf, double w,
                                                               const double* x, const double* u, const double* eta,
-                                                              double rho, double* rec) {
-  using L = StageLayout<4, 2>;
+                                                              double rho, double* v) {
   const double* ref = mp.reference + static_cast<long long>(node) * 4;
   const double* W = leaf ? mp.Wf : mp.Wx;
   double q[4], Q[4];  // diagonal of Q
@@ -358,13 +397,13 @@ __device__ __forceinline__ bool unicycle_linearize_structured(const ModelParams&
   const double* vp = mp.vehicles + static_cast<long long>(node) * mp.nv * 2;
   double sq0 = 0.0, sq1 = 0.0, s00 = 0.0, s10 = 0.0, s01 = 0.0, s11 = 0.0;
 #pragma unroll
-  for (int v = 0; v < kMaxVehicles; ++v) {
-    if (v < mp.nv) {
-      const double dx = x[0] - vp[2 * v + 0];
-      const double dy = x[1] - vp[2 * v + 1];
+  for (int vv = 0; vv < kMaxVehicles; ++vv) {
+    if (vv < mp.nv) {
+      const double dx = x[0] - vp[2 * vv + 0];
+      const double dy = x[1] - vp[2 * vv + 1];
       const double dist = sqrt(dx * dx + dy * dy + 1e-6);
       const double g = mp.radius - dist;
-      const double e = eta[nb + v];
+      const double e = eta[nb + vv];
       const double as = (g >= 0.0 || e > 0.0) ? rho : 0.0;
       const double lam = e + as * g;
       const double j0 = -dx / dist, j1 = -dy / dist;
@@ -376,22 +415,21 @@ __device__ __forceinline__ bool unicycle_linearize_structured(const ModelParams&
       s11 = fma(j1 * as, j1, s11);
     }
   }
-  double Qf[16];
+  v[8] = w * (Q[0] + s00);
+  v[9] = w * (0.0 + s10);
+  v[10] = w * (0.0 + s01);
+  v[11] = w * (Q[1] + s11);
+  v[12] = w * (Q[2] + 0.0);
+  v[13] = w * (Q[3] + 0.0);
+  v[16] = w * (q[0] + sq0);
+  v[17] = w * (q[1] + sq1);
+  v[18] = w * (q[2] + 0.0);
+  v[19] = w * (q[3] + 0.0);
+  bool ok = true;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) Qf[i] = (i % 5 == 0) ? Q[i / 5] + 0.0 : 0.0 + 0.0;
-  Qf[0] = Q[0] + s00;
-  Qf[1] = 0.0 + s10;
-  Qf[4] = 0.0 + s01;
-  Qf[5] = Q[1] + s11;
-  q[0] += sq0;
-  q[1] += sq1;
-  q[2] += 0.0;
-  q[3] += 0.0;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) rec[L::Q + i] = w * Qf[i];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) rec[L::q + i] = w * q[i];
-  if (leaf) return all_finite<16>(rec + L::Q) && all_finite<4>(rec + L::q);
+  for (int e = 8; e < 20; ++e)
+    if (e < 14 || e >= 16) ok = ok && isfinite(v[e]);
+  if (leaf) return ok;
   // Box rows [a - amax, -a - amax, w - wmax, -w - wmax]: Ju = (+1, -1) on u0, u1.
   double as[4], lam[4];
   {
@@ -405,17 +443,42 @@ __device__ __forceinline__ bool unicycle_linearize_structured(const ModelParams&
   double r0 = mp.Wu[0] * u[0], r1 = mp.Wu[3] * u[1];
   r0 += fma(-1.0, lam[1], fma(1.0, lam[0], 0.0));
   r1 += fma(-1.0, lam[3], fma(1.0, lam[2], 0.0));
-  rec[L::R + 0] = w * (mp.Wu[0] + fma(-as[1], -1.0, fma(as[0], 1.0, 0.0)));
-  rec[L::R + 1] = w * (0.0 + 0.0);
-  rec[L::R + 2] = w * (0.0 + 0.0);
-  rec[L::R + 3] = w * (mp.Wu[3] + fma(-as[3], -1.0, fma(as[2], 1.0, 0.0)));
+  v[14] = w * (mp.Wu[0] + fma(-as[1], -1.0, fma(as[0], 1.0, 0.0)));
+  v[15] = w * (mp.Wu[3] + fma(-as[3], -1.0, fma(as[2], 1.0, 0.0)));
+  v[20] = w * r0;
+  v[21] = w * r1;
+  // Jacobians (unicycle_step_jacobians_sparse, variable entries only).
+  {
+    const double dt = mp.dt, hdt = 0.5 * dt;
+    const double psi2 = x[2] + hdt * u[1], v2 = x[3] + hdt * u[0];
+    const double psi4 = x[2] + dt * u[1], v4 = x[3] + dt * u[0];
+    double s1, c1, s2, c2, s4, c4;
+    sincos(x[2], &s1, &c1);
+    sincos(psi2, &s2, &c2);
+    sincos(psi4, &s4, &c4);
+    const double j1[4] = {-x[3] * s1, c1, x[3] * c1, s1};
+    const double j2[4] = {-v2 * s2, c2, v2 * c2, s2};
+    const double j4[4] = {-v4 * s4, c4, v4 * c4, s4};
+    const double s6 = dt / 6.0;
+    // v[0..3] = A(0,2) A(0,3) A(1,2) A(1,3); j index e = 2r + (c - 2).
 #pragma unroll
-  for (int i = 0; i < 8; ++i) rec[L::M + i] = w * (0.0 + 0.0);
-  rec[L::r + 0] = w * r0;
-  rec[L::r + 1] = w * r1;
-  unicycle_step_jacobians_sparse(x, u, mp.dt, rec + L::A, rec + L::B);
-  return all_finite<16>(rec + L::A) && all_finite<8>(rec + L::B) && all_finite<16>(rec + L::Q) &&
-         all_finite<4>(rec + L::R) && all_finite<4>(rec + L::q) && all_finite<2>(rec + L::r);
+    for (int e = 0; e < 4; ++e) v[e] = 0.0 + s6 * (((j1[e] + 2.0 * j2[e]) + 2.0 * j2[e]) + j4[e]);
+    // v[4..7] = B(0,0) B(0,1) B(1,0) B(1,1): column 0 uses J(r,3), column 1 J(r,2).
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+#pragma unroll
+      for (int cu = 0; cu < 2; ++cu) {
+        const int e = 2 * r + (cu == 0 ? 1 : 0);
+        const double d2 = j2[e] * hdt, d3 = j2[e] * hdt, d4 = j4[e] * dt;
+        v[4 + 2 * r + cu] = s6 * (((0.0 + 2.0 * d2) + 2.0 * d3) + d4);
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) ok = ok && isfinite(v[e]);
+#pragma unroll
+  for (int e = 14; e < 16; ++e) ok = ok && isfinite(v[e]);
+  return ok && isfinite(v[20]) && isfinite(v[21]);
 }
 
 // linearize (solver.hpp:76-136) of one node: weighted, AL-augmented
@@ -426,7 +489,14 @@ __device__ __forceinline__ bool node_linearize(const ModelParams& mp, int node, 
                                                const double* u, const double* eta, double rho, double* rec) {
   using L = StageLayout<NX, NU>;
   if constexpr (NX == 4 && NU == 2) {
-    if (mp.kind == kModelUnicycle && mp.w_diag) return unicycle_linearize_structured(mp, node, leaf, w, x, u, eta, rho, rec);
+    if (mp.kind == kModelUnicycle && mp.w_diag) {  // constants written once per solve
+      double v[UniRec::kVar];
+      const bool ok = unicycle_linearize_structured(mp, node, leaf, w, x, u, eta, rho, v);
+#pragma unroll
+      for (int e = 0; e < UniRec::kVar; ++e)
+        if (!leaf || (e >= 8 && e < 14) || (e >= 16 && e < 20)) rec[UniRec::pos(e)] = v[e];
+      return ok;
+    }
     if (mp.kind == kModelUnicycle) {
       const double* ref = mp.reference + static_cast<long long>(node) * 4;
       double e[4];

@@ -198,6 +198,9 @@ struct Solver {
       : g(g_), t(t_), mp(mp_), w(w_), o(o_) {}
 
   __device__ bool is_leaf(int i) const { return t.first_child[i] < 0; }
+  // Unicycle with diagonal weights: stage records hold UniRec's variable
+  // entries per pass over per-solve constants (model.cuh).
+  __device__ bool structured() const { return NX == 4 && NU == 2 && mp.kind == kModelUnicycle && mp.w_diag; }
   __device__ double* stage(int i) const { return w.stage + static_cast<size_t>(i) * SL::stride; }
   __device__ double* bwd(int slot) const { return w.bwd + static_cast<size_t>(slot) * BL::stride; }
   __device__ double* fwd(int slot) const { return w.fwd + static_cast<size_t>(slot) * FL::stride; }
@@ -1153,6 +1156,10 @@ struct Solver {
       }
       // eta = 0; the caller filled w.u with the initial inputs.
       for (int i = g.rank(); i < t.n * t.max_con; i += g.size()) w.eta[i] = 0.0;
+      if constexpr (NX == 4 && NU == 2) {
+        if (structured())  // constant part of every stage record, once per solve
+          for (int i = g.rank(); i < t.n; i += g.size()) unicycle_stage_constants(mp.dt, is_leaf(i), stage(i));
+      }
       g_rho = o.penalty_init;
       if (!rollout()) {
         if (g.leader()) {

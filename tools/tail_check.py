@@ -38,4 +38,7 @@ print(f"{shape}: kernel {ms:.1f} ms; instance ms mean {tt.mean():.2f} p50 {np.me
       f"p99 {np.percentile(tt, 99):.2f} max {tt.max():.2f}; sum/slots {tt.sum() / slots:.1f} ms; "
       f"us/pass mean {1e3 * (tt / passes).mean():.1f}")
 top = np.argsort(-tt)[:8]
-print("slowest:", [(int(i), round(float(tt[i]), 1), int(passes[i])) for i in top])
+try:
+    print("slowest:", [(int(i), round(float(tt[i]), 1), int(passes[i])) for i in top], flush=True)
+except BrokenPipeError:
+    pass
