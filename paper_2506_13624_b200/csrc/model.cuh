@@ -361,6 +361,25 @@ struct UniRec {
   }
 };
 
+// Constant value at dense offset k of a non-leaf structured record.
+__device__ __forceinline__ double unicycle_stage_constant(double dt, int k) {
+  using L = StageLayout<4, 2>;
+  const double s6 = dt / 6.0;
+  if (k < L::B) return ((k - L::A) % 5 == 0) ? 1.0 : 0.0;
+  if (k == L::B + 3 || k == L::B + 6) return s6 * (((1.0 + 2.0 * 1.0) + 2.0 * 1.0) + 1.0);
+  if (k == L::B + 2 || k == L::B + 7) return s6 * (((0.0 + 2.0 * 0.0) + 2.0 * 0.0) + 0.0);
+  return 0.0;
+}
+
+// Dense A (4x4) and B (4x2) of a structured record from its variable entries.
+__device__ __forceinline__ void unicycle_load_AB(const double* rec, double dt, double* A, double* B) {
+  using L = StageLayout<4, 2>;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) A[k] = UniRec::is_var(L::A + k) ? rec[L::A + k] : unicycle_stage_constant(dt, L::A + k);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) B[k] = UniRec::is_var(L::B + k) ? rec[L::B + k] : unicycle_stage_constant(dt, L::B + k);
+}
+
 // The constant entries of a structured record (exactly what the dense path writes there).
 __device__ __forceinline__ void unicycle_stage_constants(double dt, bool leaf, double* rec) {
   using L = StageLayout<4, 2>;

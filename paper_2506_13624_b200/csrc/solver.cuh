@@ -828,6 +828,12 @@ struct Solver {
     for (int i = g.rank(); i < t.n; i += g.size()) {
       const double* si = stage(i);
       const double* dxi = w.dx + i * NX;
+      if constexpr (NX == 4 && NU == 2) {
+        if (structured()) {
+          ec_structured(i, si, dxi, &a1, &a2);
+          continue;
+        }
+      }
       double Qdx[NX];
       mv<NX, NX>(si + SL::Q, dxi, Qdx);
       if (is_leaf(i)) {
@@ -866,12 +872,13 @@ struct Solver {
       for (int j = 0; j < NX; ++j) h[j] = w.x0[j] - w.x[j];
       return;
     }
-    const double* sp = stage(p);
+    double A[NX * NX], Bm[NX * NU];
+    load_AB(p, A, Bm);
     double BK[NX * NX], Acl[NX * NX], Bk[NX], t1[NX];
-    mm<NX, NU, NX>(sp + SL::B, pol(p) + PL::K, BK);
+    mm<NX, NU, NX>(Bm, pol(p) + PL::K, BK);
 #pragma unroll
-    for (int j = 0; j < NX * NX; ++j) Acl[j] = sp[SL::A + j] + BK[j];
-    mv<NX, NU>(sp + SL::B, pol(p) + PL::k, Bk);
+    for (int j = 0; j < NX * NX; ++j) Acl[j] = A[j] + BK[j];
+    mv<NX, NU>(Bm, pol(p) + PL::k, Bk);
     mv<NX, NX>(Acl, w.dx + p * NX, t1);
 #pragma unroll
     for (int j = 0; j < NX; ++j) h[j] = (t1[j] + Bk[j]) + w.defect[head * NX + j];
@@ -885,14 +892,59 @@ struct Solver {
   // du = K dx + k is formed per node in the EC phase. Block-local: under a
   // GridGroup each block walks its own share of the depth's segments.
   static constexpr int kWE = NX * NX + 2 * NX;  // walk element: Acl, B k, defect of the next node
-  __device__ void walk_element(int i, int nxt, double* e) const {
-    const double* si = stage(i);
-    const double* po = pol(i);
-    double BK[NX * NX], Bk[NX];
-    mm<NX, NU, NX>(si + SL::B, po + PL::K, BK);
+  // EC terms of one node from a structured record (variable entries only):
+  // the dense products below with the exact-zero terms dropped, same bits.
+  __device__ void ec_structured(int i, const double* si, const double* dxi, double* a1, double* a2) {
+    const double d0 = dxi[0], d1 = dxi[1], d2 = dxi[2], d3 = dxi[3];
+    const double Q00 = si[SL::Q + 0], Q10 = si[SL::Q + 1], Q01 = si[SL::Q + 4], Q11 = si[SL::Q + 5];
+    const double Qdx[4] = {fma(Q01, d1, Q00 * d0), fma(Q11, d1, Q10 * d0), si[SL::Q + 10] * d2,
+                           si[SL::Q + 15] * d3};
+    const double qdx = dot<4>(si + SL::q, dxi);
+    const double xQx = dot<4>(dxi, Qdx);
+    if (is_leaf(i)) {
+      *a1 += qdx;
+      *a2 += 0.5 * xQx;
+      return;
+    }
+    double* dui = w.du + i * NU;
+    if (seq_len(seg_len(t.node_seg[i]))) {  // walked segment: du = K dx + k
+      const double* po = pol(i);
+      double du[NU];
+      mv<NU, NX>(po + PL::K, dxi, du);
 #pragma unroll
-    for (int q = 0; q < NX * NX; ++q) e[q] = si[SL::A + q] + BK[q];
-    mv<NX, NU>(si + SL::B, po + PL::k, Bk);
+      for (int j = 0; j < NU; ++j) dui[j] = du[j] + po[PL::k + j];
+    }
+    const double u0 = dui[0], u1 = dui[1];
+    const double Rdu[2] = {si[SL::R + 0] * u0, si[SL::R + 3] * u1};
+    const double Mdx[2] = {0.0, 0.0};
+    *a1 += qdx + fma(si[SL::r + 1], u1, si[SL::r + 0] * u0);
+    *a2 += (0.5 * xQx + dot<2>(dui, Mdx)) + 0.5 * dot<2>(dui, Rdu);
+  }
+
+  // A, B of node i's stage record (structured records: variable entries only).
+  __device__ void load_AB(int i, double* A, double* Bm) const {
+    const double* si = stage(i);
+    if constexpr (NX == 4 && NU == 2) {
+      if (structured()) {
+        unicycle_load_AB(si, mp.dt, A, Bm);
+        return;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NX * NX; ++q) A[q] = si[SL::A + q];
+#pragma unroll
+    for (int q = 0; q < NX * NU; ++q) Bm[q] = si[SL::B + q];
+  }
+
+  __device__ void walk_element(int i, int nxt, double* e) const {
+    const double* po = pol(i);
+    double A[NX * NX], Bm[NX * NU];
+    load_AB(i, A, Bm);
+    double BK[NX * NX], Bk[NX];
+    mm<NX, NU, NX>(Bm, po + PL::K, BK);
+#pragma unroll
+    for (int q = 0; q < NX * NX; ++q) e[q] = A[q] + BK[q];
+    mv<NX, NU>(Bm, po + PL::k, Bk);
 #pragma unroll
     for (int j = 0; j < NX; ++j) {
       e[NX * NX + j] = Bk[j];
