@@ -573,4 +573,4 @@ def debug_ric_step_cycles(steps: int = 512, prefetch: int = 1, ctx: Optional[Con
     ctx = ctx or default_context()
     v = (C.c_double * 6)()
     _check(lib().bmpc_debug_ric_step_cycles(ctx._h, int(steps), int(prefetch), v))
-    return (v[0], list(v[1:])) if prefetch == 2 else v[0]
+    return (v[0], list(v[1:])) if prefetch >= 2 else v[0]

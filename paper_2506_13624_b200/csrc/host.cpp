@@ -1293,7 +1293,7 @@ int bmpc_batch_phase_profile(bmpc_batch* b, int instance, double* out, int n) {
 int bmpc_debug_ric_step_cycles(bmpc_ctx* ctx, int steps, int prefetch, double* cycles) {
   if (!ctx || !cycles) return fail(BMPC_ERR_INVALID, "null argument");
   cudaSetDevice(ctx->device);
-  *cycles = ric_step_cycles(steps, prefetch, ctx->stream, prefetch == 2 ? cycles + 1 : nullptr);
+  *cycles = ric_step_cycles(steps, prefetch, ctx->stream, prefetch >= 2 ? cycles + 1 : nullptr);
   return cudaGetLastError() == cudaSuccess ? BMPC_OK : fail(BMPC_ERR_CUDA, "ric benchmark failed");
 }
 

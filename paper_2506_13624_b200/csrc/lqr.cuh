@@ -786,15 +786,9 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
   }
   __syncwarp(mask);
   stamp(2);
-  // Huu = sym(Quu); every lane factors it and forms its row of Huu^-1.
-  int a3, v3, o3, g3;
-  if (lane < NU * NX) {  // K(a, j) = -Hinv(a,:) Qux(:, j)
-    a3 = lane % NU, v3 = F::Qux + (lane / NU) * NU, o3 = F::K + lane, g3 = PolicyLayout<NX, NU>::K + lane;
-  } else if (lane < NU * NX + NU) {  // k(a) = -Hinv(a,:) qu
-    a3 = lane - NU * NX, v3 = F::qu, o3 = F::k + a3, g3 = PolicyLayout<NX, NU>::k + a3;
-  } else {
-    a3 = 0, v3 = F::ZERO, o3 = F::DUMMY, g3 = -1;
-  }
+  // Huu = sym(Quu); every lane factors it and forms Huu^-1, then builds the
+  // K / k columns its own outputs need (no shared-memory round trip for K):
+  // K(a, j) = -Huu^-1(a, :) Qux(:, j), k(a) = -Huu^-1(a, :) qu.
   double H[NU * NU];
 #pragma unroll
   for (int t = 0; t < NU * NU; ++t) H[t] = Fm[F::Quu + t];
@@ -802,28 +796,19 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
   Ldlt<NU> f;
   f.compute(H);
   const bool pos = f.positive();
-  double row[NU];
-  {
-    double inv[NU * NU];
+  double inv[NU * NU];
 #pragma unroll
-    for (int t = 0; t < NU * NU; ++t) inv[t] = (t % (NU + 1) == 0) ? 1.0 : 0.0;
-    f.template solve<NU>(inv);
+  for (int t = 0; t < NU * NU; ++t) inv[t] = (t % (NU + 1) == 0) ? 1.0 : 0.0;
+  f.template solve<NU>(inv);
+  auto kcol = [&](const double* v, double* out) {  // out = -Huu^-1 v
 #pragma unroll
-    for (int b = 0; b < NU; ++b) {
-      double v = inv[0 + b * NU];
+    for (int a = 0; a < NU; ++a) {
+      double s = 0.0;
 #pragma unroll
-      for (int a = 1; a < NU; ++a) v = (a == a3) ? inv[a + b * NU] : v;
-      row[b] = v;
+      for (int b = 0; b < NU; ++b) s = fma(inv[a + b * NU], v[b], s);
+      out[a] = -s;
     }
-  }
-  {
-    double v = 0.0;
-#pragma unroll
-    for (int b = 0; b < NU; ++b) v = fma(row[b], Fm[v3 + b], v);
-    Fm[o3] = -v;
-    if (pol_g && g3 >= 0) pol_g[g3] = -v;
-  }
-  __syncwarp(mask);
+  };
   stamp(3);
   double o4[R4];
   short oo4[R4], ot4[R4], g4[R4];
@@ -835,20 +820,43 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
     if (q < NX * NX) {  // P(i,j) = sym(Qxx + Qux' K)
       const int i = q % NX, j = q / NX;
       ot4[r] = short(F::PT + i * NX + j);
+      double qi[NU], qj[NU], Ki[NU], Kj[NU];
+#pragma unroll
+      for (int t = 0; t < NU; ++t) {
+        qi[t] = Fm[F::Qux + t + i * NU];
+        qj[t] = Fm[F::Qux + t + j * NU];
+      }
+      kcol(qi, Ki);
+      kcol(qj, Kj);
+      if (pol_g && i == 0) {  // lanes of column 0 of P hold K(:, j): the policy write
+#pragma unroll
+        for (int t = 0; t < NU; ++t) pol_g[PolicyLayout<NX, NU>::K + t + j * NU] = Kj[t];
+      }
       a = Fm[F::Qxx + q];
       b = Fm[F::Qxx + j + i * NX];
 #pragma unroll
       for (int t = 0; t < NU; ++t) {
-        a = fma(Fm[F::Qux + t + i * NU], Fm[F::K + t + j * NU], a);
-        b = fma(Fm[F::Qux + t + j * NU], Fm[F::K + t + i * NU], b);
+        a = fma(qi[t], Kj[t], a);
+        b = fma(qj[t], Ki[t], b);
       }
       oo4[r] = short(F::P + q);
       g4[r] = short(ValueLayout<NX>::P + q);
     } else if (q < F::n4) {  // p = qx + Qux' k
       const int i = q - NX * NX;
+      double qi[NU], qu[NU], kk[NU];
+#pragma unroll
+      for (int t = 0; t < NU; ++t) {
+        qi[t] = Fm[F::Qux + t + i * NU];
+        qu[t] = Fm[F::qu + t];
+      }
+      kcol(qu, kk);
+      if (pol_g && i == 0) {
+#pragma unroll
+        for (int t = 0; t < NU; ++t) pol_g[PolicyLayout<NX, NU>::k + t] = kk[t];
+      }
       a = Fm[F::qx + i];
 #pragma unroll
-      for (int t = 0; t < NU; ++t) a = fma(Fm[F::Qux + t + i * NU], Fm[F::k + t], a);
+      for (int t = 0; t < NU; ++t) a = fma(qi[t], kk[t], a);
       b = a;
       oo4[r] = short(F::p + i);
       g4[r] = short(ValueLayout<NX>::p + i);
@@ -858,8 +866,9 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
     }
     o4[r] = 0.5 * (a + b);
   }
-  __syncwarp(mask);
   stamp(4);
+  // P, p are no longer read in this step (S1/S2 finished behind barriers);
+  // the next step opens with a __syncwarp.
 #pragma unroll
   for (int r = 0; r < R4; ++r) {
     Fm[oo4[r]] = o4[r];

@@ -176,15 +176,15 @@ double grid_sync_us(int blocks, int threads, int iters, cudaStream_t stream) {
 
 namespace bmpc_b200 {
 
-template <bool kStamp>
+template <bool kStamp, int TS>
 __global__ void ric_bench_kernel(const double* stages, const double* defects, double* vals, double* pols, int steps,
                                  int prefetch, unsigned long long* cycles) {
-  constexpr int NX = 4, NU = 2, TS = 16;
+  constexpr int NX = 4, NU = 2;
   using SL = StageLayout<NX, NU>;
   using F = RicFlat<NX, NU>;
   __shared__ __align__(16) double Fm[F::size];
   const int lane = threadIdx.x;
-  const unsigned mask = 0xffffu;
+  const unsigned mask = TS == 32 ? 0xffffffffu : ((1u << TS) - 1u);
   for (int k = lane; k < F::size; k += TS) Fm[k] = 0.0;
   __syncwarp(mask);
   for (int k = lane; k < NX * NX; k += TS) ric_put_P<NX, NU>(Fm, k, (k % 5 == 0) ? 1.0 : 0.0);
@@ -248,15 +248,17 @@ double ric_step_cycles(int steps, int prefetch, cudaStream_t stream, double* sta
   cudaMemcpy(dd, hd.data(), hd.size() * 8, cudaMemcpyHostToDevice);
   for (int r = 0; r < 2; ++r) {
     if (prefetch == 2)
-      ric_bench_kernel<true><<<1, 16, 0, stream>>>(ds, dd, dv, dp, steps, prefetch, dc);
+      ric_bench_kernel<true, 16><<<1, 16, 0, stream>>>(ds, dd, dv, dp, steps, prefetch, dc);
+    else if (prefetch == 3)  // 32-lane team (diagnostic)
+      ric_bench_kernel<true, 32><<<1, 32, 0, stream>>>(ds, dd, dv, dp, steps, prefetch, dc);
     else
-      ric_bench_kernel<false><<<1, 16, 0, stream>>>(ds, dd, dv, dp, steps, prefetch, dc);
+      ric_bench_kernel<false, 16><<<1, 16, 0, stream>>>(ds, dd, dv, dp, steps, prefetch, dc);
   }
   unsigned long long hc[7];
   cudaMemcpyAsync(hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, stream);
   cudaStreamSynchronize(stream);
   cudaFree(ds), cudaFree(dd), cudaFree(dv), cudaFree(dp), cudaFree(dc);
-  if (stages)
+  if (stages && prefetch >= 2)
     for (int q = 0; q < 5; ++q) stages[q] = static_cast<double>(hc[2 + q]) / steps;
   return static_cast<double>(hc[0]) / steps;
 }
