@@ -42,7 +42,9 @@ __global__ void __launch_bounds__(THREADS, MINB) solve_cta_kernel(const Topo* __
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   red.part = reinterpret_cast<double*>(dyn_smem);
   __syncthreads();
-  Solver<NX, NU, CtaGroupT<THREADS>, SEQ> s(CtaGroupT<THREADS>{&red}, ctx.topo, ctx.mp, ctx.work, opts);
+  // One warp per segment team when the block is wide enough (>= 4 teams).
+  constexpr int kTeam = (THREADS >= 128 && team_size<NX, NU>() == 16) ? 32 : 0;
+  Solver<NX, NU, CtaGroupT<THREADS>, SEQ, kTeam> s(CtaGroupT<THREADS>{&red}, ctx.topo, ctx.mp, ctx.work, opts);
   s.tsm = dyn_smem + red_smem_bytes(THREADS);
   s.wbuf = reinterpret_cast<double*>(s.tsm);
   s.wcap = THREADS;

@@ -176,7 +176,9 @@ __device__ __forceinline__ void red_acc(const G& g, int k, double v, bool is_sum
 // kSeqOnly: every segment takes the team Riccati sweep / walk; the scan path
 // (and its register footprint) is compiled out — used for batches of trees
 // whose segments are all short (e.g. cfg0/cfg4).
-template <int NX, int NU, class G, bool kSeqOnly = false>
+// kTeam > 0 overrides the team width (32 = one warp per segment, for blocks
+// of >= 128 threads where the shorter per-step stages pay).
+template <int NX, int NU, class G, bool kSeqOnly = false, int kTeam = 0>
 struct Solver {
   using SL = StageLayout<NX, NU>;
   using BL = BwdLayout<NX>;
@@ -391,7 +393,7 @@ struct Solver {
   // Backward suffix scan of segments at depth d, elements already in level 0
   // (reversed). f(a, b) = combine_bwd(first = b, second = a).
   // Team size of the cooperative combine (0: one thread per combination).
-  static constexpr int kTS = team_size<NX, NU>();
+  static constexpr int kTS = kTeam > 0 ? kTeam : team_size<NX, NU>();
 
   // Items of a per-segment phase, one kTS-lane team per item.
   template <class F>
