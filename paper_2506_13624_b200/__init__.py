@@ -541,7 +541,7 @@ def batch_phase_profile(batch: "Batch", instance: int = 0) -> dict:
     res = {name: out[i] * 1e-6 for i, name in enumerate(PHASES)}
     if out[13] > 0:  # diagnostic counters, not times
         res["sweep_cycles_per_step"] = out[12] / out[13]
-    res["walk_cycles"] = (out[14], out[15], out[11], out[18])  # head_dx, chunk loop, depth walks, walks ns
+    res["walk_cycles"] = (out[14], out[15], out[11], out[18], out[19], out[20])  # head_dx, chunks, depths, ns, elements, chain
     res["sm_mhz"] = 1e3 * out[16] / out[17] if out[17] > 0 else 0.0  # effective SM clock of the solve
     return res
 

@@ -189,7 +189,10 @@ struct Solver {
   G g;
   const Topo& t;
   const ModelParams& mp;
-  Work& w;
+  // By value: the pointers become registers / private stack slots, so a
+  // generic store can no longer force reloading them from the block's
+  // shared-memory copy (which it might alias) before every access.
+  const Work w;
   const DevOptions& o;
   double g_rho{0.0};  // current AL penalty (uniform across the group)
   double* wbuf{nullptr};  // forward-walk elements (aliases tsm; wcap elements of kWE doubles)
@@ -983,24 +986,39 @@ struct Solver {
       }
       for (int c0 = 0; c0 < T; c0 += C) {
         const int cn = min(C, T - c0);
+        long long tq0 = 0;
+        if (w.prof && lr == 0) tq0 = clock64();
         for (int q = lr; q < ng * cn; q += ls) {
           const int r = q / cn, kk = q - r * cn;
           const SegIdx qs = seg_idx(sb + b + (j0 + r) * nb);
           walk_element(node_at(qs, c0 + kk), node_at(qs, c0 + kk + 1), wbuf + (r * C + kk) * kWE);
         }
         __syncthreads();
+        if (w.prof && lr == 0) {
+          const long long now = clock64();
+          g.sm->prof[19] += static_cast<double>(now - tq0);
+          tq0 = now;
+        }
         if (walker) {
-          const double* e = wbuf + lr * C * kWE;
+          // The chain touches shared memory only: dx_{k+1} replaces the
+          // consumed element's B k slot, copied out block-wide below.
+          double* e = wbuf + lr * C * kWE;
           for (int kk = 0; kk < cn; ++kk, e += kWE) {
-            const int nxt = node_at(sq, c0 + kk + 1);
             double t1[NX];
             mv<NX, NX>(e, dx, t1);
 #pragma unroll
             for (int j = 0; j < NX; ++j) {
               dx[j] = (t1[j] + e[NX * NX + j]) + e[NX * NX + NX + j];
-              w.dx[nxt * NX + j] = dx[j];
+              e[NX * NX + j] = dx[j];
             }
           }
+        }
+        if (w.prof && lr == 0) g.sm->prof[20] += static_cast<double>(clock64() - tq0);
+        __syncthreads();
+        for (int q = lr; q < ng * cn * NX; q += ls) {
+          const int r = q / (cn * NX), rem = q - r * cn * NX, kk = rem / NX, j = rem - kk * NX;
+          const SegIdx qs = seg_idx(sb + b + (j0 + r) * nb);
+          w.dx[node_at(qs, c0 + kk + 1) * NX + j] = wbuf[(r * C + kk) * kWE + NX * NX + j];
         }
         __syncthreads();
       }
