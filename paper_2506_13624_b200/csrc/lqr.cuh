@@ -830,7 +830,7 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
       kcol(qj, Kj);
       if (pol_g && i == 0) {  // lanes of column 0 of P hold K(:, j): the policy write
 #pragma unroll
-        for (int t = 0; t < NU; ++t) pol_g[PolicyLayout<NX, NU>::K + t + j * NU] = Kj[t];
+        for (int t = 0; t < NU; ++t) __stcg(pol_g + PolicyLayout<NX, NU>::K + t + j * NU, Kj[t]);
       }
       a = Fm[F::Qxx + q];
       b = Fm[F::Qxx + j + i * NX];
@@ -852,7 +852,7 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
       kcol(qu, kk);
       if (pol_g && i == 0) {
 #pragma unroll
-        for (int t = 0; t < NU; ++t) pol_g[PolicyLayout<NX, NU>::k + t] = kk[t];
+        for (int t = 0; t < NU; ++t) __stcg(pol_g + PolicyLayout<NX, NU>::k + t, kk[t]);
       }
       a = Fm[F::qx + i];
 #pragma unroll
@@ -873,7 +873,9 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
   for (int r = 0; r < R4; ++r) {
     Fm[oo4[r]] = o4[r];
     Fm[ot4[r]] = o4[r];
-    if (V_g && g4[r] >= 0) V_g[g4[r]] = o4[r];
+    // Explicit global-space stores: a generic store would order the next
+    // step's shared-memory loads behind it.
+    if (V_g && g4[r] >= 0) __stcg(V_g + g4[r], o4[r]);
   }
   const unsigned bad = __ballot_sync(mask, !pos);
   stamp(5);
