@@ -243,7 +243,7 @@ def main():
     for _ in range(e2e_steps):
         h2d = batch.set_models()
         batch.solve()
-        _, d2h = batch.results(xh, uh, want_reports=True)
+        _, d2h = batch.results(xh, uh, want_reports=True, as_array=True)
     e2e_el = time.perf_counter() - t0
     te = torch.tensor([e2e_el], dtype=torch.float64, device="cuda")
     if world > 1:

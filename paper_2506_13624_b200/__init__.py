@@ -456,11 +456,19 @@ class Batch:
         opts = (options or SolverOptions())._c()
         _check(lib().bmpc_batch_solve(self._h, C.byref(opts)))
 
-    def results(self, x: Optional[np.ndarray] = None, u: Optional[np.ndarray] = None, want_reports=True):
+    def results(self, x: Optional[np.ndarray] = None, u: Optional[np.ndarray] = None, want_reports=True,
+                as_array=False):
+        """Trajectories into x [count, n, nx] / u [count, n, nu] and the reports:
+        SolveReport objects, or with as_array=True one zero-copy numpy structured
+        array of the C bmpc_report records (fields status, inner_iterations, ...)."""
         reps = (_Report * self.count)() if want_reports else None
         b = C.c_size_t()
         _check(lib().bmpc_batch_results(self._h, _ptr(x), _ptr(u), reps, C.byref(b)))
-        return ([_report(r) for r in reps] if want_reports else None), b.value
+        if not want_reports:
+            return None, b.value
+        if as_array:
+            return np.ctypeslib.as_array(reps), b.value
+        return [_report(r) for r in reps], b.value
 
     def pack_results(self, d_dst_ptr: int) -> int:
         """Pack [x | u] of every instance into a device buffer (e.g. a torch

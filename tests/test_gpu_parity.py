@@ -341,6 +341,20 @@ def test_probe_schedule_is_bit_identical():
                 np.testing.assert_array_equal(ra[k], rb[k])
 
 
+def test_results_as_array_matches_reports(ctx):
+    probs = [B.build_intersection_case(B.intersection_spec(20, 4.0, 0.4), 2, 2, perturb_seed=s) for s in range(6)]
+    bt = B.Batch(ctx, probs)
+    bt.set_models()
+    bt.solve()
+    reps, _ = bt.results()
+    arr, _ = bt.results(as_array=True)
+    assert len(arr) == len(reps)
+    for r, a in zip(reps, arr):
+        assert (r.status, r.inner_iterations, r.outer_iterations, r.n_records) == \
+            (a["status"], a["inner_iterations"], a["outer_iterations"], a["n_records"])
+        assert r.final_cost == a["final_cost"] and r.alpha_evals == a["alpha_evals"]
+
+
 def test_native_library_loaded(ctx):
     """The CUDA path is the one that ran: the in-tree .so is mapped and
     launched kernels."""
