@@ -196,6 +196,12 @@ void bmpc_batch_destroy(bmpc_batch* batch);
  * ctx stream. Returns the bytes copied in *h2d_bytes (may be NULL). */
 int bmpc_batch_set_models(bmpc_batch* batch, const bmpc_model_desc* models, size_t* h2d_bytes);
 /* Device-to-device replication of instance 0's data into all instances. */
+/* Per-call measured states only: x0 [count][state_dim] (host) is uploaded
+ * over the node data already resident from bmpc_batch_set_models /
+ * bmpc_batch_replicate — the receding-horizon case where the scenario
+ * (references, predictions) is fixed and each call brings new initial states.
+ * h2d_bytes (optional) receives the bytes copied. */
+int bmpc_batch_set_initial_states(bmpc_batch* batch, const double* x0, size_t* h2d_bytes);
 int bmpc_batch_replicate(bmpc_batch* batch);
 /* Per-instance thread-block shape: `threads` per block with at least
  * `min_blocks` resident per SM (compiled variants only). */

@@ -470,6 +470,14 @@ class Batch:
             return np.ctypeslib.as_array(reps), b.value
         return [_report(r) for r in reps], b.value
 
+    def set_initial_states(self, x0: np.ndarray) -> int:
+        """Upload new initial states [count, nx] over the resident scenario data
+        (bmpc_batch_set_initial_states); returns H2D bytes."""
+        x0 = np.ascontiguousarray(x0, dtype=np.float64).reshape(self.count, self.nx)
+        b = C.c_size_t()
+        _check(lib().bmpc_batch_set_initial_states(self._h, _ptr(x0), C.byref(b)))
+        return b.value
+
     def pack_results(self, d_dst_ptr: int) -> int:
         """Pack [x | u] of every instance into a device buffer (e.g. a torch
         tensor's data_ptr()) for the NVLink gather; returns bytes."""

@@ -1067,6 +1067,25 @@ int bmpc_batch_set_models(bmpc_batch* b, const bmpc_model_desc* models, size_t* 
   }
 }
 
+int bmpc_batch_set_initial_states(bmpc_batch* b, const double* x0, size_t* h2d_bytes) {
+  try {
+    if (!b || !x0) return fail(BMPC_ERR_INVALID, "null argument");
+    ck(cudaSetDevice(b->ctx->device), "cudaSetDevice");
+    const size_t C = static_cast<size_t>(b->count);
+    const size_t nx = static_cast<size_t>(b->nx), x0s = align2(nx);
+    cudaStream_t s = b->ctx->stream;
+    ck(cudaStreamSynchronize(s), "staging reuse");
+    if (!b->h_stage) ck(cudaMallocHost(&b->h_stage, (C * b->node_data_doubles + C * x0s) * sizeof(double)), "pinned");
+    double* hx0 = b->h_stage + C * b->node_data_doubles;
+    for (size_t i = 0; i < C; ++i) std::memcpy(hx0 + i * x0s, x0 + i * nx, nx * sizeof(double));
+    ck(cudaMemcpyAsync(b->x0.p, hx0, C * x0s * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
+    if (h2d_bytes) *h2d_bytes = C * x0s * sizeof(double);
+    return BMPC_OK;
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
+}
+
 int bmpc_batch_replicate(bmpc_batch* b) {
   try {
     if (!b) return fail(BMPC_ERR_INVALID, "null argument");

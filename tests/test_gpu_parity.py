@@ -355,6 +355,26 @@ def test_results_as_array_matches_reports(ctx):
         assert r.final_cost == a["final_cost"] and r.alpha_evals == a["alpha_evals"]
 
 
+def test_set_initial_states_matches_full_upload(ctx):
+    """Receding-horizon call: the scenario stays resident, only x0 changes."""
+    spec = B.intersection_spec(20, 4.0, 0.4)
+    pert = [B.build_intersection_case(spec, 2, 2, perturb_seed=s) for s in range(5)]
+    base = [B.build_intersection_case(spec, 2, 2) for _ in range(5)]
+    outs = []
+    for probs, x0 in ((pert, None), (base, np.array([p.initial_state for p in pert]))):
+        bt = B.Batch(ctx, probs)
+        bt.set_models()
+        if x0 is not None:
+            assert bt.set_initial_states(x0) == 5 * 4 * 8
+        bt.solve()
+        x = np.zeros((5, bt.n, bt.nx))
+        arr, _ = bt.results(x, as_array=True)
+        outs.append((x, arr["inner_iterations"].copy(), arr["final_cost"].copy()))
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    np.testing.assert_array_equal(outs[0][2], outs[1][2])
+
+
 def test_native_library_loaded(ctx):
     """The CUDA path is the one that ran: the in-tree .so is mapped and
     launched kernels."""
