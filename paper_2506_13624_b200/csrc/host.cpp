@@ -1163,6 +1163,7 @@ static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_input
   d.zero_inputs = zero_inputs ? 1 : 0;
   d.seq_max_len = seq_max_for(b->ctx);
   d.ls_block = ls_block_for(b->ctx);
+  d.fwd_scan_min = std::getenv("BMPC_FWD_SCAN_MIN") ? std::atoi(std::getenv("BMPC_FWD_SCAN_MIN")) : 0;
   cudaError_t e;
   if (b->grid_mode) {
     e = launch_solve_grid(b->nx, b->nu, b->plan->d_topo.as<Topo>(), b->mps.as<ModelParams>(), b->works.as<Work>(), d,

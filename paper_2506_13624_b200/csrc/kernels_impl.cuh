@@ -79,6 +79,7 @@ __device__ void lqr_tree_body(G g, BlockCtx& ctx, double reg, double* scalars, i
   ModelParams dummy{};
   DevOptions o{};
   o.seq_max_len = seq_max;
+  o.fwd_scan_min = seq_max > 0 ? seq_max + 1 : 1;  // kernel-level API: forward mirrors the backward strategy
   o.keep_values = 1;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   Solver<NX, NU, G> s(g, ctx.topo, dummy, ctx.work, o);

@@ -233,6 +233,11 @@ struct Solver {
   __device__ double* val(int i) const { return w.value + static_cast<size_t>(i) * VL::stride; }
   // Segments of at most seq_max_len nodes take the team Riccati sweep.
   __device__ bool seq_len(int L) const { return kSeqOnly || (kTS > 0 && L <= o.seq_max_len); }
+  // Forward strategy, independent of the backward one: the closed-loop walk
+  // (O(L) dependent steps of ~100 cycles out of shared memory) beats the
+  // prefix scan of affine maps (2 log L grid-synchronised levels) at every
+  // segment length measured; fwd_scan_min > 0 restores the scan from that length.
+  __device__ bool fwd_walk(int L) const { return kSeqOnly || o.fwd_scan_min <= 0 || L < o.fwd_scan_min; }
   // (P, p) of node i after the backward pass (either path); P at +0, p at +NX*NX.
   __device__ const double* value_ptr(int i) const {
     const int s = t.node_seg[i];
@@ -736,7 +741,7 @@ struct Solver {
   // (lqr_scan.hpp:177-187, all depths at once) then a per-node depth sweep;
   // short segments: a team walk dx_{k+1} = A dx + B du + d. Returns (a1, a2).
   __device__ void forward(double* a1_out, double* a2_out) {
-    auto scan_E = [&](int d) { return seq_len(t.depth_len[d]) ? 0 : t.depth_len[d] - 1; };
+    auto scan_E = [&](int d) { return fwd_walk(t.depth_len[d]) ? 0 : t.depth_len[d] - 1; };
     if constexpr (!kSeqOnly) {
     for_multi_depth_items([&](int d) { return scan_E(d); }, [&](int d, int s, int k) {
       const int i = seg_node(s, k), nxt = seg_node(s, k + 1);
@@ -785,7 +790,7 @@ struct Solver {
     // Depth sweep.
     for (int d = 0; d < t.ndepth; ++d) {
       const int L = t.depth_len[d];
-      if (seq_len(L)) {
+      if (fwd_walk(L)) {
         long long tf0 = 0, nf0 = 0;
         if (w.prof && threadIdx.x == 0) {
           tf0 = clock64();
@@ -846,7 +851,7 @@ struct Solver {
         a2 += 0.5 * dot<NX>(dxi, Qdx);
       } else {
         double* dui = w.du + i * NU;
-        if (seq_len(seg_len(t.node_seg[i]))) {  // walked segment: du = K dx + k
+        if (fwd_walk(seg_len(t.node_seg[i]))) {  // walked segment: du = K dx + k
           const double* po = pol(i);
           double du[NU];
           mv<NU, NX>(po + PL::K, dxi, du);
@@ -912,7 +917,7 @@ struct Solver {
       return;
     }
     double* dui = w.du + i * NU;
-    if (seq_len(seg_len(t.node_seg[i]))) {  // walked segment: du = K dx + k
+    if (fwd_walk(seg_len(t.node_seg[i]))) {  // walked segment: du = K dx + k
       const double* po = pol(i);
       double du[NU];
       mv<NU, NX>(po + PL::K, dxi, du);
