@@ -157,7 +157,7 @@ int bmpc_ctx_set_stream(bmpc_ctx* ctx, void* cuda_stream); /* cudaStream_t; NULL
 int bmpc_ctx_synchronize(bmpc_ctx* ctx);
 /* Backward/forward strategy per tree segment: segments of at most `len`
  * nodes use the team-cooperative sequential Riccati sweep, longer ones the
- * associative scan (0 = scan everywhere; default 64, env BMPC_SEQ_MAX). */
+ * associative scan (0 = scan everywhere; default 384, env BMPC_SEQ_MAX). */
 int bmpc_ctx_set_seq_max_len(bmpc_ctx* ctx, int len);
 /* Line search (solver.hpp:459-518) in rounds of `alphas` step sizes: a round
  * evaluates its alphas for every node and stops at the first accepted one, so

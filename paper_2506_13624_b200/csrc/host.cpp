@@ -641,7 +641,7 @@ struct bmpc_ctx {
 static int seq_max_for(const bmpc_ctx* c) {
   if (c && c->seq_max_len >= 0) return c->seq_max_len;
   if (const char* env = std::getenv("BMPC_SEQ_MAX")) return std::atoi(env);
-  return 64;
+  return 384;
 }
 
 // Step sizes evaluated per line-search round. The accepted alpha is the first

@@ -33,20 +33,9 @@ for name, p in cases:
     bt = B.Batch(ctx, [p])
     bt.set_models()
     line = []
-    for sm in (0, 64, 128, 256, 512, 1024):
+    for sm in (0, 64, 256, 384, 512, 768, 1024):
         B.set_seq_max_len(ctx, sm)
         ms = timed(bt)
         r, _ = bt.results()
         line.append("seq<=%d: %.2fms (%d it)" % (sm, ms, r[0].inner_iterations))
     print(name, p.tree.node_count, " | ".join(line), flush=True)
-cnt = 4096
-probs = [B.build_intersection_case(B.intersection_spec(63, 10.0, 0.1), 2, 2, perturb_seed=42 + i) for i in range(cnt)]
-bt = B.Batch(ctx, probs)
-bt.set_models()
-for sm in (0, 256):
-    B.set_seq_max_len(ctx, sm)
-    for shape in [(256, 1), (256, 2), (128, 4), (64, 8), (128, 8)]:
-        bt.set_launch(*shape)
-        ms = timed(bt)
-        print("batch seq<=%d" % sm, shape, bt.info()["regs_per_thread"], "%.1f ms %.0f solves/s" % (ms, cnt / ms * 1e3),
-              flush=True)
