@@ -430,7 +430,7 @@ struct DevBuf {
 struct Plan {
   int n{0}, ndepth{0}, nseg{0}, scratch{0}, max_con{0};
   bool has_constraints{false};
-  std::vector<int> depth_begin, depth_len, seg_off, seg_nodes, seg_scratch, seg_stride, node_seg, node_pos;
+  std::vector<int> depth_begin, depth_len, seg_off, seg_nodes, seg_scratch, seg_stride, node_seg, node_pos, seg_depth;
   DevBuf d_ints, d_weight, d_topo;
   Topo topo{};
 };
@@ -501,6 +501,7 @@ std::unique_ptr<Plan> make_plan(const bmpc_tree& t, int max_con, bool has_constr
     for (int k = 1; k < L && stride; ++k)
       if (sg.nodes[static_cast<size_t>(k)] - sg.nodes[static_cast<size_t>(k) - 1] != stride) stride = 0;
     pl->seg_stride.push_back(stride);
+    pl->seg_depth.push_back(sg.depth);
     // Scan levels n_0 = L, n_{l+1} = ceil(n_l/2): total <= 2L + (#levels).
     scratch += 2 * L + 32;
   }
@@ -525,6 +526,7 @@ std::unique_ptr<Plan> make_plan(const bmpc_tree& t, int max_con, bool has_constr
   const size_t o_st = put(pl->seg_stride.data(), pl->seg_stride.size());
   const size_t o_ns = put(pl->node_seg.data(), pl->node_seg.size());
   const size_t o_np = put(pl->node_pos.data(), pl->node_pos.size());
+  const size_t o_sd = put(pl->seg_depth.data(), pl->seg_depth.size());
   pl->d_ints = DevBuf(ints.size() * sizeof(int));
   ck(cudaMemcpyAsync(pl->d_ints.p, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice, s), "plan");
   pl->d_weight = DevBuf(static_cast<size_t>(n) * sizeof(double));
@@ -546,6 +548,7 @@ std::unique_ptr<Plan> make_plan(const bmpc_tree& t, int max_con, bool has_constr
   tp.seg_stride = base + o_st;
   tp.node_seg = base + o_ns;
   tp.node_pos = base + o_np;
+  tp.seg_depth = base + o_sd;
   tp.has_constraints = has_constraints ? 1 : 0;
   tp.max_con = std::max(max_con, 1);
   pl->d_topo = DevBuf(sizeof(Topo));
@@ -1147,10 +1150,20 @@ static int batch_set_inputs(bmpc_batch* b, const double* initial_inputs) {
 }
 
 // Every segment short enough for the team sweep: launch the sweep-only kernel.
+// Sweep or scan per depth level (Solver::seq_depth): short segments, or many
+// long ones at one depth (the scan's work grows with them; tools/exp_seq.py).
+constexpr int kSeqWideSegs = 64, kSeqWideMax = 1024;
+static bool seq_depth_host(const Plan& pl, int d, int seq_max) {
+  const int L = pl.depth_len[static_cast<size_t>(d)];
+  const int ns = pl.depth_begin[static_cast<size_t>(d) + 1] - pl.depth_begin[static_cast<size_t>(d)];
+  return seq_max > 0 && (L <= seq_max || (ns >= kSeqWideSegs && L <= kSeqWideMax));
+}
+
+// Every depth takes the team sweep: launch the sweep-only kernel.
 static bool seq_only(const bmpc_batch* b, int seq_max) {
-  int longest = 0;
-  for (int L : b->plan->depth_len) longest = std::max(longest, L);
-  return seq_max > 0 && longest <= seq_max;
+  for (int d = 0; d < b->plan->ndepth; ++d)
+    if (!seq_depth_host(*b->plan, d, seq_max)) return false;
+  return true;
 }
 
 static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_inputs) {
@@ -1162,6 +1175,8 @@ static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_input
   DevOptions d = to_dev(o);
   d.zero_inputs = zero_inputs ? 1 : 0;
   d.seq_max_len = seq_max_for(b->ctx);
+  d.seq_wide_segs = kSeqWideSegs;
+  d.seq_wide_max = kSeqWideMax;
   d.ls_block = ls_block_for(b->ctx);
   d.fwd_scan_min = std::getenv("BMPC_FWD_SCAN_MIN") ? std::atoi(std::getenv("BMPC_FWD_SCAN_MIN")) : 0;
   cudaError_t e;

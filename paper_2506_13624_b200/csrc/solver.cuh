@@ -232,7 +232,16 @@ struct Solver {
   }
   __device__ double* val(int i) const { return w.value + static_cast<size_t>(i) * VL::stride; }
   // Segments of at most seq_max_len nodes take the team Riccati sweep.
-  __device__ bool seq_len(int L) const { return kSeqOnly || (kTS > 0 && L <= o.seq_max_len); }
+  // Backward strategy per depth level: team sweep for short segments, or for
+  // many long ones at one depth; the associative scan otherwise (host mirror:
+  // seq_depth_host).
+  __device__ bool seq_depth(int d) const {
+    if (kSeqOnly) return true;
+    if (kTS <= 0 || o.seq_max_len <= 0) return false;
+    const int L = t.depth_len[d], ns = t.depth_begin[d + 1] - t.depth_begin[d];
+    return L <= o.seq_max_len || (o.seq_wide_segs > 0 && ns >= o.seq_wide_segs && L <= o.seq_wide_max);
+  }
+  __device__ bool seq_seg(int s) const { return kSeqOnly || seq_depth(t.seg_depth[s]); }
   // Forward strategy, independent of the backward one: the closed-loop walk
   // (O(L) dependent steps of ~100 cycles out of shared memory) beats the
   // prefix scan of affine maps (2 log L grid-synchronised levels) at every
@@ -241,7 +250,7 @@ struct Solver {
   // (P, p) of node i after the backward pass (either path); P at +0, p at +NX*NX.
   __device__ const double* value_ptr(int i) const {
     const int s = t.node_seg[i];
-    return seq_len(seg_len(s)) ? val(i) : value_of(i);
+    return seq_seg(s) ? val(i) : value_of(i);
   }
 
   // ------------------------------------------------------ nonlinear rollout
@@ -632,7 +641,7 @@ struct Solver {
     int err = kBwdOk;
     for (int d = t.ndepth - 1; d >= 0; --d) {
       const int L = t.depth_len[d];
-      if (seq_len(L)) {
+      if (seq_depth(d)) {
         const int e = riccati_sweep_depth(d, reg);
         err = err ? err : e;
         mark(2);
@@ -695,7 +704,7 @@ struct Solver {
       if (is_leaf(i)) continue;
       const int s = t.node_seg[i], k = t.node_pos[i];
       if constexpr (!kSeqOnly) {
-        if (!seq_len(seg_len(s)) && k + 1 < seg_len(s)) {
+        if (!seq_seg(s) && k + 1 < seg_len(s)) {
           const int nxt = seg_node(s, k + 1);
           const double* v = value_of(nxt);
           const int e = feedback<NX, NU>(stage(i), reg, w.defect + nxt * NX, v + BL::P, v + BL::p,
@@ -1414,7 +1423,7 @@ struct Solver {
     const int err = backward(reg, &max_ff);
     if (w.value) {
       for (int i = g.rank(); i < t.n; i += g.size()) {
-        if (!seq_len(seg_len(t.node_seg[i]))) {
+        if (!seq_seg(t.node_seg[i])) {
           const double* v = value_of(i);
           copy<NX * NX>(v + BL::P, w.value + static_cast<size_t>(i) * VL::stride + VL::P);
           copy<NX>(v + BL::p, w.value + static_cast<size_t>(i) * VL::stride + VL::p);

@@ -36,6 +36,7 @@ struct DevOptions {  // SolverOptions (solver.hpp:28-58), device copy
   double reg_init, reg_min, reg_growth, reg_decay, reg_max;
   int zero_inputs;  // 1: initial inputs are zero (solver.hpp:604-609), skip the H2D
   int seq_max_len;  // segments of <= this many nodes use the team Riccati sweep, longer ones the scan
+  int seq_wide_segs, seq_wide_max;  // ... and depths with >= seq_wide_segs segments of <= seq_wide_max
   int ls_block;     // step sizes evaluated per line-search round (<= 0: all alpha_levels at once)
   int pass_budget;  // > 0: suspend a solve after this many inner passes in this launch (Work::resume)
   const int* order; // optional block -> instance map of a batch launch (nullptr: identity)
@@ -95,6 +96,7 @@ struct Topo {
   const int* seg_scratch;    // [nseg] first scratch slot (2*len + 32 slots reserved)
   const int* node_seg;       // [n]
   const int* node_pos;       // [n]
+  const int* seg_depth;      // [nseg] depth level of each segment
   int has_constraints;
   int max_con;               // constraint rows stored per node (eta stride)
 };
