@@ -1,0 +1,140 @@
+// adapter_check — test infrastructure: the C++ drop-in (include/bmpc_b200.hpp)
+// against the UNMODIFIED reference solve() on the same BmpcProblem objects,
+// built by the reference's own builders (compiled here against the Eigen shim,
+// see Makefile). Mirrors the call sites the drop-in replaces:
+// tests/acceptance_test.cpp:93-102 (cfg0), tests/test_solver.cpp:414-551
+// (solver fixtures, latency case, initial inputs), README.md:134-145 (usage),
+// and testing::random_lq_problem (oracles.hpp:316) for the LQ family.
+//
+// Prints one JSON object per case and exits 1 on any parity failure.
+// Parity bar (north star): identical status / inner / outer iteration counts
+// and per-iteration alpha + acceptance sequences; trajectories and final cost
+// within 1e-8 relative.
+#include <bmpc/bmpc.hpp>
+#include <bmpc/testing/oracles.hpp>
+
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <stdexcept>
+#include <string>
+
+#include "bmpc_b200.hpp"
+
+namespace {
+
+constexpr double kTol = 1e-8;
+int failures = 0;
+
+double traj_rel_err(const bmpc::TrajectoryTree& a, const bmpc::TrajectoryTree& b) {
+  double num = 0.0, den = 0.0;
+  for (size_t i = 0; i < b.state.size(); ++i) {
+    num += (a.state[i] - b.state[i]).squaredNorm();
+    den += b.state[i].squaredNorm();
+    if (b.input[i].size()) {
+      num += (a.input[i] - b.input[i]).squaredNorm();
+      den += b.input[i].squaredNorm();
+    }
+  }
+  return std::sqrt(num) / std::max(std::sqrt(den), 1e-12);
+}
+
+void compare(const std::string& name, const bmpc::SolveResult& got, const bmpc::SolveResult& want) {
+  const auto& g = got.report;
+  const auto& w = want.report;
+  bool same_seq = g.iterations.size() == w.iterations.size();
+  for (size_t k = 0; same_seq && k < w.iterations.size(); ++k)
+    same_seq = g.iterations[k].alpha == w.iterations[k].alpha &&
+               g.iterations[k].accepted == w.iterations[k].accepted && g.iterations[k].outer == w.iterations[k].outer;
+  const double traj = traj_rel_err(got.trajectory, want.trajectory);
+  const double cost = std::abs(g.final_cost - w.final_cost) / std::max(1.0, std::abs(w.final_cost));
+  const bool ok = g.status == w.status && g.inner_iterations == w.inner_iterations &&
+                  g.outer_iterations == w.outer_iterations && same_seq && traj <= kTol && cost <= kTol;
+  if (!ok) ++failures;
+  std::printf(
+      "{\"case\": \"%s\", \"ok\": %s, \"status\": [\"%s\", \"%s\"], \"inner\": [%d, %d], \"outer\": [%d, %d], "
+      "\"records\": [%zu, %zu], \"same_alpha_sequence\": %s, \"traj_rel_err\": %.3e, \"cost_rel_err\": %.3e, "
+      "\"gpu_total_s\": %.6f}\n",
+      name.c_str(), ok ? "true" : "false", bmpc::to_string(g.status), bmpc::to_string(w.status), g.inner_iterations,
+      w.inner_iterations, g.outer_iterations, w.outer_iterations, g.iterations.size(), w.iterations.size(),
+      same_seq ? "true" : "false", traj, cost, g.times.total_s);
+}
+
+void scenario_case(const std::string& name, const bmpc::ScenarioSpec& spec, bool latency, int v1, int v2,
+                   const std::vector<bmpc::VectorXd>* u0 = nullptr) {
+  bmpc::ScenarioArtifacts art;
+  const bmpc::BmpcProblem problem =
+      latency ? bmpc::build_latency_case(spec, &art) : bmpc::build_intersection_case(spec, v1, v2, &art);
+  const bmpc::SolveResult want = bmpc::solve(problem, {}, u0);
+  const bmpc::SolveResult got = bmpc::b200::solve(problem, spec, art, {}, u0);  // was bmpc::solve(problem)
+  compare(name, got, want);
+}
+
+void lq_case(const std::string& name, int horizon, const std::vector<bmpc::TreeBranching>& br, int nx, int nu,
+             uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  const bmpc::TreeTopology tree = bmpc::build_tree(horizon, br);
+  const bmpc::BmpcProblem problem = bmpc::testing::random_lq_problem(rng, tree, nx, nu);
+  compare(name, bmpc::b200::solve_affine_quadratic(problem), bmpc::solve(problem));
+}
+
+template <class E, class F>
+void expect_throw(const std::string& name, F&& f) {
+  bool thrown = false;
+  try {
+    f();
+  } catch (const E&) {
+    thrown = true;
+  }
+  if (!thrown) ++failures;
+  std::printf("{\"case\": \"%s\", \"ok\": %s}\n", name.c_str(), thrown ? "true" : "false");
+}
+
+}  // namespace
+
+int main() {
+  using bmpc::intersection_spec;
+  using bmpc::latency_spec;
+  // cfg0: the acceptance problem (acceptance_test.cpp:93-94).
+  scenario_case("cfg0 intersection_spec(63,10,0.1) 2x2", intersection_spec(63, 10.0, 0.1), false, 2, 2);
+  // Solver fixtures (test_solver.cpp:414, 474, 525, 537, 544).
+  scenario_case("intersection_spec(20,4,0.4) 2x2", intersection_spec(20, 4.0, 0.4), false, 2, 2);
+  scenario_case("intersection_spec(25,5,0.4) 1x2", intersection_spec(25, 5.0, 0.4), false, 1, 2);
+  scenario_case("intersection_spec(25,5,0.4) 2x2", intersection_spec(25, 5.0, 0.4), false, 2, 2);
+  scenario_case("latency_spec(0.5,63,5,0.05)", latency_spec(0.5, 63, 5.0, 0.05), true, 0, 0);
+  scenario_case("latency_spec(1.5,63,5,0.05)", latency_spec(1.5, 63, 5.0, 0.05), true, 0, 0);
+  // cfg1 points (long horizon, one-block and whole-GPU paths).
+  scenario_case("cfg1 intersection_spec(255,10,0.1) 2x2", intersection_spec(255, 10.0, 0.1), false, 2, 2);
+  scenario_case("cfg1 intersection_spec(500,10,0.1) 2x2", intersection_spec(500, 10.0, 0.1), false, 2, 2);
+  // initial_inputs (solver.hpp:604-608).
+  {
+    const bmpc::ScenarioSpec spec = intersection_spec(63, 10.0, 0.1);
+    const bmpc::TreeTopology tree = bmpc::build_intersection_case(spec, 2, 2).tree;
+    std::vector<bmpc::VectorXd> u0(static_cast<size_t>(tree.node_count));
+    for (int i = 0; i < tree.node_count; ++i)
+      u0[static_cast<size_t>(i)] = tree.is_leaf(i) ? bmpc::VectorXd() : bmpc::VectorXd::Constant(2, 0.05 * (i % 3));
+    scenario_case("cfg0 with initial_inputs", spec, false, 2, 2, &u0);
+  }
+  // Affine-quadratic family (random_lq_problem): one Newton step converges.
+  lq_case("lq (4,2) N=30 2x2", 30, {{5, 2, {0.5, 0.5}}, {12, 2, {0.3, 0.7}}}, 4, 2, 7);
+  lq_case("lq (3,2) N=64 3-ary", 64, {{10, 3, {0.2, 0.3, 0.5}}}, 3, 2, 11);
+  lq_case("lq (2,1) N=100 path", 100, {}, 2, 1, 13);
+  // Error behaviour.
+  expect_throw<std::invalid_argument>("nonlinear_rollout rejected", [] {
+    const bmpc::ScenarioSpec spec = intersection_spec(20, 4.0, 0.4);
+    bmpc::ScenarioArtifacts art;
+    const bmpc::BmpcProblem p = bmpc::build_intersection_case(spec, 2, 2, &art);
+    bmpc::SolverOptions o;
+    o.forward = bmpc::ForwardMode::nonlinear_rollout;
+    bmpc::b200::solve(p, spec, art, o);
+  });
+  expect_throw<std::invalid_argument>("mismatched artifacts rejected", [] {
+    const bmpc::ScenarioSpec spec = intersection_spec(20, 4.0, 0.4);
+    bmpc::ScenarioArtifacts art;
+    const bmpc::BmpcProblem p = bmpc::build_intersection_case(spec, 2, 2, &art);
+    art.reference.pop_back();
+    bmpc::b200::solve(p, spec, art);
+  });
+  std::printf("{\"failures\": %d}\n", failures);
+  return failures ? 1 : 0;
+}
