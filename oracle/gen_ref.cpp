@@ -1,0 +1,36 @@
+// gen_ref — test infrastructure: the reference's `bench gen` document
+// (proj/tools/bench.cpp:327-357: scenario_spec_to_json +
+// scenario_artifacts_to_json, serialization.hpp:128-219) written by the
+// UNMODIFIED reference headers (compiled against the Eigen shim), compact.
+// tests/make_golden.py stores its output under tests/golden/ as the fixture
+// for `python -m paper_2506_13624_b200.cli gen`.
+#include <bmpc/bmpc.hpp>
+#include <bmpc/serialization.hpp>
+
+#include <iostream>
+#include <string>
+
+int main(int argc, char** argv) {
+  const std::string scenario = argc > 1 ? argv[1] : "intersection";
+  bmpc::json doc;
+  bmpc::ScenarioArtifacts artifacts;
+  if (scenario == "intersection") {
+    const bmpc::ScenarioSpec spec = bmpc::intersection_spec();
+    bmpc::build_intersection_case(spec, 2, 2, &artifacts);
+    doc["kind"] = "intersection";
+    doc["v1_count"] = 2;
+    doc["v2_count"] = 2;
+    doc["spec"] = bmpc::scenario_spec_to_json(spec);
+  } else if (scenario == "latency") {
+    const bmpc::ScenarioSpec spec = bmpc::latency_spec(0.5);
+    bmpc::build_latency_case(spec, &artifacts);
+    doc["kind"] = "latency";
+    doc["spec"] = bmpc::scenario_spec_to_json(spec);
+  } else {
+    std::cerr << "unknown scenario\n";
+    return 2;
+  }
+  doc["problem"] = bmpc::scenario_artifacts_to_json(artifacts);
+  std::cout << doc.dump() << "\n";
+  return 0;
+}

@@ -958,7 +958,10 @@ int bmpc_batch_create(bmpc_ctx* ctx, const bmpc_tree* tree, int count, const bmp
     b->resume = DevBuf(C * sizeof(DevResume));
     b->order = DevBuf(C * sizeof(int));
     // Grid mode for a single large tree: all SMs on one instance.
-    b->grid_mode = count == 1 && tree->node_count > 1024;
+    // Crossover: env BMPC_GRID_MIN_NODES (default 1024, tools/grid_crossover.py).
+    int grid_min = 1024;
+    if (const char* env = std::getenv("BMPC_GRID_MIN_NODES")) grid_min = std::atoi(env);
+    b->grid_mode = count == 1 && tree->node_count > grid_min;
     if (b->grid_mode) {
       b->grid_blocks = solve_grid_blocks(b->nx, b->nu, b->threads);
       if (b->grid_blocks < 1) return fail(BMPC_ERR_CUDA, "grid solve kernel cannot be made co-resident");

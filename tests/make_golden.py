@@ -80,6 +80,17 @@ def main():
                         leaf=leaf, dx0=dx0, meta=json.dumps(dict(horizon=6, branchings=br, nx=3, nu=2)),
                         **{k: np.asarray(v) for k, v in out.items()})
     print("lqr_tree_two_stage_nx3nu2: written")
+    # `bench gen` documents (bench.cpp:327-357) written by the reference's own
+    # serialization (oracle/_ref/gen_ref), fixtures for the CLI's gen command.
+    import gzip
+    import subprocess
+
+    for scen in ("intersection", "latency"):
+        doc = subprocess.run([os.path.join(os.path.dirname(HERE), "oracle", "_ref", "gen_ref"), scen],
+                             check=True, capture_output=True, text=True).stdout
+        with gzip.open(os.path.join(GOLDEN, "gen_%s.json.gz" % scen), "wt") as f:
+            f.write(doc)
+        print("gen_%s.json.gz: written" % scen)
 
 
 if __name__ == "__main__":
