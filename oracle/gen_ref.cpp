@@ -3,7 +3,8 @@
 // scenario_artifacts_to_json, serialization.hpp:128-219) written by the
 // UNMODIFIED reference headers (compiled against the Eigen shim), compact.
 // tests/make_golden.py stores its output under tests/golden/ as the fixture
-// for `python -m paper_2506_13624_b200.cli gen`.
+// for `python -m paper_2506_13624_b200.cli gen`; "report" / "tree" dump
+// report_to_json of the cfg0 solve and tree_spec_to_json (serialization tests).
 #include <bmpc/bmpc.hpp>
 #include <bmpc/serialization.hpp>
 
@@ -26,6 +27,15 @@ int main(int argc, char** argv) {
     bmpc::build_latency_case(spec, &artifacts);
     doc["kind"] = "latency";
     doc["spec"] = bmpc::scenario_spec_to_json(spec);
+  } else if (scenario == "report") {  // report_to_json of the cfg0 solve (acceptance_test.cpp:93-102)
+    const bmpc::BmpcProblem problem =
+        bmpc::build_intersection_case(bmpc::intersection_spec(63, 10.0, 0.1), 2, 2);
+    std::cout << bmpc::report_to_json(bmpc::solve(problem).report).dump() << "\n";
+    return 0;
+  } else if (scenario == "tree") {  // tree_spec_to_json (test_serialization.cpp:12)
+    const bmpc::TreeTopology tree = bmpc::build_tree(6, {{2, 2, {0.5, 0.5}}, {4, 3, {0.2, 0.3, 0.5}}});
+    std::cout << bmpc::tree_spec_to_json(tree).dump() << "\n";
+    return 0;
   } else {
     std::cerr << "unknown scenario\n";
     return 2;

@@ -136,6 +136,7 @@ class TreeTopology:
         self.child_count = np.ctypeslib.as_array(t.child_count, (n,)).copy()
         self.step_begin = np.ctypeslib.as_array(t.step_begin, (t.horizon + 2,)).copy()
         self.leaves = np.ctypeslib.as_array(t.leaves, (t.leaf_count,)).copy()
+        self.branchings = None  # set by build_tree; scenario trees recover it (serialization.tree_branchings)
 
     @property
     def children(self):
@@ -172,7 +173,10 @@ def build_tree(horizon: int, branchings: Sequence[tuple] = ()) -> TreeTopology:
     if rc == -1:
         raise ValueError(lib().bmpc_last_error().decode())
     _check(rc)
-    return TreeTopology(out)
+    t = TreeTopology(out)
+    t.branchings = [(int(b[0]), int(b[1]), [float(v) for v in (b[2] if len(b) > 2 else [1.0 / b[1]] * b[1])])
+                    for b in branchings]  # construction spec (TreeTopology::branchings, tree.hpp:43)
+    return t
 
 
 # ----------------------------------------------------------------- problems
@@ -318,11 +322,23 @@ class SolverOptions:
     reg_growth: float = 10.0
     reg_decay: float = 10.0
     reg_max: float = 1e10
+    # Strategy enums (solver.hpp:23-33, JSON spellings of serialization.hpp:40-61).
+    # The GPU runs the tree-scan backward pass with a linear rollout and the
+    # parallel line search; every backward strategy solves the same LQR
+    # subproblem, the other forward / line-search modes are other algorithms.
+    backward: str = "scan-tree-riccati"
+    forward: str = "linear"
+    line_search: str = "parallel"
+    scan_order: str = "tree"
+    parallel: bool = True
 
     def _c(self) -> _Options:
+        if self.forward != "linear" or self.line_search != "parallel":
+            raise ValueError("only forward='linear' with line_search='parallel' runs on the GPU path "
+                             "(got forward=%r, line_search=%r)" % (self.forward, self.line_search))
         o = _Options()
-        for f in dataclasses.fields(self):
-            setattr(o, f.name, getattr(self, f.name))
+        for name, _ in _Options._fields_:
+            setattr(o, name, getattr(self, name))
         return o
 
 

@@ -27,52 +27,19 @@ from typing import List, Optional
 
 import numpy as np
 
-from . import (SolverOptions, build_intersection_case, build_latency_case, build_tree, intersection_spec,
-               latency_spec, lq_problem, solve)
+from . import (build_intersection_case, build_latency_case, build_tree, intersection_spec, latency_spec, lq_problem,
+               solve)
+from .serialization import scenario_artifacts_to_json, scenario_spec_to_json, solver_options_from_json
 
 CSV_HEADER = ("experiment,solver,N,leaves,T_sh1,rep,iters,cost,violation,t_setup_ms,t_bp1_ms,"
               "t_bp2_ms,t_fwd_ms,t_ls_ms,t_total_ms,status")
 
-_OPT_FLOAT = ("armijo_beta", "merit_gamma", "merit_mu0", "merit_mu_init", "defect_epsilon", "tol_defect",
-              "tol_cost", "tol_feedforward", "tol_constraint", "penalty_init", "penalty_growth", "penalty_max",
-              "reg_init", "reg_min", "reg_growth", "reg_decay", "reg_max")
-_OPT_INT = ("max_inner_iterations", "max_outer_iterations", "alpha_levels")
-_STRATEGY = {"backward": ("scan-tree-riccati", "scan-condensed", "sequential-riccati"),
-             "forward": ("linear", "nonlinear"), "line_search": ("parallel", "sequential"),
-             "scan_order": ("tree", "sequential")}
 GPU_SOLVERS = ("pmsilqr", "hypmsilqr")
 ALL_SOLVERS = ("pmsilqr", "hypmsilqr", "smsilqr", "sssilqr")  # apply_solver_name, bench.cpp:59-85
 
 
 class ConfigError(ValueError):
     pass
-
-
-# ------------------------------------------------------------------ options
-def solver_options_from_json(j: dict) -> SolverOptions:
-    """solver_options_from_json (serialization.hpp:37-85): every key is
-    validated; unknown keys or strategy names raise."""
-    o = SolverOptions()
-    for key, value in j.items():
-        if key in _STRATEGY:
-            if value not in _STRATEGY[key]:
-                raise ConfigError("unknown %s: %s" % ({"backward": "backward strategy", "forward": "forward mode",
-                                                       "line_search": "line search mode",
-                                                       "scan_order": "scan order"}[key], value))
-        elif key == "parallel":
-            if not isinstance(value, bool):
-                raise ConfigError("option parallel must be a boolean")
-        elif key in _OPT_INT:
-            if isinstance(value, bool) or not isinstance(value, int):
-                raise ConfigError("option %s must be an integer" % key)
-            setattr(o, key, value)
-        elif key in _OPT_FLOAT:
-            if isinstance(value, bool) or not isinstance(value, (int, float)):
-                raise ConfigError("option %s must be a number" % key)
-            setattr(o, key, float(value))
-        else:
-            raise ConfigError("unknown solver option: " + key)
-    return o
 
 
 # ------------------------------------------------ random LQ (custom sweeps)
@@ -199,6 +166,16 @@ def report_consistent(rep) -> bool:
     return True
 
 
+def apply_solver_name(name: str, o) -> None:
+    """apply_solver_name (bench.cpp:59-85): the preset overrides the strategy
+    keys of the options."""
+    o.backward = {"pmsilqr": "scan-tree-riccati", "hypmsilqr": "scan-condensed"}.get(name, "sequential-riccati")
+    o.forward = "nonlinear" if name == "sssilqr" else "linear"
+    o.line_search = "parallel" if name in GPU_SOLVERS else "sequential"
+    if name not in GPU_SOLVERS:
+        o.parallel = False
+
+
 def parse_run_config(j: dict) -> dict:
     """parse_run_config (bench.cpp:44-57) with the reference's defaults."""
     cfg = {"experiment": "horizon-sweep", "solver": "pmsilqr", "horizons": [], "leaf_counts": [4],
@@ -207,7 +184,10 @@ def parse_run_config(j: dict) -> dict:
     for k in cfg:
         if k in j:
             cfg[k] = j[k]
-    cfg["options"] = solver_options_from_json(j.get("options", {}))
+    try:
+        cfg["options"] = solver_options_from_json(j.get("options", {}))
+    except ValueError as e:
+        raise ConfigError(str(e))
     return cfg
 
 
@@ -273,6 +253,7 @@ def run_command(config_path: str, out=sys.stdout, err=sys.stderr) -> int:
         print("bench run: solver '%s' (sequential line search / nonlinear rollout) is not on the GPU path"
               % cfg["solver"], file=err)
         return 2
+    apply_solver_name(cfg["solver"], cfg["options"])
     if cfg["repetitions"] < 1:
         print("bench run: repetitions must be >= 1", file=err)
         return 2
@@ -314,45 +295,6 @@ def run_command(config_path: str, out=sys.stdout, err=sys.stderr) -> int:
 
 
 # --------------------------------------------------------------------- gen
-_SPEC_DEFAULTS = {"state_weights": [1.0, 1.0, 0.1, 0.1], "input_weights": [0.5, 0.5],
-                  "terminal_weights": [1.0, 1.0, 0.1, 0.1], "accel_limit": 3.0, "yaw_rate_limit": 0.5,
-                  "safety_radius": 3.0, "prediction_tau": 1.5, "reference_turn_rate": 0.4,
-                  "backup_deceleration": 3.0, "continue_deceleration": 2.5}  # ScenarioSpec, scenarios.hpp:25-47
-
-
-def _spec_json(kind: str, spec) -> dict:
-    """scenario_spec_to_json (serialization.hpp:128-150) of intersection_spec()
-    / latency_spec(0.5) (scenarios.hpp:178-197, 300-317)."""
-    if kind == "intersection":
-        ego = [0.0, -20.0, math.pi / 2.0, 5.0]
-        veh = [{"position": [-3.5, 30.0], "heading": -math.pi / 2.0, "speed": 8.0,
-                "target_speeds": [8.0, 2.0, 5.0, 3.5]},
-               {"position": [0.0, -10.0], "heading": math.pi / 2.0, "speed": 5.0,
-                "target_speeds": [5.0, 1.0, 3.0, 2.0]}]
-    else:
-        ego = [0.0, 0.0, 0.0, 10.0]
-        veh = [{"position": [30.0, 0.0], "heading": 0.0, "speed": 8.0, "target_speeds": [8.0, 0.0]}]
-    d = dict(_SPEC_DEFAULTS)
-    d.update({"total_time": spec.total_time, "shared_times": list(spec.shared_times), "horizon": spec.horizon,
-              "ego_start": ego, "vehicles": veh})
-    return d
-
-
-def _tree_json(tree) -> dict:
-    """tree_spec_to_json (serialization.hpp:16-22): the branchings, recovered
-    from the built topology (arity and per-child weight ratio at each step
-    whose nodes branch)."""
-    br = []
-    for k in range(tree.horizon):
-        a, b = tree.step_begin[k], tree.step_begin[k + 1]
-        if tree.child_count[a] > 1:
-            f = tree.first_child[a]
-            ar = int(tree.child_count[a])
-            br.append({"arity": ar, "step": k,
-                       "weights": [float(tree.weight[f + c] / tree.weight[a]) for c in range(ar)]})
-    return {"branchings": br, "horizon": int(tree.horizon)}
-
-
 def gen_command(scenario: str, out_path: str, out=sys.stdout, err=sys.stderr) -> int:
     """gen_command (bench.cpp:327-357) with scenario_artifacts_to_json
     (serialization.hpp:200-219)."""
@@ -367,12 +309,8 @@ def gen_command(scenario: str, out_path: str, out=sys.stdout, err=sys.stderr) ->
     else:
         print("bench gen: unknown scenario '%s'" % scenario, file=err)
         return 2
-    doc["spec"] = _spec_json(scenario, spec)
-    a, t = p.arrays(), p.tree
-    nodes = [{"parent": int(t.parent[i]), "reference": [float(v) for v in a["reference"][i]],
-              "step": int(t.time_step[i]), "vehicles": [[float(v) for v in xy] for xy in a["vehicles"][i]],
-              "weight": float(t.weight[i])} for i in range(t.node_count)]
-    doc["problem"] = {"nodes": nodes, "tree": _tree_json(t)}
+    doc["spec"] = scenario_spec_to_json(spec)
+    doc["problem"] = scenario_artifacts_to_json(p)
     path = resolve_output(out_path)
     try:
         with open(path, "w") as f:

@@ -85,7 +85,7 @@ def main():
     import gzip
     import subprocess
 
-    for scen in ("intersection", "latency"):
+    for scen in ("intersection", "latency", "report", "tree"):
         doc = subprocess.run([os.path.join(os.path.dirname(HERE), "oracle", "_ref", "gen_ref"), scen],
                              check=True, capture_output=True, text=True).stdout
         with gzip.open(os.path.join(GOLDEN, "gen_%s.json.gz" % scen), "wt") as f:

@@ -71,13 +71,14 @@ def test_custom_points_match_c_restatement():
     assert cfg["repetitions"] == 1 and cfg["output"] == "bench_results.csv"
 
 
-def test_solver_options_from_json():
-    o = cli.solver_options_from_json({"max_inner_iterations": 7, "tol_cost": 1e-6, "backward": "scan-condensed",
-                                      "parallel": False})
-    assert o.max_inner_iterations == 7 and o.tol_cost == 1e-6
-    for bad in ({"nope": 1}, {"backward": "magic"}, {"max_inner_iterations": 1.5}):
-        with pytest.raises(cli.ConfigError):
-            cli.solver_options_from_json(bad)
+def test_solver_presets_override_strategies():
+    cfg = cli.parse_run_config({"options": {"forward": "nonlinear", "line_search": "sequential"}})
+    cli.apply_solver_name("pmsilqr", cfg["options"])  # bench.cpp:59-64: the preset wins
+    assert (cfg["options"].forward, cfg["options"].line_search) == ("linear", "parallel")
+    cfg["options"]._c()  # runs on the GPU path
+    cli.apply_solver_name("sssilqr", cfg["options"])
+    with pytest.raises(ValueError):
+        cfg["options"]._c()
 
 
 @pytest.mark.parametrize("cfg,msg", [
@@ -89,6 +90,7 @@ def test_solver_options_from_json():
     ('{"experiment": "leaf-sweep", "leaf_counts": [5]}', "unsupported leaf count 5"),
     ('{"experiment": "warp-sweep"}', "unknown experiment"),
     ('{"options": {"bogus": 1}}', "unknown solver option: bogus"),
+    ('{"options": {"backward": "magic"}}', "unknown backward strategy: magic"),
 ])
 def test_run_config_errors(tmp_path, cfg, msg):
     p = tmp_path / "c.json"
