@@ -786,6 +786,32 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
   }
   __syncwarp(mask);
   stamp(2);
+  // Operands of this lane's P / p outputs, loaded before the factorisation so
+  // their shared-memory latency overlaps it (same values, same arithmetic).
+  double s4i[R4][NU], s4j[R4][NU], s4a[R4], s4b[R4];
+#pragma unroll
+  for (int r = 0; r < R4; ++r) {
+    const int q = lane + r * TS;
+    if (q < NX * NX) {
+      const int i = q % NX, j = q / NX;
+#pragma unroll
+      for (int t = 0; t < NU; ++t) {
+        s4i[r][t] = Fm[F::Qux + t + i * NU];
+        s4j[r][t] = Fm[F::Qux + t + j * NU];
+      }
+      s4a[r] = Fm[F::Qxx + q];
+      s4b[r] = Fm[F::Qxx + j + i * NX];
+    } else {
+      const int i = q < F::n4 ? q - NX * NX : 0;
+#pragma unroll
+      for (int t = 0; t < NU; ++t) {
+        s4i[r][t] = Fm[F::Qux + t + i * NU];
+        s4j[r][t] = Fm[F::qu + t];
+      }
+      s4a[r] = Fm[F::qx + i];
+      s4b[r] = 0.0;
+    }
+  }
   // Huu = sym(Quu); every lane factors it and forms Huu^-1, then builds the
   // K / k columns its own outputs need (no shared-memory round trip for K):
   // K(a, j) = -Huu^-1(a, :) Qux(:, j), k(a) = -Huu^-1(a, :) qu.
@@ -820,20 +846,17 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
     if (q < NX * NX) {  // P(i,j) = sym(Qxx + Qux' K)
       const int i = q % NX, j = q / NX;
       ot4[r] = short(F::PT + i * NX + j);
-      double qi[NU], qj[NU], Ki[NU], Kj[NU];
-#pragma unroll
-      for (int t = 0; t < NU; ++t) {
-        qi[t] = Fm[F::Qux + t + i * NU];
-        qj[t] = Fm[F::Qux + t + j * NU];
-      }
+      double Ki[NU], Kj[NU];
+      const double* qi = s4i[r];
+      const double* qj = s4j[r];
       kcol(qi, Ki);
       kcol(qj, Kj);
       if (pol_g && i == 0) {  // lanes of column 0 of P hold K(:, j): the policy write
 #pragma unroll
         for (int t = 0; t < NU; ++t) __stcg(pol_g + PolicyLayout<NX, NU>::K + t + j * NU, Kj[t]);
       }
-      a = Fm[F::Qxx + q];
-      b = Fm[F::Qxx + j + i * NX];
+      a = s4a[r];
+      b = s4b[r];
 #pragma unroll
       for (int t = 0; t < NU; ++t) {
         a = fma(qi[t], Kj[t], a);
@@ -843,18 +866,14 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
       g4[r] = short(ValueLayout<NX>::P + q);
     } else if (q < F::n4) {  // p = qx + Qux' k
       const int i = q - NX * NX;
-      double qi[NU], qu[NU], kk[NU];
-#pragma unroll
-      for (int t = 0; t < NU; ++t) {
-        qi[t] = Fm[F::Qux + t + i * NU];
-        qu[t] = Fm[F::qu + t];
-      }
-      kcol(qu, kk);
+      double kk[NU];
+      const double* qi = s4i[r];
+      kcol(s4j[r], kk);
       if (pol_g && i == 0) {
 #pragma unroll
         for (int t = 0; t < NU; ++t) __stcg(pol_g + PolicyLayout<NX, NU>::k + t, kk[t]);
       }
-      a = Fm[F::qx + i];
+      a = s4a[r];
 #pragma unroll
       for (int t = 0; t < NU; ++t) a = fma(qi[t], kk[t], a);
       b = a;
