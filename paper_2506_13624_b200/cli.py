@@ -1,6 +1,7 @@
 """Benchmark CLI of the reference (proj/tools/bench.cpp) on the GPU solver.
 
     python -m paper_2506_13624_b200.cli run --config <file>          sweep experiments, CSV output
+    python -m paper_2506_13624_b200.cli verify [--suite <name> ...] [--mutate scan-sign]   oracle-equivalence suites
     python -m paper_2506_13624_b200.cli gen --scenario <name> --out <file>   scenario config dump
 
 Same JSON run configuration (bench.cpp:31-57, solver options as
@@ -14,9 +15,8 @@ time. Every solve runs on the GPU through the C ABI; there is no CPU path.
 Strategy names: "pmsilqr" is the GPU path; "hypmsilqr" (condensed shared
 segment) solves the same LQR subproblem and runs on the same GPU path;
 "smsilqr" / "sssilqr" (sequential line search, nonlinear rollout) are other
-algorithms and are rejected. The reference's `verify`
-oracle-equivalence suites are the parity tests under tests/ (they need the
-oracle, which the product never loads).
+algorithms and are rejected. `verify` runs the reference's
+oracle-equivalence suites against the GPU back end (paper_2506_13624_b200.verify).
 """
 import argparse
 import json
@@ -322,11 +322,36 @@ def gen_command(scenario: str, out_path: str, out=sys.stdout, err=sys.stderr) ->
     return 0
 
 
+def verify_command(suites: List[str], mutate: str, out=sys.stdout, err=sys.stderr) -> int:
+    """verify_command (bench.cpp:297-325)."""
+    from .verify import run_suites
+
+    if mutate and mutate != "scan-sign":
+        print("bench verify: unknown mutation '%s'" % mutate, file=err)
+        return 2
+    if suites == ["none"]:
+        print("no suites selected: trivially passing", file=out)
+        return 0
+    results = run_suites(suites, mutate or None)
+    if not results:
+        print("bench verify: no suite matches the selection", file=err)
+        return 2
+    ok = True
+    for r in results:
+        print(r.line(), file=out)
+        ok = ok and r.passed
+    return 0 if ok else 1
+
+
 def main(argv: Optional[List[str]] = None) -> int:
     ap = argparse.ArgumentParser(prog="bench", description="Branch-MPC solver benchmarks (GPU back end)")
     sub = ap.add_subparsers(dest="cmd", required=True)
     r = sub.add_parser("run", help="run a sweep experiment from a JSON config")
     r.add_argument("--config", required=True)
+    v = sub.add_parser("verify", help="run the oracle-equivalence suites on the GPU back end")
+    v.add_argument("--suite", action="append", default=[],
+                   help="scan-riccati, forward, associativity, condensing, tree-qp, cross-strategy, all, none")
+    v.add_argument("--mutate", default="", help="fault injection for harness sanity (scan-sign)")
     g = sub.add_parser("gen", help="generate a scenario config with its problem dump")
     g.add_argument("--scenario", required=True)
     g.add_argument("--out", required=True)
@@ -334,6 +359,8 @@ def main(argv: Optional[List[str]] = None) -> int:
     try:
         if a.cmd == "run":
             return run_command(a.config)
+        if a.cmd == "verify":
+            return verify_command(a.suite, a.mutate)
         return gen_command(a.scenario, a.out)
     except Exception as e:  # noqa: BLE001  (bench.cpp:386-389)
         print("bench: %s" % e, file=sys.stderr)
