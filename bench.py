@@ -320,14 +320,18 @@ def batch_bytes(n, nx, nu):
 
 
 def latency_table(B, ctx):
-    """Single-solve device latency for configs 0, 1 (N sweep), 3 (kernel time
-    of the one solve launch, inputs resident)."""
+    """Single-solve device latency for configs 0, 1 (N sweep), 2 (scenario
+    sweep extremes), 3 (spread and early branchings): kernel time of the one
+    solve launch, inputs resident."""
     import torch
     cases = [("cfg0 N=63 4 leaves", B.intersection_spec(63, 10.0, 0.1), "int"),
              ("cfg1 N=500 4 leaves", B.intersection_spec(500, 10.0, 0.1), "int"),
              ("cfg1 N=1000 4 leaves", B.intersection_spec(1000, 10.0, 0.1), "int"),
+             ("cfg2 N=100 2 leaves {1}", B.multistage_spec(100, [(1, 2)]), "ms"),
+             ("cfg2 N=100 64 leaves {1,26,51}", B.multistage_spec(100, [(1, 4), (26, 4), (51, 4)]), "ms"),
              ("cfg3 N=500 256 leaves {1,100,200,300}", B.multistage_spec(500, [(1, 4), (100, 4), (200, 4), (300, 4)]),
-              "ms")]
+              "ms"),
+             ("cfg3 N=500 256 leaves {1,2,3,4}", B.multistage_spec(500, [(1, 4), (2, 4), (3, 4), (4, 4)]), "ms")]
     out = {}
     for name, spec, kind in cases:
         p = B.build_intersection_case(spec, 2, 2) if kind == "int" else B.build_multistage_case(spec)

@@ -176,6 +176,20 @@ def test_grid_mode_solves_match_oracle(ctx, case):
     assert_same_solve(res, o, o["x"], o["u"], o["records"])
 
 
+CFG2_STEPS = {1: [1], 2: [1, 34], 3: [1, 26, 51]}  # branch steps per depth (spread)
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3])
+@pytest.mark.parametrize("arity", [2, 3, 4])
+def test_cfg2_scenario_sweep_matches_oracle(ctx, arity, depth):
+    """BASELINE cfg2: N=100, branching factor 2-4, branching depth 1-3 (2 to 64 leaves)."""
+    p = B.build_multistage_case(B.multistage_spec(100, [(k, arity) for k in CFG2_STEPS[depth]]))
+    assert p.tree.leaf_count() == arity ** depth
+    res = B.solve(p, ctx=ctx)
+    o = O.solve_problem(p)
+    assert_same_solve(res, o, o["x"], o["u"], o["records"])
+
+
 @pytest.mark.slow
 def test_cfg3_full_size_matches_oracle(ctx):
     """BASELINE cfg3: 256 scenarios x N=500 (59,598 nodes), AL loop active."""

@@ -14,6 +14,8 @@ import _refbind as R  # noqa: E402
 cases = [("cfg0 N=63 4 leaves", dict(family=0, horizon=63)),
          ("cfg1 N=500 4 leaves", dict(family=0, horizon=500)),
          ("cfg1 N=1000 4 leaves", dict(family=0, horizon=1000)),
+         ("cfg2 N=100 2 leaves {1}", dict(family=2, horizon=100, branchings=[(1, 2)])),
+         ("cfg2 N=100 64 leaves {1,26,51}", dict(family=2, horizon=100, branchings=[(1, 4), (26, 4), (51, 4)])),
          ("cfg3 N=500 256 leaves {1,100,200,300}",
           dict(family=2, horizon=500, branchings=[(1, 4), (100, 4), (200, 4), (300, 4)]))]
 which = sys.argv[1:] or [c[0] for c in cases]
