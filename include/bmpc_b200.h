@@ -117,14 +117,28 @@ int bmpc_scenario_build(const bmpc_scenario* spec, bmpc_problem_data** out);
 void bmpc_problem_data_free(bmpc_problem_data* data);
 
 /* -------------------------------------------------------- options/report */
-/* SolverOptions (solver.hpp:28-58); the strategy enums are fixed to the
- * north-star path (pmsilqr: scan backward, linear rollout, parallel LS). */
+/* SolverOptions (solver.hpp:28-58). The strategy enums keep the reference's
+ * numbering (solver.hpp:23-26); defaults are pmsilqr (all 0):
+ *   backward    0 scan_tree_riccati, 1 scan_condensed (solved as 0: the same
+ *               LQR subproblem), 2 sequential_riccati (team Riccati sweep on
+ *               every segment);
+ *   forward     0 linear_rollout, 1 nonlinear_rollout (single-shooting trials);
+ *   line_search 0 parallel, 1 sequential (one step size per round; the
+ *               accepted step is the same in both modes). */
+#define BMPC_BACKWARD_SCAN_TREE_RICCATI 0
+#define BMPC_BACKWARD_SCAN_CONDENSED 1
+#define BMPC_BACKWARD_SEQUENTIAL_RICCATI 2
+#define BMPC_FORWARD_LINEAR 0
+#define BMPC_FORWARD_NONLINEAR 1
+#define BMPC_LINE_SEARCH_PARALLEL 0
+#define BMPC_LINE_SEARCH_SEQUENTIAL 1
 typedef struct bmpc_options {
   int max_inner_iterations, max_outer_iterations, alpha_levels;
   double armijo_beta, merit_gamma, merit_mu0, merit_mu_init, defect_epsilon;
   double tol_defect, tol_cost, tol_feedforward, tol_constraint;
   double penalty_init, penalty_growth, penalty_max;
   double reg_init, reg_min, reg_growth, reg_decay, reg_max;
+  int backward, forward, line_search;
 } bmpc_options;
 void bmpc_options_default(bmpc_options* opts);
 

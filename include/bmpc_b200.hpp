@@ -86,12 +86,9 @@ struct FlatTree {
   }
 };
 
-/// SolverOptions (solver.hpp:28-58) -> bmpc_options; every numeric field maps 1:1.
+/// SolverOptions (solver.hpp:28-58) -> bmpc_options; every field maps 1:1
+/// (the strategy enums keep their numbering, solver.hpp:23-26).
 inline bmpc_options to_abi(const SolverOptions& o) {
-  if (o.forward != ForwardMode::linear_rollout)
-    throw std::invalid_argument("bmpc::b200: only ForwardMode::linear_rollout runs on the GPU path");
-  if (o.line_search != LineSearchMode::parallel)
-    throw std::invalid_argument("bmpc::b200: only LineSearchMode::parallel runs on the GPU path");
   bmpc_options a;
   bmpc_options_default(&a);
   a.max_inner_iterations = o.max_inner_iterations;
@@ -114,6 +111,9 @@ inline bmpc_options to_abi(const SolverOptions& o) {
   a.reg_growth = o.reg_growth;
   a.reg_decay = o.reg_decay;
   a.reg_max = o.reg_max;
+  a.backward = static_cast<int>(o.backward);
+  a.forward = static_cast<int>(o.forward);
+  a.line_search = static_cast<int>(o.line_search);
   return a;
 }
 

@@ -69,7 +69,8 @@ _OPT_DBL = ("armijo_beta", "merit_gamma", "merit_mu0", "merit_mu_init", "defect_
 
 
 class _Options(C.Structure):
-    _fields_ = [(n, C.c_int) for n in _OPT_INT] + [(n, C.c_double) for n in _OPT_DBL]
+    _fields_ = ([(n, C.c_int) for n in _OPT_INT] + [(n, C.c_double) for n in _OPT_DBL] +
+                [("backward", C.c_int), ("forward", C.c_int), ("line_search", C.c_int)])
 
 
 RECORD_FIELDS = ("outer", "accepted", "cost", "cost_al", "merit_before", "merit_after", "model_decrease",
@@ -322,23 +323,32 @@ class SolverOptions:
     reg_growth: float = 10.0
     reg_decay: float = 10.0
     reg_max: float = 1e10
-    # Strategy enums (solver.hpp:23-33, JSON spellings of serialization.hpp:40-61).
-    # The GPU runs the tree-scan backward pass with a linear rollout and the
-    # parallel line search; every backward strategy solves the same LQR
-    # subproblem, the other forward / line-search modes are other algorithms.
+    # Strategy enums (solver.hpp:23-33, JSON spellings of serialization.hpp:40-61),
+    # all on the GPU: "scan-tree-riccati" = tree-segmented scan / team sweep per
+    # segment length, "sequential-riccati" = team Riccati sweep on every
+    # segment, "scan-condensed" solved as the tree scan (same LQR subproblem);
+    # forward "nonlinear" = single-shooting trials (nonlinear rollout under the
+    # feedback policies); line_search "sequential" = one step size per round.
+    # scan_order / parallel only schedule the reference's CPU threads.
     backward: str = "scan-tree-riccati"
     forward: str = "linear"
     line_search: str = "parallel"
     scan_order: str = "tree"
     parallel: bool = True
 
+    _ENUMS = {"backward": ("scan-tree-riccati", "scan-condensed", "sequential-riccati"),
+              "forward": ("linear", "nonlinear"), "line_search": ("parallel", "sequential")}
+
     def _c(self) -> _Options:
-        if self.forward != "linear" or self.line_search != "parallel":
-            raise ValueError("only forward='linear' with line_search='parallel' runs on the GPU path "
-                             "(got forward=%r, line_search=%r)" % (self.forward, self.line_search))
         o = _Options()
         for name, _ in _Options._fields_:
-            setattr(o, name, getattr(self, name))
+            if name in self._ENUMS:
+                v = getattr(self, name)
+                if v not in self._ENUMS[name]:
+                    raise ValueError("unknown %s strategy %r" % (name, v))
+                setattr(o, name, self._ENUMS[name].index(v))
+            else:
+                setattr(o, name, getattr(self, name))
         return o
 
 

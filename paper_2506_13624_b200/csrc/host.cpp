@@ -859,6 +859,9 @@ void bmpc_options_default(bmpc_options* o) {  // solver.hpp:35-57
   o->reg_growth = 10.0;
   o->reg_decay = 10.0;
   o->reg_max = 1e10;
+  o->backward = BMPC_BACKWARD_SCAN_TREE_RICCATI;
+  o->forward = BMPC_FORWARD_LINEAR;
+  o->line_search = BMPC_LINE_SEARCH_PARALLEL;
 }
 
 int bmpc_ctx_create(int device, bmpc_ctx** out) {
@@ -1182,6 +1185,12 @@ static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_input
   d.seq_wide_max = kSeqWideMax;
   d.ls_block = ls_block_for(b->ctx);
   d.fwd_scan_min = std::getenv("BMPC_FWD_SCAN_MIN") ? std::atoi(std::getenv("BMPC_FWD_SCAN_MIN")) : 0;
+  // Strategy enums (solver.hpp:23-26; presets bench.cpp:60-83).
+  if (o.backward < 0 || o.backward > 2 || o.forward < 0 || o.forward > 1 || o.line_search < 0 || o.line_search > 1)
+    return fail(BMPC_ERR_INVALID, "unknown backward / forward / line_search strategy");
+  if (o.backward == BMPC_BACKWARD_SEQUENTIAL_RICCATI) d.seq_max_len = 1 << 30;  // sweep every segment
+  if (o.line_search == BMPC_LINE_SEARCH_SEQUENTIAL) d.ls_block = 1;
+  d.nonlinear_ls = o.forward == BMPC_FORWARD_NONLINEAR ? 1 : 0;
   cudaError_t e;
   if (b->grid_mode) {
     e = launch_solve_grid(b->nx, b->nu, b->plan->d_topo.as<Topo>(), b->mps.as<ModelParams>(), b->works.as<Work>(), d,

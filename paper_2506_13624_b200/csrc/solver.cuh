@@ -1140,6 +1140,129 @@ struct Solver {
     return -1;
   }
 
+  // ------------------------------ single-shooting line search (sssilqr)
+  // ForwardMode::nonlinear_rollout (solver.hpp:463-467): each trial is
+  // nonlinear_rollout(problem, nominal, policies, alpha, x0)
+  // (problem.hpp:170-191): u_i = u_nom_i + K_i (x_i - x_nom_i) + alpha k_i,
+  // x_child = f(x_i, u_i), walked one thread per segment, depth levels in
+  // order. The trial lands in (dx, du) — the linear step is not needed once
+  // EC is formed, and a rejected pass recomputes it. A non-finite state (the
+  // reference throws, evaluate_trial catches) rejects the trial. Alphas are
+  // tried largest first; the first accepted is the parallel mode's answer too.
+  __device__ bool rollout_policy(double alpha) {
+    if (g.leader()) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) w.dx[j] = w.x0[j];
+    }
+    g.sync();
+    double bad = 0.0;
+    for (int d = 0; d < t.ndepth; ++d) {
+      const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
+      for (int s = sb + g.rank(); s < se; s += g.size()) {
+        const int L = seg_len(s);
+        int prev = t.parent[seg_node(s, 0)];
+        for (int k = 0; k < L; ++k) {
+          const int i = seg_node(s, k);
+          double xi[NX];
+          if (prev >= 0) {
+            node_dynamics<NX, NU>(mp, prev, w.dx + prev * NX, w.du + prev * NU, xi);
+            if (!all_finite<NX>(xi)) bad = 1.0;
+            copy<NX>(xi, w.dx + i * NX);
+          } else {
+#pragma unroll
+            for (int j = 0; j < NX; ++j) xi[j] = w.dx[i * NX + j];
+          }
+          if (is_leaf(i)) {
+#pragma unroll
+            for (int j = 0; j < NU; ++j) w.du[i * NU + j] = 0.0;
+          } else {
+            const double* pk = pol(i);
+            double e[NX];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) e[j] = xi[j] - w.x[i * NX + j];
+#pragma unroll
+            for (int r = 0; r < NU; ++r) {
+              double kv = 0.0;
+#pragma unroll
+              for (int j = 0; j < NX; ++j) kv += pk[PL::K + r + j * NU] * e[j];  // K column-major NU x NX
+              w.du[i * NU + r] = (w.u[i * NU + r] + kv) + alpha * pk[PL::k + r];
+            }
+          }
+          prev = i;
+        }
+      }
+      g.sync();
+    }
+    red_put(g, 0, bad, false);
+    g.finish(1, 0);
+    return g.sm->total[0] == 0.0;
+  }
+
+  // evaluate (problem.hpp:109-146) of the trajectory held in (dx, du).
+  __device__ Eval evaluate_trial() {
+    double c = 0, cal = 0, dl = 0, vm = -INFINITY;
+    for (int i = g.rank(); i < t.n; i += g.size()) {
+      const bool leaf = is_leaf(i);
+      const double* xi = w.dx + i * NX;
+      double u[NU];
+#pragma unroll
+      for (int j = 0; j < NU; ++j) u[j] = leaf ? 0.0 : w.du[i * NU + j];
+      double nc, pen, gm;
+      node_cost<NX, NU>(mp, i, leaf, xi, u, w.eta + static_cast<size_t>(i) * t.max_con, g_rho, &nc, &pen, &gm);
+      const double wi = t.weight[i];
+      c += wi * nc;
+      cal += wi * (nc + pen);
+      vm = fmax(vm, gm);
+      const int p = t.parent[i];
+      if (p >= 0) {
+        double f[NX];
+        node_dynamics<NX, NU>(mp, p, w.dx + p * NX, w.du + p * NU, f);
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < NX; ++j) s += fabs(f[j] - xi[j]);
+        dl += s;
+      }
+    }
+    red_put(g, 0, c, true);
+    red_put(g, 1, cal, true);
+    red_put(g, 2, dl, true);
+    red_put(g, 3, vm, false);
+    g.finish(4, 3);
+    return {g.sm->total[0], g.sm->total[1], g.sm->total[2], fmax(g.sm->total[3], 0.0)};
+  }
+
+  __device__ int line_search_nonlinear(int levels, double merit0, double a1, double a2, double mu, double dl1_nom,
+                                       Eval* chosen, double* merit_chosen, double* decrease_chosen, int* evals) {
+    for (int l = 0; l < levels; ++l) {
+      const double alpha = ldexp(1.0, -l);
+      ++*evals;
+      if (!rollout_policy(alpha)) continue;
+      const Eval ev = evaluate_trial();
+      const bool finite = isfinite(ev.cost_al) && isfinite(ev.defect_l1);
+      const double m = finite ? ev.cost_al + mu * ev.defect_l1 : INFINITY;
+      const double ec = a1 * alpha + a2 * alpha * alpha;
+      const double dec = o.armijo_beta * (ec - alpha * mu * dl1_nom);
+      if (isfinite(m) && m <= merit0 + dec) {
+        *chosen = ev;
+        *merit_chosen = m;
+        *decrease_chosen = dec;
+        return l;
+      }
+    }
+    return -1;
+  }
+
+  // Accept the trial held in (dx, du).
+  __device__ void take_trial() {
+    for (int i = g.rank(); i < t.n; i += g.size()) {
+#pragma unroll
+      for (int j = 0; j < NX; ++j) w.x[i * NX + j] = w.dx[i * NX + j];
+#pragma unroll
+      for (int j = 0; j < NU; ++j) w.u[i * NU + j] = w.du[i * NU + j];
+    }
+    g.sync();
+  }
+
   __device__ void take_step(double alpha) {
     for (int i = g.rank(); i < t.n; i += g.size()) {
 #pragma unroll
@@ -1335,8 +1458,10 @@ struct Solver {
         Eval after;
         double merit_after = 0.0, dec = 0.0;
         mark(8);
-        const int lvl =
-            line_search(o.alpha_levels, merit0, a1, a2, mu, ev.defect_l1, &after, &merit_after, &dec, &alpha_evals);
+        const int lvl = o.nonlinear_ls ? line_search_nonlinear(o.alpha_levels, merit0, a1, a2, mu, ev.defect_l1,
+                                                               &after, &merit_after, &dec, &alpha_evals)
+                                       : line_search(o.alpha_levels, merit0, a1, a2, mu, ev.defect_l1, &after,
+                                                     &merit_after, &dec, &alpha_evals);
         mark(7);
         double t4 = now_s();
         times[4] += t4 - t3;
@@ -1366,7 +1491,10 @@ struct Solver {
           }
           continue;
         }
-        take_step(rec.alpha);
+        if (o.nonlinear_ls)
+          take_trial();
+        else
+          take_step(rec.alpha);
         reg = reg / o.reg_decay >= o.reg_min ? reg / o.reg_decay : 0.0;
         ++inner;
         rec.merit_after = merit_after;

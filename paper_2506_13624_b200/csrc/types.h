@@ -42,6 +42,7 @@ struct DevOptions {  // SolverOptions (solver.hpp:28-58), device copy
   const int* order; // optional block -> instance map of a batch launch (nullptr: identity)
   int keep_values;  // 1: store (P, p) of every node (kernel-level API); 0: segment heads only
   int fwd_scan_min; // segments of >= this length take the forward prefix scan (0: walk everywhere)
+  int nonlinear_ls; // 1: ForwardMode::nonlinear_rollout trials (sssilqr, solver.hpp:463-467)
 };
 
 // Suspended solve() loop state (batch scheduling): a solve can stop at the top

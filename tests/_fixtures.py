@@ -23,7 +23,12 @@ def load(name):
 
 
 def scenario_names():
-    return [n for n in names() if not n.startswith("lq") and not n.startswith("lqr_tree")]
+    return [n for n in names() if not n.startswith(("lq", "preset_"))]
+
+
+def preset_names():
+    """Other solver presets (tests/make_golden_presets.py)."""
+    return names("preset_")
 
 
 def lq_names():

@@ -76,15 +76,18 @@ def test_solver_presets_override_strategies():
     cli.apply_solver_name("pmsilqr", cfg["options"])  # bench.cpp:59-64: the preset wins
     assert (cfg["options"].forward, cfg["options"].line_search) == ("linear", "parallel")
     cfg["options"]._c()  # runs on the GPU path
-    cli.apply_solver_name("sssilqr", cfg["options"])
-    with pytest.raises(ValueError):
-        cfg["options"]._c()
+    cli.apply_solver_name("sssilqr", cfg["options"])  # bench.cpp:74-79
+    c = cfg["options"]._c()
+    assert (c.backward, c.forward, c.line_search) == (2, 1, 1)
+    assert cfg["options"].parallel is False
+    cli.apply_solver_name("smsilqr", cfg["options"])
+    c = cfg["options"]._c()
+    assert (c.backward, c.forward, c.line_search) == (2, 0, 1)
 
 
 @pytest.mark.parametrize("cfg,msg", [
     ("{not json", "bad config JSON"),
     ('{"solver": "fastest"}', "unknown solver"),
-    ('{"solver": "smsilqr"}', "not on the GPU path"),
     ('{"repetitions": 0}', "repetitions must be >= 1"),
     ('{"experiment": "leaf-sweep", "leaf_counts": []}', "empty sweep list"),
     ('{"experiment": "leaf-sweep", "leaf_counts": [5]}', "unsupported leaf count 5"),

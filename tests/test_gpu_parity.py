@@ -128,6 +128,26 @@ def test_solve_matches_reference_goldens(ctx, name):
     assert_same_solve(res, fx["report"], fx["x"], fx["u"], fx["records"])
 
 
+@pytest.mark.parametrize("name", F.preset_names())
+def test_solver_presets_match_reference_goldens(ctx, name):
+    """smsilqr (team Riccati sweep everywhere, sequential line search) and
+    sssilqr (single-shooting trials: nonlinear rollout under the feedback
+    policies, solver.hpp:463-467 / problem.hpp:170-191) against the
+    reference's own solves with those presets (bench.cpp:60-83)."""
+    fx = F.load(name)
+    meta = fx["meta"]
+    p = F.build_product_problem(B, meta)
+    o = B.SolverOptions()
+    o.backward = ("scan-tree-riccati", "scan-condensed", "sequential-riccati")[meta["backward"]]
+    o.forward = ("linear", "nonlinear")[meta["forward"]]
+    o.line_search = ("parallel", "sequential")[meta["line_search"]]
+    o.parallel = False
+    res = B.solve(p, o, ctx=ctx)
+    assert_same_solve(res, fx["report"], fx["x"], fx["u"], fx["records"])
+    if meta["forward"] == 1:  # single shooting keeps the trajectory dynamically consistent
+        assert res.report.final_defect_l1 <= 1e-12
+
+
 @pytest.mark.parametrize("name", F.lq_names())
 def test_lq_single_newton_step(ctx, name):
     """tests/acceptance_test.cpp:64-90 and test_solver.cpp:385-411."""

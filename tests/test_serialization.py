@@ -50,7 +50,10 @@ def test_solver_options_flat_keys():  # test_serialization.cpp:25-43
         S.solver_options_from_json({"not_an_option": 1})
     with pytest.raises(ValueError):
         S.solver_options_from_json({"backward": "mystery"})
-    with pytest.raises(ValueError):  # not on the GPU path
+    c = o._c()  # every strategy runs on the GPU (enum numbering of solver.hpp:23-26)
+    assert (c.backward, c.forward, c.line_search) == (1, 1, 1)
+    o.forward = "sideways"
+    with pytest.raises(ValueError):
         o._c()
     back = S.solver_options_from_json(S.solver_options_to_json(B.SolverOptions(reg_init=1e-3, alpha_levels=7)))
     assert back == B.SolverOptions(reg_init=1e-3, alpha_levels=7)
