@@ -61,12 +61,12 @@ void compare(const std::string& name, const bmpc::SolveResult& got, const bmpc::
 }
 
 void scenario_case(const std::string& name, const bmpc::ScenarioSpec& spec, bool latency, int v1, int v2,
-                   const std::vector<bmpc::VectorXd>* u0 = nullptr) {
+                   const std::vector<bmpc::VectorXd>* u0 = nullptr, const bmpc::SolverOptions& opts = {}) {
   bmpc::ScenarioArtifacts art;
   const bmpc::BmpcProblem problem =
       latency ? bmpc::build_latency_case(spec, &art) : bmpc::build_intersection_case(spec, v1, v2, &art);
-  const bmpc::SolveResult want = bmpc::solve(problem, {}, u0);
-  const bmpc::SolveResult got = bmpc::b200::solve(problem, spec, art, {}, u0);  // was bmpc::solve(problem)
+  const bmpc::SolveResult want = bmpc::solve(problem, opts, u0);
+  const bmpc::SolveResult got = bmpc::b200::solve(problem, spec, art, opts, u0);  // was bmpc::solve(problem, opts)
   compare(name, got, want);
 }
 
@@ -120,14 +120,18 @@ int main() {
   lq_case("lq (3,2) N=64 3-ary", 64, {{10, 3, {0.2, 0.3, 0.5}}}, 3, 2, 11);
   lq_case("lq (2,1) N=100 path", 100, {}, 2, 1, 13);
   // Error behaviour.
-  expect_throw<std::invalid_argument>("nonlinear_rollout rejected", [] {
-    const bmpc::ScenarioSpec spec = intersection_spec(20, 4.0, 0.4);
-    bmpc::ScenarioArtifacts art;
-    const bmpc::BmpcProblem p = bmpc::build_intersection_case(spec, 2, 2, &art);
-    bmpc::SolverOptions o;
-    o.forward = bmpc::ForwardMode::nonlinear_rollout;
-    bmpc::b200::solve(p, spec, art, o);
-  });
+  // The other presets (apply_solver_name, tools/bench.cpp:60-83).
+  {
+    bmpc::SolverOptions sm;
+    sm.backward = bmpc::BackwardStrategy::sequential_riccati;
+    sm.line_search = bmpc::LineSearchMode::sequential;
+    sm.parallel = false;
+    bmpc::SolverOptions ss = sm;
+    ss.forward = bmpc::ForwardMode::nonlinear_rollout;
+    scenario_case("smsilqr cfg0", intersection_spec(63, 10.0, 0.1), false, 2, 2, nullptr, sm);
+    scenario_case("sssilqr cfg0", intersection_spec(63, 10.0, 0.1), false, 2, 2, nullptr, ss);
+    scenario_case("sssilqr latency_spec(1.5,63,5,0.05)", latency_spec(1.5, 63, 5.0, 0.05), true, 0, 0, nullptr, ss);
+  }
   expect_throw<std::invalid_argument>("mismatched artifacts rejected", [] {
     const bmpc::ScenarioSpec spec = intersection_spec(20, 4.0, 0.4);
     bmpc::ScenarioArtifacts art;

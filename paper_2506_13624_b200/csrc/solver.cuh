@@ -1159,13 +1159,22 @@ struct Solver {
     for (int d = 0; d < t.ndepth; ++d) {
       const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
       for (int s = sb + g.rank(); s < se; s += g.size()) {
+        // The walked state / input stay in registers along the segment; only
+        // the head reads its parent's (written one depth level earlier).
         const int L = seg_len(s);
         int prev = t.parent[seg_node(s, 0)];
+        double xp[NX], up[NU];
+        if (prev >= 0) {
+#pragma unroll
+          for (int j = 0; j < NX; ++j) xp[j] = w.dx[prev * NX + j];
+#pragma unroll
+          for (int j = 0; j < NU; ++j) up[j] = w.du[prev * NU + j];
+        }
         for (int k = 0; k < L; ++k) {
           const int i = seg_node(s, k);
           double xi[NX];
           if (prev >= 0) {
-            node_dynamics<NX, NU>(mp, prev, w.dx + prev * NX, w.du + prev * NU, xi);
+            node_dynamics<NX, NU>(mp, prev, xp, up, xi);
             if (!all_finite<NX>(xi)) bad = 1.0;
             copy<NX>(xi, w.dx + i * NX);
           } else {
@@ -1174,7 +1183,7 @@ struct Solver {
           }
           if (is_leaf(i)) {
 #pragma unroll
-            for (int j = 0; j < NU; ++j) w.du[i * NU + j] = 0.0;
+            for (int j = 0; j < NU; ++j) up[j] = 0.0;
           } else {
             const double* pk = pol(i);
             double e[NX];
@@ -1185,9 +1194,13 @@ struct Solver {
               double kv = 0.0;
 #pragma unroll
               for (int j = 0; j < NX; ++j) kv += pk[PL::K + r + j * NU] * e[j];  // K column-major NU x NX
-              w.du[i * NU + r] = (w.u[i * NU + r] + kv) + alpha * pk[PL::k + r];
+              up[r] = (w.u[i * NU + r] + kv) + alpha * pk[PL::k + r];
             }
           }
+#pragma unroll
+          for (int j = 0; j < NU; ++j) w.du[i * NU + j] = up[j];
+#pragma unroll
+          for (int j = 0; j < NX; ++j) xp[j] = xi[j];
           prev = i;
         }
       }
