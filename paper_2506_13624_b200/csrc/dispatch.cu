@@ -66,6 +66,14 @@ bool cta_variant_supported(int nx, int nu, int threads, int min_blocks) {
 cudaError_t launch_solve_cta(int nx, int nu, const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
                              const DevOptions& opts, int count, int threads, int min_blocks, bool seq_only,
                              cudaStream_t stream) {
+  if (opts.nonlinear_ls) {  // single-shooting kernels: one shape per (nx, nu)
+#define X(a, b)           \
+  if (nx == a && nu == b) \
+    return SolveLaunch<a, b>::solve_cta_nonlinear(d_topo, d_mp, d_work, opts, count, seq_only, stream);
+    BMPC_SOLVE_DIMS(X)
+#undef X
+    return cudaErrorInvalidValue;
+  }
 #define X(a, b, t, m)                                                 \
   if (nx == a && nu == b && threads == t && min_blocks == m)          \
     return CtaVariant<a, b, t, m>::launch(d_topo, d_mp, d_work, opts, count, seq_only, stream);
@@ -84,9 +92,11 @@ int solve_cta_regs(int nx, int nu, int threads, int min_blocks, bool seq_only) {
 
 cudaError_t launch_solve_grid(int nx, int nu, const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
                               const DevOptions& opts, double* red, int blocks, int threads, cudaStream_t stream) {
-#define X(a, b)           \
-  if (nx == a && nu == b) \
-    return SolveLaunch<a, b>::solve_grid(d_topo, d_mp, d_work, opts, red, blocks, threads, stream);
+#define X(a, b)                                                                                              \
+  if (nx == a && nu == b)                                                                                    \
+    return opts.nonlinear_ls                                                                                 \
+               ? SolveLaunch<a, b>::solve_grid_nonlinear(d_topo, d_mp, d_work, opts, red, blocks, threads, stream) \
+               : SolveLaunch<a, b>::solve_grid(d_topo, d_mp, d_work, opts, red, blocks, threads, stream);
   BMPC_SOLVE_DIMS(X)
 #undef X
   return cudaErrorInvalidValue;

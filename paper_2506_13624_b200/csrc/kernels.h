@@ -50,6 +50,12 @@ struct SolveLaunch {
   static cudaError_t solve_grid(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
                                 const DevOptions& opts, double* red, int blocks, int threads, cudaStream_t stream);
   static int grid_blocks(int threads);
+  // Single-shooting line search compiled in (DevOptions::nonlinear_ls).
+  static cudaError_t solve_cta_nonlinear(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
+                                         const DevOptions& opts, int count, bool seq_only, cudaStream_t stream);
+  static cudaError_t solve_grid_nonlinear(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
+                                          const DevOptions& opts, double* red, int blocks, int threads,
+                                          cudaStream_t stream);
 };
 
 // Dispatch over the compiled dimension sets (dispatch.cu).

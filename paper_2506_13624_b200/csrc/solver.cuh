@@ -178,7 +178,10 @@ __device__ __forceinline__ void red_acc(const G& g, int k, double v, bool is_sum
 // whose segments are all short (e.g. cfg0/cfg4).
 // kTeam > 0 overrides the team width (32 = one warp per segment, for blocks
 // of >= 128 threads where the shorter per-step stages pay).
-template <int NX, int NU, class G, bool kSeqOnly = false, int kTeam = 0>
+// kNL: the single-shooting line search (ForwardMode::nonlinear_rollout) is
+// compiled in — only into the kernels launched for that mode, so the
+// multiple-shooting solve loop keeps its register allocation.
+template <int NX, int NU, class G, bool kSeqOnly = false, int kTeam = 0, bool kNL = false>
 struct Solver {
   using SL = StageLayout<NX, NU>;
   using BL = BwdLayout<NX>;
@@ -1170,8 +1173,25 @@ struct Solver {
 #pragma unroll
           for (int j = 0; j < NU; ++j) up[j] = w.du[prev * NU + j];
         }
+        const SegIdx sq = seg_idx(s);
         for (int k = 0; k < L; ++k) {
-          const int i = seg_node(s, k);
+          const int i = node_at(sq, k);
+          // The node's nominal point and policy are loaded before the
+          // dynamics of the step that produces its state, so their latency
+          // hides under the RK4 arithmetic of the dependency chain.
+          const bool leaf = is_leaf(i);
+          double xn[NX], un[NU], Kp[NU * NX], kp[NU];
+          if (!leaf) {
+            const double* pk = pol(i);
+#pragma unroll
+            for (int j = 0; j < NX; ++j) xn[j] = w.x[i * NX + j];
+#pragma unroll
+            for (int j = 0; j < NU; ++j) un[j] = w.u[i * NU + j];
+#pragma unroll
+            for (int j = 0; j < NU * NX; ++j) Kp[j] = pk[PL::K + j];
+#pragma unroll
+            for (int j = 0; j < NU; ++j) kp[j] = pk[PL::k + j];
+          }
           double xi[NX];
           if (prev >= 0) {
             node_dynamics<NX, NU>(mp, prev, xp, up, xi);
@@ -1181,20 +1201,19 @@ struct Solver {
 #pragma unroll
             for (int j = 0; j < NX; ++j) xi[j] = w.dx[i * NX + j];
           }
-          if (is_leaf(i)) {
+          if (leaf) {
 #pragma unroll
             for (int j = 0; j < NU; ++j) up[j] = 0.0;
           } else {
-            const double* pk = pol(i);
             double e[NX];
 #pragma unroll
-            for (int j = 0; j < NX; ++j) e[j] = xi[j] - w.x[i * NX + j];
+            for (int j = 0; j < NX; ++j) e[j] = xi[j] - xn[j];
 #pragma unroll
             for (int r = 0; r < NU; ++r) {
               double kv = 0.0;
 #pragma unroll
-              for (int j = 0; j < NX; ++j) kv += pk[PL::K + r + j * NU] * e[j];  // K column-major NU x NX
-              up[r] = (w.u[i * NU + r] + kv) + alpha * pk[PL::k + r];
+              for (int j = 0; j < NX; ++j) kv += Kp[r + j * NU] * e[j];  // K column-major NU x NX
+              up[r] = (un[r] + kv) + alpha * kp[r];
             }
           }
 #pragma unroll
@@ -1471,10 +1490,12 @@ struct Solver {
         Eval after;
         double merit_after = 0.0, dec = 0.0;
         mark(8);
-        const int lvl = o.nonlinear_ls ? line_search_nonlinear(o.alpha_levels, merit0, a1, a2, mu, ev.defect_l1,
-                                                               &after, &merit_after, &dec, &alpha_evals)
-                                       : line_search(o.alpha_levels, merit0, a1, a2, mu, ev.defect_l1, &after,
-                                                     &merit_after, &dec, &alpha_evals);
+        int lvl;
+        if constexpr (kNL)
+          lvl = line_search_nonlinear(o.alpha_levels, merit0, a1, a2, mu, ev.defect_l1, &after, &merit_after, &dec,
+                                      &alpha_evals);
+        else
+          lvl = line_search(o.alpha_levels, merit0, a1, a2, mu, ev.defect_l1, &after, &merit_after, &dec, &alpha_evals);
         mark(7);
         double t4 = now_s();
         times[4] += t4 - t3;
@@ -1504,7 +1525,7 @@ struct Solver {
           }
           continue;
         }
-        if (o.nonlinear_ls)
+        if constexpr (kNL)
           take_trial();
         else
           take_step(rec.alpha);
@@ -1582,5 +1603,6 @@ struct Solver {
     }
   }
 };
+
 
 }  // namespace bmpc_b200
