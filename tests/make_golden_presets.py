@@ -23,10 +23,14 @@ CASES = ("cfg0_intersection_63", "intersection_20_4s", "latency_0p5_63", "multis
          "cfg4_instance_seed42")
 
 
+# Whole-GPU (cooperative grid) path: trees > 1024 nodes.
+EXTRA = {"intersection_300": (0, 300, 10.0, (0.1, 0.0), (2, 2), (), None)}
+
+
 def main():
     for solver, (bw, fw, ls) in PRESETS.items():
-        for name in CASES:
-            fam, N, T, sh, v, br, seed = SCENARIOS[name]
+        for name in CASES + tuple(EXTRA):
+            fam, N, T, sh, v, br, seed = {**SCENARIOS, **EXTRA}[name]
             sc = R.scenario(fam, N, total_time=T, shared=sh, v=v, branchings=br, perturb_seed=seed)
             o = R.default_options()
             o.backward, o.forward, o.line_search, o.parallel = bw, fw, ls, 0

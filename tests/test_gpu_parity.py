@@ -418,3 +418,40 @@ def test_native_library_loaded(ctx):
     assert ctx.launches >= n0 + 1  # the solve (+ the result pack kernel)
     maps = open("/proc/self/maps").read()
     assert "libbmpc_b200.so" in maps
+
+
+def test_single_shooting_batch_schedule_and_singles_agree():
+    """sssilqr over a batch larger than one wave (probe / order / main /
+    finish launches of the single-shooting kernel): bit-identical to the
+    one-launch FIFO batch and to single solves, and instance 0 (seed 42)
+    matches the reference's own sssilqr solve."""
+    probs = [B.build_intersection_case(B.intersection_spec(63, 10.0, 0.1), 2, 2, perturb_seed=42 + s)
+             for s in range(400)]
+    o = B.SolverOptions(backward="sequential-riccati", forward="nonlinear", line_search="sequential", parallel=False)
+    outs = {}
+    for probe in (0, 10):
+        c = B.Context(0)
+        B.set_schedule(c, probe)
+        bt = B.Batch(c, probs, max_records=600)
+        bt.set_models()
+        bt.solve(o)
+        x = np.zeros((len(probs), bt.n, bt.nx))
+        u = np.zeros((len(probs), bt.n, bt.nu))
+        reps, _ = bt.results(x, u)
+        outs[probe] = (x, u, reps, bt.records(0, 600))
+    x0, u0, r0, rec0 = outs[0]
+    x1, u1, r1, _ = outs[10]
+    np.testing.assert_array_equal(x1, x0)
+    np.testing.assert_array_equal(u1, u0)
+    assert [(a.status, a.inner_iterations, a.outer_iterations) for a in r1] == \
+        [(a.status, a.inner_iterations, a.outer_iterations) for a in r0]
+    fx = F.load("preset_sssilqr_cfg4_instance_seed42")
+    assert (r0[0].inner_iterations, r0[0].outer_iterations) == \
+        (fx["report"]["inner_iterations"], fx["report"]["outer_iterations"])
+    np.testing.assert_array_equal(rec0["alpha"], fx["records"]["alpha"])
+    assert _gen.rel_err(x0[0], fx["x"]) <= TOL and _gen.rel_err(u0[0], fx["u"]) <= TOL
+    ctx = B.Context(0)
+    for i in (0, 7, 399):
+        r = B.solve(probs[i], o, ctx=ctx)
+        np.testing.assert_array_equal(r.trajectory.state, x0[i])
+        assert r.report.inner_iterations == r0[i].inner_iterations
