@@ -149,3 +149,19 @@ def test_run_custom_matches_oracle(tmp_path):
     rep = ref
     assert int(row[6]) == rep["inner_iterations"]
     assert abs(float(row[7]) - rep["final_cost"]) <= 1e-8 * max(1.0, abs(rep["final_cost"]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("solver", ["smsilqr", "sssilqr"])
+def test_run_presets_match_reference(tmp_path, monkeypatch, solver):
+    """`bench run` with the other presets (apply_solver_name, bench.cpp:60-83)
+    on the GPU: the CSV row carries the reference preset's counts and cost."""
+    monkeypatch.setenv("BMPC_OUT_DIR", str(tmp_path))
+    p = tmp_path / "c.json"
+    p.write_text(json.dumps({"experiment": "horizon-sweep", "horizons": [63], "solver": solver, "output": "p.csv"}))
+    assert cli.run_command(str(p), out=io.StringIO(), err=io.StringIO()) == 0
+    row = (tmp_path / "p.csv").read_text().splitlines()[1].split(",")
+    rep = json.loads(str(_golden("preset_%s_cfg0_intersection_63" % solver)["report"]))
+    assert row[-1] == "converged"
+    assert int(row[6]) == rep["inner_iterations"]
+    assert abs(float(row[7]) - rep["final_cost"]) <= 1e-8 * max(1.0, abs(rep["final_cost"]))
