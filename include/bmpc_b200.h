@@ -166,6 +166,8 @@ typedef struct bmpc_report {
 /* ------------------------------------------------------------- context */
 typedef struct bmpc_ctx bmpc_ctx;
 int bmpc_ctx_create(int device, bmpc_ctx** out);
+/* Destroying a ctx that still has live batches only marks it; the last
+ * bmpc_batch_destroy frees it (any destruction order is safe). */
 void bmpc_ctx_destroy(bmpc_ctx* ctx);
 int bmpc_ctx_set_stream(bmpc_ctx* ctx, void* cuda_stream); /* cudaStream_t; NULL = ctx-owned stream */
 int bmpc_ctx_synchronize(bmpc_ctx* ctx);

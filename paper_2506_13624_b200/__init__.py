@@ -487,6 +487,15 @@ class Batch:
         """Trajectories into x [count, n, nx] / u [count, n, nu] and the reports:
         SolveReport objects, or with as_array=True one zero-copy numpy structured
         array of the C bmpc_report records (fields status, inner_iterations, ...)."""
+        # The C call memcpys count*n*nx / count*n*nu doubles into the raw
+        # buffers: only exact float64, C-contiguous, writable arrays pass.
+        for name, a, shape in (("x", x, (self.count, self.n, self.nx)), ("u", u, (self.count, self.n, self.nu))):
+            if a is None:
+                continue
+            if not isinstance(a, np.ndarray) or a.dtype != np.float64 or a.shape != shape or \
+                    not a.flags.c_contiguous or not a.flags.writeable:
+                raise ValueError(f"{name} must be a writable C-contiguous float64 array of shape {shape}, got "
+                                 f"{getattr(a, 'dtype', type(a))} {getattr(a, 'shape', '')}")
         reps = (_Report * self.count)() if want_reports else None
         b = C.c_size_t()
         _check(lib().bmpc_batch_results(self._h, _ptr(x), _ptr(u), reps, C.byref(b)))

@@ -611,8 +611,16 @@ void fill_report(const DevResult& r, bmpc_report* out) {
     case kErrRegCap: msg = "regularization exceeded its cap"; break;
     case kErrFactorization: msg = "combine_bwd: singular (I + C P) at regularization cap"; break;
     case kErrLineSearch: msg = "line search failed at maximum regularization"; break;
-    case kErrLinearizeNonfinite:
+    case kErrLinearizeNonfinite:  // the reference's three linearize messages (solver.hpp:102-145)
       std::snprintf(buf, sizeof buf, "linearize: non-finite expansion at node %d", r.error_node);
+      msg = buf;
+      break;
+    case kErrLinearizeTerminal:
+      std::snprintf(buf, sizeof buf, "linearize: non-finite terminal expansion at node %d", r.error_node);
+      msg = buf;
+      break;
+    case kErrDefectNonfinite:
+      std::snprintf(buf, sizeof buf, "linearize: non-finite defect at node %d", r.error_node);
       msg = buf;
       break;
     case kErrRolloutNonfinite:
@@ -637,7 +645,18 @@ struct bmpc_ctx {
   bool own_stream{false};
   long long launches{0};
   int sms{0};
+  // Batches alive on this ctx: bmpc_ctx_destroy with live batches only marks
+  // the ctx, the last bmpc_batch_destroy frees it (any destruction order is
+  // safe, e.g. garbage-collected language bindings at interpreter exit).
+  int live_batches{0};
+  bool destroy_pending{false};
 };
+
+static void ctx_free(bmpc_ctx* c) {
+  cudaSetDevice(c->device);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
 
 // Crossover between the team Riccati sweep and the scan (segment length).
 // Measured on B200: the O(L) sweep wins below a few hundred nodes.
@@ -885,9 +904,11 @@ int bmpc_ctx_create(int device, bmpc_ctx** out) {
 
 void bmpc_ctx_destroy(bmpc_ctx* c) {
   if (!c) return;
-  cudaSetDevice(c->device);
-  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
-  delete c;
+  if (c->live_batches > 0) {
+    c->destroy_pending = true;
+    return;
+  }
+  ctx_free(c);
 }
 
 int bmpc_ctx_set_seq_max_len(bmpc_ctx* c, int len) {
@@ -910,12 +931,18 @@ int bmpc_ctx_set_line_search_block(bmpc_ctx* c, int alphas) {
 
 int bmpc_ctx_set_stream(bmpc_ctx* c, void* stream) {
   if (!c) return fail(BMPC_ERR_INVALID, "null ctx");
-  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  // The replacement stream must belong to the ctx's device, not the current one.
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(BMPC_ERR_CUDA, "cudaSetDevice");
   if (stream) {
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     c->stream = static_cast<cudaStream_t>(stream);
     c->own_stream = false;
   } else {
-    cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    cudaStream_t s = nullptr;
+    const cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return fail(BMPC_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    c->stream = s;
     c->own_stream = true;
   }
   return BMPC_OK;
@@ -1008,6 +1035,7 @@ int bmpc_batch_create(bmpc_ctx* ctx, const bmpc_tree* tree, int count, const bmp
       w.prof = nullptr;
     }
     ck(cudaMemcpyAsync(b->works.p, b->h_works.data(), C * sizeof(Work), cudaMemcpyHostToDevice, ctx->stream), "works");
+    ++ctx->live_batches;
     *out = b.release();
     return BMPC_OK;
   } catch (const std::invalid_argument& e) {
@@ -1019,9 +1047,11 @@ int bmpc_batch_create(bmpc_ctx* ctx, const bmpc_tree* tree, int count, const bmp
 
 void bmpc_batch_destroy(bmpc_batch* b) {
   if (!b) return;
-  cudaSetDevice(b->ctx->device);
-  cudaStreamSynchronize(b->ctx->stream);
+  bmpc_ctx* c = b->ctx;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
   delete b;
+  if (--c->live_batches == 0 && c->destroy_pending) ctx_free(c);
 }
 
 int bmpc_batch_set_models(bmpc_batch* b, const bmpc_model_desc* models, size_t* h2d_bytes) {
@@ -1185,6 +1215,9 @@ static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_input
   d.seq_wide_max = kSeqWideMax;
   d.ls_block = ls_block_for(b->ctx);
   d.fwd_scan_min = std::getenv("BMPC_FWD_SCAN_MIN") ? std::atoi(std::getenv("BMPC_FWD_SCAN_MIN")) : 0;
+  // Chunked (time-parallel) backward sweep in wide blocks, opt-in (BMPC_CHUNK_BWD=1): measured slower
+  // than the team sweep on every shape (cfg0 alone, 256 threads: 129 vs 80 us per pass).
+  d.chunk_bwd = std::getenv("BMPC_CHUNK_BWD") ? std::atoi(std::getenv("BMPC_CHUNK_BWD")) : 0;
   // Strategy enums (solver.hpp:23-26; presets bench.cpp:60-83).
   if (o.backward < 0 || o.backward > 2 || o.forward < 0 || o.forward > 1 || o.line_search < 0 || o.line_search > 1)
     return fail(BMPC_ERR_INVALID, "unknown backward / forward / line_search strategy");

@@ -81,6 +81,7 @@ __device__ void lqr_tree_body(G g, BlockCtx& ctx, double reg, double* scalars, i
   o.seq_max_len = seq_max;
   o.fwd_scan_min = seq_max > 0 ? seq_max + 1 : 1;  // kernel-level API: forward mirrors the backward strategy
   o.keep_values = 1;
+  o.chunk_bwd = 1;  // long segments in 256-thread blocks: the chunked sweep (tested against the oracle here)
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   Solver<NX, NU, G> s(g, ctx.topo, dummy, ctx.work, o);
   s.tsm = dyn_smem + red_smem_bytes(blockDim.x);
@@ -132,6 +133,9 @@ static size_t team_smem_bytes(int threads) {
   return red_smem_bytes(threads) + (team > walk ? team : walk);
 }
 
+// The dynamic shared-memory opt-in is a per-device-context attribute, so it is
+// set before every launch (a host-side call of ~1 us) rather than once per
+// process: a process that solves on several devices gets it on each.
 template <class K>
 static void allow_smem(K kernel, size_t bytes) {
   cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -198,13 +202,13 @@ template <int NX, int NU, int T, int MB>
 cudaError_t CtaVariant<NX, NU, T, MB>::launch(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
                                               const DevOptions& opts, int count, bool seq_only, cudaStream_t stream) {
   const size_t smem = team_smem_bytes<NX, NU>(T);
-  static bool once = (allow_smem(solve_cta_kernel<NX, NU, T, MB, false>, smem),
-                      allow_smem(solve_cta_kernel<NX, NU, T, MB, true>, smem), true);
-  (void)once;
-  if (seq_only && team_size<NX, NU>() > 0)
+  if (seq_only && team_size<NX, NU>() > 0) {
+    allow_smem(solve_cta_kernel<NX, NU, T, MB, true>, smem);
     solve_cta_kernel<NX, NU, T, MB, true><<<count, T, smem, stream>>>(d_topo, d_mp, d_work, opts, count);
-  else
+  } else {
+    allow_smem(solve_cta_kernel<NX, NU, T, MB, false>, smem);
     solve_cta_kernel<NX, NU, T, MB, false><<<count, T, smem, stream>>>(d_topo, d_mp, d_work, opts, count);
+  }
   return cudaGetLastError();
 }
 
@@ -238,13 +242,13 @@ cudaError_t SolveLaunch<NX, NU>::solve_cta_nonlinear(const Topo* d_topo, const M
                                                      cudaStream_t stream) {
   constexpr int T = 256;
   const size_t smem = team_smem_bytes<NX, NU>(T);
-  static bool once = (allow_smem(solve_cta_kernel<NX, NU, T, 1, false, true>, smem),
-                      allow_smem(solve_cta_kernel<NX, NU, T, 1, true, true>, smem), true);
-  (void)once;
-  if (seq_only && team_size<NX, NU>() > 0)
+  if (seq_only && team_size<NX, NU>() > 0) {
+    allow_smem(solve_cta_kernel<NX, NU, T, 1, true, true>, smem);
     solve_cta_kernel<NX, NU, T, 1, true, true><<<count, T, smem, stream>>>(d_topo, d_mp, d_work, opts, count);
-  else
+  } else {
+    allow_smem(solve_cta_kernel<NX, NU, T, 1, false, true>, smem);
     solve_cta_kernel<NX, NU, T, 1, false, true><<<count, T, smem, stream>>>(d_topo, d_mp, d_work, opts, count);
+  }
   return cudaGetLastError();
 }
 

@@ -452,8 +452,9 @@ __device__ int team_combine_bwd(const double* e1g, const double* e2g, double* ou
     ok = isfinite(a_out) && isfinite(C_out) && isfinite(P_out);
   }
   if (lane < NX) ok = ok && isfinite(c_out) && isfinite(p_out);
-  // Every lane finished reading the staged operands before `out` (which may
-  // alias e1g/e2g) is written — the stores below only touch global memory.
+  // `out` may alias e1g / e2g or the staged operands themselves (sm.e2, the
+  // chunked scan's accumulator): every lane finishes its reads first.
+  __syncwarp(mask);
   if (act) {
     out[E::A + lane] = a_out;
     out[E::C + lane] = C_out;

@@ -24,6 +24,8 @@
 
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "linalg.cuh"
 #include "lqr.cuh"
 #include "model.cuh"
@@ -283,7 +285,9 @@ struct Solver {
           if (prev >= 0) {
             double xn[NX];
             node_dynamics<NX, NU>(mp, prev, w.x + prev * NX, w.u + prev * NU, xn);
-            if (!all_finite<NX>(xn) && bad == 0.0) bad = prev + 1;
+            // First failing node in index order (the reference throws there,
+            // problem.hpp:160-162): reduce max of (n - node).
+            if (!all_finite<NX>(xn)) bad = fmax(bad, static_cast<double>(t.n - prev));
             copy<NX>(xn, w.x + i * NX);
           }
           prev = i;
@@ -294,7 +298,7 @@ struct Solver {
     red_put(g, 0, bad, false);
     g.finish(1, 0);
     if (g.sm->total[0] > 0.0) {
-      if (g.leader()) w.result->error_node = static_cast<int>(g.sm->total[0]) - 1;
+      if (g.leader()) w.result->error_node = t.n - static_cast<int>(g.sm->total[0]);
       return false;
     }
     return true;
@@ -371,10 +375,13 @@ struct Solver {
   }
 
   // ------------------------------------ linearize + evaluate (fused, Phase L)
-  // Returns the nominal evaluation; sets *bad_node (1-based) on a non-finite
-  // expansion or defect (linearize throws there, solver.hpp:106-146).
-  __device__ Eval linearize_evaluate(int* bad_node) {
-    double c = 0, cal = 0, dl = 0, vm = -INFINITY, bad = 0;
+  // Returns the nominal evaluation. On a non-finite expansion or defect,
+  // *bad_node = 1 + the node the reference throws at and *bad_code its error
+  // (linearize, solver.hpp:76-149: every node's expansion is checked in index
+  // order first, then every defect): the smallest failing expansion node, else
+  // the smallest failing defect node.
+  __device__ Eval linearize_evaluate(int* bad_node, int* bad_code) {
+    double c = 0, cal = 0, dl = 0, vm = -INFINITY, bad = 0, badd = 0;
     for (int i = g.rank(); i < t.n; i += g.size()) {
       const bool leaf = is_leaf(i);
       const double* eta = w.eta + static_cast<size_t>(i) * t.max_con;
@@ -389,15 +396,20 @@ struct Solver {
       dl += d;
       vm = fmax(vm, v);
       const bool dok = all_finite<NX>(w.defect + i * NX);
-      if (!(ok && dok) && bad == 0) bad = i + 1;
+      if (!ok) bad = fmax(bad, static_cast<double>(t.n - i));
+      if (!dok) badd = fmax(badd, static_cast<double>(t.n - i));
     }
     red_put(g, 0, c, true);
     red_put(g, 1, cal, true);
     red_put(g, 2, dl, true);
     red_put(g, 3, vm, false);
     red_put(g, 4, bad, false);
-    g.finish(5, 3);
-    *bad_node = static_cast<int>(g.sm->total[4]);
+    red_put(g, 5, badd, false);
+    g.finish(6, 3);
+    const int be = static_cast<int>(g.sm->total[4]), bd = static_cast<int>(g.sm->total[5]);
+    *bad_node = be > 0 ? t.n - be + 1 : (bd > 0 ? t.n - bd + 1 : 0);
+    *bad_code = be > 0 ? (is_leaf(t.n - be) ? kErrLinearizeTerminal : kErrLinearizeNonfinite)
+                       : kErrDefectNonfinite;
     return {g.sm->total[0], g.sm->total[1], g.sm->total[2], fmax(g.sm->total[3], 0.0)};
   }
 
@@ -526,10 +538,201 @@ struct Solver {
     return ((a > b ? a : b) + 15) / 16 * 16;  // 16-byte aligned slots (vector loads)
   }
 
+  // Team Bellman steps along one segment, nodes k_hi down to k_lo (positions
+  // in the segment), starting from the value of node k_hi + 1 already staged
+  // in the team's flat array Fm (P, PT, p). The next node's stage record and
+  // edge offset are prefetched into registers while each step computes.
+  // Values are stored at the segment head (the parent's branch step reads
+  // them) or everywhere with keep_values; policies always.
+  template <int TS>
+  __device__ int team_chain(const SegIdx& sq, int k_hi, int k_lo, double reg, int lane, unsigned mask, double* Fm) {
+    using F = RicFlat<NX, NU>;
+    constexpr int PRE = (SL::size + TS - 1) / TS;
+    int err = kBwdOk;
+    __syncwarp(mask);
+    {
+      const double* s0 = stage(node_at(sq, k_hi));
+      for (int k = lane; k < SL::size; k += TS) Fm[F::S + k] = s0[k];
+      if (lane < NX) Fm[F::c + lane] = w.defect[node_at(sq, k_hi + 1) * NX + lane];
+    }
+    // Base pointers in registers: the step's generic stores could alias the
+    // shared-memory Work struct, which would force a reload every step.
+    const double* const stg = w.stage;
+    const double* const dfc = w.defect;
+    double* const vbase = w.value;
+    double* const pbase = w.policy;
+    for (int k = k_hi; k >= k_lo; --k) {
+      const int i = node_at(sq, k);
+      double pre[PRE];
+      double prec = 0.0;
+      if (k > k_lo) {
+        const double* sp = stg + static_cast<size_t>(node_at(sq, k - 1)) * SL::stride;
+#pragma unroll
+        for (int j = 0; j < PRE; ++j) {
+          const int idx = lane + j * TS;
+          pre[j] = idx < SL::size ? sp[idx] : 0.0;
+        }
+        if (lane < NX) prec = dfc[i * NX + lane];
+      }
+      double* const vi = (k == 0 || o.keep_values) ? vbase + static_cast<size_t>(i) * VL::stride : nullptr;
+      const int e = team_riccati_step_u<NX, NU, TS>(reg, mask, Fm, lane, vi, pbase + static_cast<size_t>(i) * PL::stride);
+      err = err ? err : e;
+      if (k > k_lo) {
+        __syncwarp(mask);
+#pragma unroll
+        for (int j = 0; j < PRE; ++j) {
+          const int idx = lane + j * TS;
+          if (idx < SL::size) Fm[F::S + idx] = pre[j];
+        }
+        if (lane < NX) Fm[F::c + lane] = prec;
+      }
+    }
+    return err;
+  }
+
+  // ----------------------------------------- chunked (time-parallel) sweep
+  // Block-local backward pass of the segments of depth d when the block has
+  // more teams than the depth has segments: each segment is cut into J chunks
+  // of Ck positions and
+  //   A) every chunk folds its one-step elements (init_bwd_element, the
+  //      terminal embedded at the last position) with combine_bwd
+  //      (lqr_scan.hpp:28-111) into one chunk element G_j (one team per chunk);
+  //   B) one team per segment forms the suffixes S_j = G_j (+) S_{j+1} of the
+  //      chunk elements (J - 1 combinations), so the value function at every
+  //      chunk boundary is known (the (P, p) of S_j, backward_scan,
+  //      lqr_scan.hpp:123-141);
+  //   C) every chunk runs its Bellman steps from the value at its right
+  //      boundary (team_chain), producing the policies (feedback_from_values
+  //      + the value update) and the head values.
+  // Latency ~(Ck - 1 + J - 1) combinations + Ck steps instead of L - 1 steps:
+  // the time-parallel form of the reference's P1 scan with only block
+  // barriers between the phases.
+  static constexpr int kTC = team_size<NX, NU>();  // 16-lane teams (the allocated team slots)
+  __device__ int chunk_count(int d) const {
+    if (kTC <= 0 || G::bdim() < 256 || !o.chunk_bwd) return 1;
+    const int L = t.depth_len[d], ns = t.depth_begin[d + 1] - t.depth_begin[d];
+    if (L < 8) return 1;
+    const int J = min((G::bdim() / kTC) / max(ns, 1), L / 4);
+    return J >= 2 ? J : 1;
+  }
+
+  __device__ int chunked_bwd_depth(int d, double reg) {
+    int err = kBwdOk;
+    if constexpr (kTC > 0) {
+      using F = RicFlat<NX, NU>;
+      const int L = t.depth_len[d];
+      const int sb = t.depth_begin[d], se = t.depth_begin[d + 1], ns = se - sb;
+      int J = chunk_count(d);
+      const int Ck = (L + J - 1) / J;
+      J = (L + Ck - 1) / Ck;
+      // Element of position pos (chain step pos, the terminal at L - 1) in
+      // slot L - 1 - pos; chunk elements G_j in slots L + j, suffixes S_j in L + J + j.
+      // 0a: terminals (regularized leaf cost / branch-node Bellman step over the summed children).
+      for_depth_items(d, 1, [&](int s, int) {
+        const int b = seg_node(s, L - 1);
+        double P[NX * NX], p[NX];
+        if (is_leaf(b)) {
+          copy<NX * NX>(stage(b) + SL::Q, P);
+          copy<NX>(stage(b) + SL::q, p);
+#pragma unroll
+          for (int j = 0; j < NX; ++j) P[j + j * NX] += reg;
+        } else {
+          double Pn[NX * NX], pn[NX];
+#pragma unroll
+          for (int j = 0; j < NX * NX; ++j) Pn[j] = 0.0;
+#pragma unroll
+          for (int j = 0; j < NX; ++j) pn[j] = 0.0;
+          const int c0 = t.first_child[b], nc = t.nchild[b];
+          for (int ch = c0; ch < c0 + nc; ++ch) {
+            const double* v = value_ptr(ch);
+            double Pd[NX];
+            mv<NX, NX>(v, w.defect + ch * NX, Pd);
+#pragma unroll
+            for (int j = 0; j < NX * NX; ++j) Pn[j] += v[j];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) pn[j] += v[NX * NX + j] + Pd[j];
+          }
+          const int e = riccati_step<NX, NU>(stage(b), reg, Pn, pn, P, p, pol(b) + PL::K, pol(b) + PL::k);
+          err = err ? err : e;
+        }
+        if (o.keep_values) {
+          copy<NX * NX>(P, val(b) + VL::P);
+          copy<NX>(p, val(b) + VL::p);
+        }
+        embed_terminal<NX>(P, p, bwd(t.seg_scratch[s] + 0));
+      });
+      // 0b: one-step elements of the chain nodes (chain_stage, solver.hpp:189-193).
+      for_depth_items(d, L - 1, [&](int s, int k) {
+        const int i = seg_node(s, k), nxt = seg_node(s, k + 1);
+        const int e = init_bwd_element<NX, NU>(stage(i), reg, w.defect + nxt * NX, bwd(t.seg_scratch[s] + L - 1 - k));
+        err = err ? err : e;
+      });
+      g.sync();
+      const int team = threadIdx.x / kTC, nteams = G::bdim() / kTC, lane = threadIdx.x % kTC;
+      const unsigned mask = kTC == 32 ? 0xffffffffu : (((1u << kTC) - 1u) << ((threadIdx.x & 31) / kTC * kTC));
+      unsigned char* slot = reinterpret_cast<unsigned char*>(tsm) + team * slot_bytes();
+      TeamSmem<NX>& cs = *reinterpret_cast<TeamSmem<NX>*>(slot);
+      // A: chunk elements.
+      for (int q = team; q < ns * J; q += nteams) {
+        const int s = sb + q / J, j = q % J, base = t.seg_scratch[s];
+        const int a = j * Ck, b = min(L, a + Ck);
+        __syncwarp(mask);
+        for (int k = lane; k < BL::size; k += kTC) cs.e2[k] = bwd(base + L - 1 - (b - 1))[k];
+        for (int pos = b - 2; pos >= a; --pos) {
+          const int e = team_combine_bwd<NX, kTC>(bwd(base + L - 1 - pos), cs.e2, cs.e2, lane, mask, cs);
+          err = err ? err : e;
+        }
+        __syncwarp(mask);
+        for (int k = lane; k < BL::size; k += kTC) bwd(base + L + j)[k] = cs.e2[k];
+      }
+      g.sync();
+      // B: suffixes of the chunk elements, S_{J-1} .. S_1 (S_0 is not needed).
+      for (int q = team; q < ns; q += nteams) {
+        const int base = t.seg_scratch[sb + q];
+        __syncwarp(mask);
+        for (int k = lane; k < BL::size; k += kTC) {
+          const double v = bwd(base + L + J - 1)[k];
+          cs.e2[k] = v;
+          bwd(base + L + J + J - 1)[k] = v;
+        }
+        for (int j = J - 2; j >= 1; --j) {
+          const int e = team_combine_bwd<NX, kTC>(bwd(base + L + j), cs.e2, cs.e2, lane, mask, cs);
+          err = err ? err : e;
+          __syncwarp(mask);
+          for (int k = lane; k < BL::size; k += kTC) bwd(base + L + J + j)[k] = cs.e2[k];
+        }
+      }
+      g.sync();
+      // C: Bellman steps of every chunk from the value at its right boundary.
+      double* Fm = reinterpret_cast<double*>(slot);
+      for (int q = team; q < ns * J; q += nteams) {
+        const int s = sb + q / J, j = q % J, base = t.seg_scratch[s];
+        const int a = j * Ck, b = min(L, a + Ck);
+        const SegIdx sq = seg_idx(s);
+        // Value at position b (chunk j + 1's head), or the terminal itself.
+        const double* vb = j == J - 1 ? bwd(base + 0) : bwd(base + L + J + j + 1);
+        __syncwarp(mask);
+        for (int k = lane; k < NX * NX; k += kTC) ric_put_P<NX, NU>(Fm, k, vb[BL::P + k]);
+        for (int k = lane; k < NX; k += kTC) Fm[F::p + k] = vb[BL::p + k];
+        if (lane < NX) Fm[F::ZERO + lane] = 0.0;
+        const int k_hi = (j == J - 1 ? L - 1 : b) - 1;
+        if (k_hi >= a) {
+          const int e = team_chain<kTC>(sq, k_hi, a, reg, lane, mask, Fm);
+          err = err ? err : e;
+        }
+      }
+    }
+    g.sync();
+    return err;
+  }
+
   // Team Riccati sweep of every (short) segment at depth d: terminal (leaf
   // cost + reg, or the branch-node step over the summed children), then the
   // chain nodes tail -> head. Produces values (w.value) and policies.
   __device__ int riccati_sweep_depth(int d, double reg) {
+    if constexpr (!std::is_same<G, GridGroup>::value) {
+      if (chunk_count(d) > 1) return chunked_bwd_depth(d, reg);
+    }
     int err = kBwdOk;
     if constexpr (kTS > 0) {
       using F = RicFlat<NX, NU>;
@@ -583,48 +786,12 @@ struct Solver {
                                                          (o.keep_values || L == 1) ? val(b) : nullptr, pol(b));
           err = err ? err : e;
         }
-        // Chain nodes tail -> head; the next node's stage record and edge
-        // offset are prefetched into registers while this step computes.
-        if (L >= 2) {
-          __syncwarp(mask);
-          const double* s0 = stage(node_at(sq, L - 2));
-          for (int k = lane; k < SL::size; k += kTS) Fm[F::S + k] = s0[k];
-          if (lane < NX) Fm[F::c + lane] = w.defect[b * NX + lane];
-        }
+        // Chain nodes tail -> head.
         long long tc0 = 0;
         if (w.prof && threadIdx.x == 0) tc0 = clock64();
-        // Base pointers in registers: the step's generic stores could alias the
-        // shared-memory Work struct, which would force a reload every step.
-        const double* const stg = w.stage;
-        const double* const dfc = w.defect;
-        double* const vbase = w.value;
-        double* const pbase = w.policy;
-        for (int k = L - 2; k >= 0; --k) {
-          const int i = node_at(sq, k);
-          double pre[PRE];
-          double prec = 0.0;
-          if (k >= 1) {
-            const double* sp = stg + static_cast<size_t>(node_at(sq, k - 1)) * SL::stride;
-#pragma unroll
-            for (int j = 0; j < PRE; ++j) {
-              const int idx = lane + j * kTS;
-              pre[j] = idx < SL::size ? sp[idx] : 0.0;
-            }
-            if (lane < NX) prec = dfc[i * NX + lane];
-          }
-          double* const vi = (k == 0 || o.keep_values) ? vbase + static_cast<size_t>(i) * VL::stride : nullptr;
-          const int e = team_riccati_step_u<NX, NU, kTS>(reg, mask, Fm, lane, vi,
-                                                         pbase + static_cast<size_t>(i) * PL::stride);
+        if (L >= 2) {
+          const int e = team_chain<kTS>(sq, L - 2, 0, reg, lane, mask, Fm);
           err = err ? err : e;
-          if (k >= 1) {
-            __syncwarp(mask);
-#pragma unroll
-            for (int j = 0; j < PRE; ++j) {
-              const int idx = lane + j * kTS;
-              if (idx < SL::size) Fm[F::S + idx] = pre[j];
-            }
-            if (lane < NX) Fm[F::c + lane] = prec;
-          }
         }
         if (w.prof && threadIdx.x == 0 && L >= 2) {  // diagnostic: cycles per chain step
           g.sm->prof[12] += static_cast<double>(clock64() - tc0);
@@ -1445,12 +1612,12 @@ struct Solver {
           return;
         }
         double t0 = now_s();
-        int bad = 0;
+        int bad = 0, bad_code = kErrNone;
         mark(9);
-        const Eval ev = linearize_evaluate(&bad);
+        const Eval ev = linearize_evaluate(&bad, &bad_code);
         mark(0);
         if (bad) {
-          err_code = kErrLinearizeNonfinite;
+          err_code = bad_code;
           err_node = bad - 1;
           failed = true;
           break;

@@ -43,6 +43,7 @@ struct DevOptions {  // SolverOptions (solver.hpp:28-58), device copy
   int keep_values;  // 1: store (P, p) of every node (kernel-level API); 0: segment heads only
   int fwd_scan_min; // segments of >= this length take the forward prefix scan (0: walk everywhere)
   int nonlinear_ls; // 1: ForwardMode::nonlinear_rollout trials (sssilqr, solver.hpp:463-467)
+  int chunk_bwd;    // 1: blocks of >= 256 threads sweep long segments with the chunked scan
 };
 
 // Suspended solve() loop state (batch scheduling): a solve can stop at the top
@@ -70,6 +71,8 @@ enum ErrorCode : int {
   kErrLinearizeNonfinite = 4,
   kErrRolloutNonfinite = 5,  // nonlinear_rollout throws (uncaught in the reference)
   kErrAlphaLevels = 6,
+  kErrDefectNonfinite = 7,     // linearize: non-finite defect (solver.hpp:142-145)
+  kErrLinearizeTerminal = 8,   // linearize: non-finite terminal expansion (solver.hpp:102-105)
 };
 
 struct DevResult {  // SolveReport (solver.hpp:572-582) minus the records

@@ -76,11 +76,9 @@ cudaError_t launch_order_by_key(const DevResume* d_resume, int count, int* d_ord
   int npow2 = 1;
   while (npow2 < count) npow2 <<= 1;
   const size_t smem = static_cast<size_t>(npow2) * (sizeof(double) + sizeof(int));
-  static bool once = (cudaFuncSetAttribute(reinterpret_cast<const void*>(order_by_key_kernel),
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(kMaxSortCount * (sizeof(double) + sizeof(int)))),
-                      true);
-  (void)once;
+  // Per-device-context attribute: set before every launch (see allow_smem).
+  cudaFuncSetAttribute(reinterpret_cast<const void*>(order_by_key_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(kMaxSortCount * (sizeof(double) + sizeof(int))));
   order_by_key_kernel<<<1, 1024, smem, stream>>>(d_resume, count, npow2, d_order);
   return cudaGetLastError();
 }

@@ -22,8 +22,11 @@ def load(name):
     return d
 
 
+POPULATION = ("cfg4_population", "cfg3_early")  # compact population fixtures (tests/make_golden_batch.py)
+
+
 def scenario_names():
-    return [n for n in names() if not n.startswith(("lq", "preset_"))]
+    return [n for n in names() if not n.startswith(("lq", "preset_")) and n not in POPULATION]
 
 
 def preset_names():

@@ -52,9 +52,12 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(SO):
-            raise FileNotFoundError(f"{SO} missing: run `make -C oracle`")
-        _lib = C.CDLL(SO)
+        so = SO
+        if os.environ.get("BMPC_ORACLE_VARIANT") == "fma":  # rounding-sensitivity twin (oracle/Makefile)
+            so = SO.replace("libbmpc_oracle.so", "libbmpc_oracle_fma.so")
+        if not os.path.exists(so):
+            raise FileNotFoundError(f"{so} missing: run `make -C oracle`")
+        _lib = C.CDLL(so)
     return _lib
 
 
