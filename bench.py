@@ -115,6 +115,39 @@ def build_problems(B, rank, count):
     return [B.build_intersection_case(spec, 2, 2, perturb_seed=42 + rank * count + i) for i in range(count)]
 
 
+def host_info():
+    """Cores this process may run on (affinity / cgroup aware) and the CPU model."""
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return cores, model
+
+
+def ref_single_ms(family, horizon, branchings=(), parallel=1, caps=None, repeats=1):
+    """The reference's own single-solve time (SolveReport::times.total_s,
+    solver.hpp:563-570) of one scenario on this host; caps = (inner, outer)
+    bounds the run for per-pass timing of the largest trees."""
+    import _refbind as R
+
+    sc = R.scenario(family, horizon, total_time=10.0, shared=(0.1, 0.0), v=(2, 2), branchings=branchings)
+    o = R.default_options()
+    o.parallel = parallel
+    if caps:
+        o.max_inner_iterations, o.max_outer_iterations = caps
+    best, rep = None, None
+    for _ in range(repeats):
+        _, _, rep, _ = R.solve(sc, o, max_records=4000)
+        t = rep["times"][5]
+        best = t if best is None else min(best, t)
+    return 1e3 * best, rep["n_records"] + rep["outer_iterations"], rep
+
+
 def cpu_reference(sample, threads, seed0=42):
     """Reference CPU solver (oracle/_ref) over `sample` perturbed cfg0
     instances on `threads` host threads; returns (solves/s, seconds)."""
@@ -137,14 +170,17 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    sample = args.ref_sample or max(2 * threads, 32)
-    for _ in range(args.warmup):
-        cpu_reference(min(sample, threads), threads)
+    threads, model = host_info()
+    # Each step: a work-stealing pool of `threads` std::threads over `sample`
+    # distinct cfg4 instances (8 per thread, so one long solve does not decide
+    # the wall time); successive steps take successive slices of the 4096 seeds.
+    sample = args.ref_sample or 8 * threads
+    for w in range(args.warmup):
+        cpu_reference(threads, threads, seed0=42 + (w * threads) % PER_GPU)
     vals = []
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        v, _, _ = cpu_reference(sample, threads)
+    for k in range(args.steps):
+        v, _, _ = cpu_reference(sample, threads, seed0=42 + (k * sample) % PER_GPU)
         vals.append(v)
     wall = time.perf_counter() - t0
     v = float(np.median(vals))
@@ -153,9 +189,10 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference scenario builders, seeded perturbations)",
             "config": {"workload": WORKLOAD, "sample_instances_per_step": sample},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"{sample} perturbed cfg0 instances per step, solve() with parallel=false "
-                                       f"on {threads} std::threads"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference", "cpu": model,
+                             "sample": f"{sample} distinct perturbed cfg0 instances per step (successive slices of "
+                                       f"the 4096 bench seeds), reference solve() with parallel=false on a "
+                                       f"{threads}-thread work-stealing pool"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -267,7 +304,7 @@ def main():
         prof = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(prof):
             try:
-                traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+                traffic = json.load(open(prof)).get("dram_bytes_per_step")
             except Exception:
                 traffic = None
         line = {
@@ -291,23 +328,28 @@ def main():
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
                          "peak_source": "measured DFMA microbenchmark (bmpc_fp64_peak_tflops)",
+                         "traffic_source": "DRAM bytes read+written by every launch of one step, one ncu session "
+                                           "(profiles/traffic.json, tools/traffic.py)",
                          "kernel_ms": kernel_ms,
                          "algorithmic_flops_per_launch": flops_per_launch},
             "clocks": clocks.summary(),
         }
         if world == 1:
-            threads = os.cpu_count() or 1
-            sample = max(threads, 16)
+            threads, model = host_info()
+            sample = 256
             try:
                 v, secs, _ = cpu_reference(sample, threads)
+                serial_ms, _, _ = ref_single_ms(0, 63, parallel=0, repeats=3)
                 line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-                                        "sample": f"{sample} perturbed cfg0 instances, reference solve() "
-                                                  f"(parallel=false) on {threads} threads, {secs:.1f} s"}
+                                        "cpu": model, "serial_single_solve_ms": serial_ms,
+                                        "sample": f"{sample} perturbed cfg0 instances (seeds 42..{41 + sample}), "
+                                                  f"reference solve() (parallel=false) on a {threads}-thread "
+                                                  f"work-stealing pool, {secs:.1f} s wall"}
             except Exception as e:  # reference library absent
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                         "sample": f"unavailable: {e}"}
             if not args.no_latency:
-                line["latency_ms"] = latency_table(B, ctx)
+                line["latency_ms"] = latency_table(B, ctx, peak)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -319,22 +361,27 @@ def batch_bytes(n, nx, nu):
     return 8 * n * (nx + nu + 8 + 58 + nx + 12 + 2 * 56 + 2 * 20 + nx + nu + 20) * 1.0
 
 
-def latency_table(B, ctx):
-    """Single-solve device latency for configs 0, 1 (N sweep), 2 (scenario
-    sweep extremes), 3 (spread and early branchings): kernel time of the one
-    solve launch, inputs resident."""
+def latency_table(B, ctx, peak):
+    """Single-solve latency of configs 0-3 on the GPU (kernel time of the one
+    solve launch, inputs resident) next to the reference's own solve() on this
+    host (SolveReport total time, default options = its own std::async
+    parallelism), with each config's FP64 roofline fraction. The two cfg3
+    trees take the reference minutes per solve, so the reference runs a capped
+    solve there (3 inner passes, one outer) and the comparison is per pass."""
     import torch
-    cases = [("cfg0 N=63 4 leaves", B.intersection_spec(63, 10.0, 0.1), "int"),
-             ("cfg1 N=500 4 leaves", B.intersection_spec(500, 10.0, 0.1), "int"),
-             ("cfg1 N=1000 4 leaves", B.intersection_spec(1000, 10.0, 0.1), "int"),
-             ("cfg2 N=100 2 leaves {1}", B.multistage_spec(100, [(1, 2)]), "ms"),
-             ("cfg2 N=100 64 leaves {1,26,51}", B.multistage_spec(100, [(1, 4), (26, 4), (51, 4)]), "ms"),
-             ("cfg3 N=500 256 leaves {1,100,200,300}", B.multistage_spec(500, [(1, 4), (100, 4), (200, 4), (300, 4)]),
-              "ms"),
-             ("cfg3 N=500 256 leaves {1,2,3,4}", B.multistage_spec(500, [(1, 4), (2, 4), (3, 4), (4, 4)]), "ms")]
+    cases = [("cfg0 N=63 4 leaves", "int", 63, ()),
+             ("cfg1 N=500 4 leaves", "int", 500, ()),
+             ("cfg1 N=1000 4 leaves", "int", 1000, ()),
+             ("cfg2 N=100 2 leaves {1}", "ms", 100, ((1, 2),)),
+             ("cfg2 N=100 64 leaves {1,26,51}", "ms", 100, ((1, 4), (26, 4), (51, 4))),
+             ("cfg3 N=500 256 leaves {1,100,200,300}", "ms", 500, ((1, 4), (100, 4), (200, 4), (300, 4))),
+             ("cfg3 N=500 256 leaves {1,2,3,4}", "ms", 500, ((1, 4), (2, 4), (3, 4), (4, 4)))]
     out = {}
-    for name, spec, kind in cases:
-        p = B.build_intersection_case(spec, 2, 2) if kind == "int" else B.build_multistage_case(spec)
+    for name, kind, N, br in cases:
+        if kind == "int":
+            p = B.build_intersection_case(B.intersection_spec(N, 10.0, 0.1), 2, 2)
+        else:
+            p = B.build_multistage_case(B.multistage_spec(N, list(br)))
         bt = B.Batch(ctx, [p])
         bt.set_models()
         bt.solve()
@@ -346,8 +393,28 @@ def latency_table(B, ctx):
         e1.record(s)
         torch.cuda.synchronize()
         rep, _ = bt.results(want_reports=True)
-        out[name] = {"ms": e0.elapsed_time(e1), "nodes": p.tree.node_count, "status": rep[0].status_name,
-                     "inner": rep[0].inner_iterations, "outer": rep[0].outer_iterations}
+        r = rep[0]
+        ms = e0.elapsed_time(e1)
+        passes = r.n_records + r.outer_iterations
+        nl = int((p.tree.child_count > 0).sum())
+        row = {"ms": ms, "nodes": p.tree.node_count, "status": r.status_name, "inner": r.inner_iterations,
+               "outer": r.outer_iterations, "passes": passes, "us_per_pass": 1e3 * ms / passes}
+        # FP64 roofline: algorithmic flops per pass (SURVEY §8d constants, per evaluated step size).
+        flops = nl * (F_PASS * passes + F_ALPHA * r.alpha_evals)
+        row["roofline_frac"] = flops / (ms * 1e-3) / (peak * 1e12) if peak else None
+        try:
+            if name.startswith("cfg3"):
+                ref_ms, ref_passes, _ = ref_single_ms(2, N, br, caps=(3, 1))
+                row["reference_ms_per_pass"] = ref_ms / ref_passes
+                row["speedup_per_pass"] = (ref_ms / ref_passes) / row["us_per_pass"] * 1e3
+            else:
+                ref_ms, ref_passes, rr = ref_single_ms(0 if kind == "int" else 2, N, br)
+                row["reference_ms"] = ref_ms
+                row["reference_inner"] = rr["inner_iterations"]
+                row["speedup"] = ref_ms / ms
+        except Exception as e:  # reference library absent
+            row["reference_ms"] = f"unavailable: {e}"
+        out[name] = row
     return out
 
 
