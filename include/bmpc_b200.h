@@ -119,9 +119,12 @@ void bmpc_problem_data_free(bmpc_problem_data* data);
 /* -------------------------------------------------------- options/report */
 /* SolverOptions (solver.hpp:28-58). The strategy enums keep the reference's
  * numbering (solver.hpp:23-26); defaults are pmsilqr (all 0):
- *   backward    0 scan_tree_riccati, 1 scan_condensed (solved as 0: the same
- *               LQR subproblem), 2 sequential_riccati (team Riccati sweep on
- *               every segment);
+ *   backward    0 scan_tree_riccati, 1 scan_condensed (hypmsilqr: the shared
+ *               segment condensed into a dense QP over its inputs and solved
+ *               by Cholesky / pivoted LU on the device, open-loop policies
+ *               K = 0, k = u there, solver.hpp:297-307; at most 4096 stacked
+ *               shared inputs, else BMPC_ERR_UNSUPPORTED), 2 sequential_riccati
+ *               (team Riccati sweep on every segment);
  *   forward     0 linear_rollout, 1 nonlinear_rollout (single-shooting trials);
  *   line_search 0 parallel, 1 sequential (one step size per round; the
  *               accepted step is the same in both modes). */

@@ -16,11 +16,11 @@
 //     or any problem whose dynamics are affine and costs quadratic): the blocks
 //     are read back through the callbacks themselves at x = 0, u = 0.
 //
-// Strategy options: the GPU runs the north-star path (tree scan backward pass,
-// linear rollout, parallel line search). The backward strategies of the
-// reference solve the same LQR subproblem, so any `opts.backward` is accepted;
-// `nonlinear_rollout` / `sequential` line search are different algorithms and
-// are rejected with std::invalid_argument.
+// Strategy options: every backward strategy (tree scan, condensed shared
+// segment, sequential Riccati), forward mode (linear / nonlinear rollout) and
+// line-search mode (parallel / sequential) of SolverOptions runs on the GPU
+// with the reference's semantics; scan_order and parallel only schedule the
+// reference's CPU threads and are ignored.
 //
 // Errors follow the reference: a non-finite initial rollout throws
 // std::runtime_error (problem.hpp:160-162 throws out of solve); numerical

@@ -326,7 +326,8 @@ class SolverOptions:
     # Strategy enums (solver.hpp:23-33, JSON spellings of serialization.hpp:40-61),
     # all on the GPU: "scan-tree-riccati" = tree-segmented scan / team sweep per
     # segment length, "sequential-riccati" = team Riccati sweep on every
-    # segment, "scan-condensed" solved as the tree scan (same LQR subproblem);
+    # segment, "scan-condensed" = the shared segment condensed into a dense QP
+    # solved on the device (hypmsilqr, condensed.hpp / solver.hpp:297-307);
     # forward "nonlinear" = single-shooting trials (nonlinear rollout under the
     # feedback policies); line_search "sequential" = one step size per round.
     # scan_order / parallel only schedule the reference's CPU threads.

@@ -13,8 +13,8 @@ exit codes (2 on a bad config) and the same BMPC_OUT_DIR handling
 time. Every solve runs on the GPU through the C ABI; there is no CPU path.
 
 Strategy names: every preset runs on the GPU. "pmsilqr" is the tree scan;
-"hypmsilqr" (condensed shared segment) solves the same LQR subproblem on the
-same path; "smsilqr" runs the team Riccati sweep on every segment with the
+"hypmsilqr" condenses the shared segment into a dense QP over its inputs and
+solves it on the device (Cholesky, pivoted-LU fallback, condensed.hpp); "smsilqr" runs the team Riccati sweep on every segment with the
 sequential line search; "sssilqr" adds single-shooting trials (nonlinear
 rollout under the feedback policies, solver.hpp:463-467). `verify` runs the reference's
 oracle-equivalence suites against the GPU back end (paper_2506_13624_b200.verify).

@@ -551,6 +551,30 @@ std::unique_ptr<Plan> make_plan(const bmpc_tree& t, int max_con, bool has_constr
   tp.seg_depth = base + o_sd;
   tp.has_constraints = has_constraints ? 1 : 0;
   tp.max_con = std::max(max_con, 1);
+  // Shared segment (steps <= N_b) and boundary (the heads of the deepest
+  // segments, step N_b + 1) for the condensed strategy: BFS numbering makes
+  // them the index ranges [0, m) and [m, m + nb).
+  tp.n_shared = 0;
+  tp.n_bound = 0;
+  if (pl->ndepth >= 2) {
+    int m = 0;
+    for (int s2 = 0; s2 < pl->depth_begin[static_cast<size_t>(pl->ndepth) - 1]; ++s2)
+      m += pl->seg_off[static_cast<size_t>(s2) + 1] - pl->seg_off[static_cast<size_t>(s2)];
+    const int nb = pl->nseg - pl->depth_begin[static_cast<size_t>(pl->ndepth) - 1];
+    bool ok = true;
+    for (int s2 = 0; s2 < pl->nseg && ok; ++s2) {
+      const bool shared = pl->seg_depth[static_cast<size_t>(s2)] < pl->ndepth - 1;
+      for (int k = pl->seg_off[static_cast<size_t>(s2)]; k < pl->seg_off[static_cast<size_t>(s2) + 1]; ++k) {
+        const int i = pl->seg_nodes[static_cast<size_t>(k)];
+        const bool head = k == pl->seg_off[static_cast<size_t>(s2)];
+        if (shared ? i >= m : (head ? (i < m || i >= m + nb) : i < m + nb)) ok = false;
+      }
+    }
+    if (ok) {
+      tp.n_shared = m;
+      tp.n_bound = nb;
+    }
+  }
   pl->d_topo = DevBuf(sizeof(Topo));
   ck(cudaMemcpyAsync(pl->d_topo.p, &tp, sizeof(Topo), cudaMemcpyHostToDevice, s), "plan");
   ck(cudaStreamSynchronize(s), "plan sync");
@@ -715,6 +739,7 @@ struct bmpc_batch {
   int probe_threads{256}, probe_min_blocks{1}, main_budget{0}, fin_threads{256}, fin_min_blocks{1};
   bool grid_mode{false};
   int grid_blocks{0};
+  DevBuf cond;  // condensed-strategy scratch, allocated by the first scan_condensed solve
 };
 
 namespace {
@@ -1189,6 +1214,8 @@ static int batch_set_inputs(bmpc_batch* b, const double* initial_inputs) {
 // Sweep or scan per depth level (Solver::seq_depth): short segments, or many
 // long ones at one depth (the scan's work grows with them; tools/exp_seq.py).
 constexpr int kSeqWideSegs = 64, kSeqWideMax = 1024;
+// scan_condensed: largest dense QP (stacked shared inputs) the one-block solve takes.
+constexpr size_t kCondMaxInputs = 4096;
 static bool seq_depth_host(const Plan& pl, int d, int seq_max) {
   const int L = pl.depth_len[static_cast<size_t>(d)];
   const int ns = pl.depth_begin[static_cast<size_t>(d) + 1] - pl.depth_begin[static_cast<size_t>(d)];
@@ -1222,6 +1249,26 @@ static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_input
   if (o.backward < 0 || o.backward > 2 || o.forward < 0 || o.forward > 1 || o.line_search < 0 || o.line_search > 1)
     return fail(BMPC_ERR_INVALID, "unknown backward / forward / line_search strategy");
   if (o.backward == BMPC_BACKWARD_SEQUENTIAL_RICCATI) d.seq_max_len = 1 << 30;  // sweep every segment
+  if (o.backward == BMPC_BACKWARD_SCAN_CONDENSED && b->plan->topo.n_shared > 0) {
+    // Dense QP over the stacked shared inputs (condense_tree): H, a copy for
+    // the LU fallback / residual check, h, u, pivots, plus per-node records.
+    const Topo& tp = b->plan->topo;
+    const size_t n = static_cast<size_t>(tp.n_shared) * b->nu;
+    if (n > kCondMaxInputs)
+      return fail(BMPC_ERR_UNSUPPORTED, "scan_condensed: shared segment of " + std::to_string(n) +
+                                            " inputs exceeds the dense-solve limit " + std::to_string(kCondMaxInputs));
+    const size_t rec = (static_cast<size_t>(b->nx) * b->nx + b->nx) * 2 + b->nx + static_cast<size_t>(b->nx) * b->nu;
+    const size_t per = static_cast<size_t>(tp.n_shared + tp.n_bound) * ((rec + 1) & ~size_t{1}) + 2 * n * n + 4 * n + 2;
+    const size_t need = per * static_cast<size_t>(b->count) * sizeof(double);
+    if (b->cond.bytes < need) {
+      b->cond = DevBuf(need);
+      for (int i = 0; i < b->count; ++i) b->h_works[static_cast<size_t>(i)].cond = b->cond.as<double>() + per * i;
+      ck(cudaMemcpyAsync(b->works.p, b->h_works.data(), b->h_works.size() * sizeof(Work), cudaMemcpyHostToDevice,
+                         b->ctx->stream),
+         "works");
+    }
+    d.condensed = 1;
+  }
   if (o.line_search == BMPC_LINE_SEARCH_SEQUENTIAL) d.ls_block = 1;
   d.nonlinear_ls = o.forward == BMPC_FORWARD_NONLINEAR ? 1 : 0;
   cudaError_t e;

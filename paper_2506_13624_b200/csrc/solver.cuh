@@ -807,9 +807,337 @@ struct Solver {
   // (non-leaves) and P (leaves). Depth levels leaves-first; each level by the
   // team Riccati sweep (short segments) or the associative scan (long ones).
   // Returns error code and max_feedforward.
+  // ------------------------------------------- condensed P2 ("hypmsilqr")
+  // backward_pass with BackwardStrategy::scan_condensed (solver.hpp:297-307):
+  // P1 (the leaf segments, steps > N_b) as in the tree scan; the shared
+  // segment (nodes 0..m-1, steps <= N_b) is condensed against the P1 values at
+  // the boundary nodes (step N_b + 1) into one dense QP over the stacked
+  // shared inputs, min 1/2 u'Hu + h'u (condense_tree, condensed.hpp:205-279),
+  // solved by solve_dense (condensed.hpp:122-137: Cholesky, pivoted LU when
+  // H is not positive definite, residual bound 1e-9 (|H| |u| + |h|) else
+  // FactorizationError), and every shared node gets the open-loop policy
+  // K = 0, k = u (solver.hpp:301-307).
+  // H and h are formed on the tree instead of per root-to-boundary path: with
+  // z the zero-input perturbation (z_0 = dx0, z_ch = A z + d_ch), V_j the
+  // cost-to-go Hessian without control (V_b = P_b at the boundary,
+  // V_i = Q_i + A_i' (sum_ch V_ch) A_i), lam_j its gradient, and
+  // S_ba = dx_b / du_a = (A_{..} ... A_{a's child}) B_a for an ancestor a of b:
+  //   H_aa = R_a + B_a' Vs_a B_a,  H_ab = S_ba' (A_b' Vs_b B_b + M_b'),
+  //   h_a  = B_a' lams_a + M_a z_a + r_a,
+  // which is G' diag(H^p) G / G' stack(h^p) of condense_tree (the per-path
+  // split of the shared costs by multiplicity sums back to each cost once).
+  struct CondL {  // per-node scratch record of nodes [0, m + nb)
+    static constexpr int z = 0, V = NX, lam = V + NX * NX, Vs = lam + NX, lams = Vs + NX * NX, W = lams + NX,
+                         size = W + NX * NU, stride = (size + 1) & ~1;
+  };
+  __device__ double* crec(int i) const { return w.cond + static_cast<size_t>(i) * CondL::stride; }
+  __device__ int cond_n() const { return t.n_shared * NU; }
+  __device__ double* cH() const { return w.cond + static_cast<size_t>(t.n_shared + t.n_bound) * CondL::stride; }
+  __device__ double* cHc() const { return cH() + static_cast<size_t>(cond_n()) * cond_n(); }
+  __device__ double* ch() const { return cHc() + static_cast<size_t>(cond_n()) * cond_n(); }
+  __device__ double* cu() const { return ch() + cond_n(); }
+  __device__ double* cpiv() const { return cu() + cond_n(); }
+  __device__ double* cflag() const { return cpiv() + cond_n(); }
+
+  // Stage blocks of a non-leaf node (structured records: constants included).
+  __device__ void load_QRMqr(int i, double* Q, double* R, double* M, double* q, double* r) const {
+    const double* si = stage(i);
+    copy<NX * NX>(si + SL::Q, Q);
+    copy<NU * NU>(si + SL::R, R);
+    copy<NU * NX>(si + SL::M, M);
+    copy<NX>(si + SL::q, q);
+    copy<NU>(si + SL::r, r);
+  }
+
+  // solve_dense (condensed.hpp:122-137) over the whole group: u = -H^-1 h
+  // with H = cHc() (symmetric, both triangles). Eigen::LLT as a right-looking
+  // column Cholesky (each column: scale, then the trailing rank-1 update, one
+  // warp per trailing column so the column-major rows stream coalesced; the
+  // pivot sqrt is recomputed by every thread, so two group barriers per
+  // column), the two triangular solves with one barrier per column. A
+  // non-positive pivot (LLT info() != Success) falls back to
+  // Eigen::PartialPivLU on one block. Returns kBwdOk or kFactorization
+  // (non-finite u or residual |Hu + h| > 1e-9 (|H|_F |u| + |h|)); u in cu().
+  __device__ int dense_solve() {
+    const int n = cond_n();
+    double* H = cH();
+    double* Hc = cHc();
+    double* h = ch();
+    double* u = cu();
+    double* y = cpiv();  // forward-solve workspace (pivots in the LU fallback)
+    double* dg = cflag() + 2;  // [n] Cholesky diagonal
+    auto at = [n](double* A, int i, int j) -> double& { return A[i + static_cast<size_t>(j) * n]; };
+    const int rank = g.rank(), size = g.size();
+    const int gw = rank >> 5, nw = size >> 5, lane = threadIdx.x & 31;
+    for (int k = rank; k < n * n; k += size) H[k] = Hc[k];
+    for (int k = rank; k < n; k += size) u[k] = -h[k];
+    g.sync();
+    bool llt_ok = true;
+    for (int k = 0; k < n; ++k) {
+      const double d = at(H, k, k);
+      if (!(d > 0.0)) {
+        llt_ok = false;  // every thread reads the same value: a uniform exit
+        break;
+      }
+      const double lkk = sqrt(d);
+      if (rank == 0) dg[k] = lkk;
+      for (int i = k + 1 + rank; i < n; i += size) at(H, i, k) /= lkk;
+      g.sync();
+      for (int j = k + 1 + gw; j < n; j += nw) {
+        const double ljk = at(H, j, k);
+        for (int i = j + lane; i < n; i += 32) at(H, i, j) = fma(-at(H, i, k), ljk, at(H, i, j));
+      }
+      g.sync();
+    }
+    if (llt_ok) {
+      for (int k = 0; k < n; ++k) {  // L y = -h
+        const double yk = u[k] / dg[k];
+        if (rank == 0) y[k] = yk;
+        for (int i = k + 1 + rank; i < n; i += size) u[i] = fma(-at(H, i, k), yk, u[i]);
+        g.sync();
+      }
+      for (int k = n - 1; k >= 0; --k) {  // L' u = y
+        const double xk = y[k] / dg[k];
+        if (rank == 0) u[k] = xk;
+        for (int i = rank; i < k; i += size) y[i] = fma(-at(H, k, i), xk, y[i]);
+        g.sync();
+      }
+    } else if (g.block() == 0) {
+      // Eigen::PartialPivLU of the original H, one block.
+      const int tid = threadIdx.x, nt = blockDim.x;
+      double* piv = y;
+      for (int k = tid; k < n * n; k += nt) H[k] = Hc[k];
+      for (int k = tid; k < n; k += nt) u[k] = -h[k];
+      __syncthreads();
+      for (int k = 0; k < n; ++k) {
+        if (tid == 0) {
+          int p = k;
+          double best = fabs(at(H, k, k));
+          for (int i = k + 1; i < n; ++i) {
+            const double v = fabs(at(H, i, k));
+            if (v > best) best = v, p = i;
+          }
+          piv[k] = p;
+        }
+        __syncthreads();
+        const int p = static_cast<int>(piv[k]);
+        if (p != k)
+          for (int j = tid; j < n; j += nt) {
+            const double a = at(H, k, j);
+            at(H, k, j) = at(H, p, j);
+            at(H, p, j) = a;
+          }
+        __syncthreads();
+        const double ukk = at(H, k, k);
+        if (ukk != 0.0)
+          for (int i = k + 1 + tid; i < n; i += nt) at(H, i, k) /= ukk;
+        __syncthreads();
+        for (int j = k + 1 + (tid >> 5); j < n; j += nt >> 5) {
+          const double ukj = at(H, k, j);
+          for (int i = k + 1 + lane; i < n; i += 32) at(H, i, j) = fma(-at(H, i, k), ukj, at(H, i, j));
+        }
+        __syncthreads();
+      }
+      if (tid == 0)
+        for (int k = 0; k < n; ++k) {
+          const int p = static_cast<int>(piv[k]);
+          const double a = u[k];
+          u[k] = u[p];
+          u[p] = a;
+        }
+      __syncthreads();
+      for (int k = 0; k < n; ++k) {  // unit-lower L
+        const double yk = u[k];
+        for (int i = k + 1 + tid; i < n; i += nt) u[i] = fma(-at(H, i, k), yk, u[i]);
+        __syncthreads();
+      }
+      for (int k = n - 1; k >= 0; --k) {
+        if (tid == 0) u[k] /= at(H, k, k);
+        __syncthreads();
+        const double xk = u[k];
+        for (int i = tid; i < k; i += nt) u[i] = fma(-at(H, i, k), xk, u[i]);
+        __syncthreads();
+      }
+    }
+    g.sync();
+    // Residual bound (condensed.hpp:128-135); 2-norms, Frobenius |H|.
+    double r2 = 0.0, H2 = 0.0, u2 = 0.0, h2 = 0.0, bad = 0.0;
+    for (int i = rank; i < n; i += size) {
+      double ri = h[i];
+      for (int j = 0; j < n; ++j) {
+        const double hij = at(Hc, i, j);
+        ri = fma(hij, u[j], ri);
+        H2 = fma(hij, hij, H2);
+      }
+      r2 = fma(ri, ri, r2);
+      u2 = fma(u[i], u[i], u2);
+      h2 = fma(h[i], h[i], h2);
+      if (!isfinite(u[i])) bad = 1.0;
+    }
+    red_put(g, 0, r2, true);
+    red_put(g, 1, H2, true);
+    red_put(g, 2, u2, true);
+    red_put(g, 3, h2, true);
+    red_put(g, 4, bad, false);
+    g.finish(5, 4);
+    const double bound = 1e-9 * (sqrt(g.sm->total[1]) * sqrt(g.sm->total[2]) + sqrt(g.sm->total[3]));
+    return (g.sm->total[4] > 0.0 || !(sqrt(g.sm->total[0]) <= bound)) ? kFactorization : kBwdOk;
+  }
+
+  __device__ int condensed_p2(double reg) {
+    const int m = t.n_shared, nb = t.n_bound, n = cond_n();
+    const int D = t.ndepth;
+    double* H = cHc();
+    double* h = ch();
+    for (int k = g.rank(); k < n * n; k += g.size()) H[k] = 0.0;
+    // (1) zero-input perturbations z, depth by depth (the boundary: heads of depth D-1).
+    for (int d = 0; d < D; ++d) {
+      const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
+      const int L = d == D - 1 ? 1 : t.depth_len[d];
+      for (int sg = sb + g.rank(); sg < se; sg += g.size()) {
+        const SegIdx sq = seg_idx(sg);
+        double z[NX];
+        const int hd = sq.head, p = t.parent[hd];
+        if (p < 0) {
+#pragma unroll
+          for (int j = 0; j < NX; ++j) z[j] = w.x0[j] - w.x[j];
+        } else {
+          double A[NX * NX], Bm[NX * NU], t1[NX];
+          load_AB(p, A, Bm);
+          mv<NX, NX>(A, crec(p) + CondL::z, t1);
+#pragma unroll
+          for (int j = 0; j < NX; ++j) z[j] = t1[j] + w.defect[hd * NX + j];
+        }
+        copy<NX>(z, crec(hd) + CondL::z);
+        for (int k = 1; k < L; ++k) {
+          const int prev = node_at(sq, k - 1), i = node_at(sq, k);
+          double A[NX * NX], Bm[NX * NU], t1[NX];
+          load_AB(prev, A, Bm);
+          mv<NX, NX>(A, z, t1);
+#pragma unroll
+          for (int j = 0; j < NX; ++j) z[j] = t1[j] + w.defect[i * NX + j];
+          copy<NX>(z, crec(i) + CondL::z);
+        }
+      }
+      g.sync();
+    }
+    // (2) boundary values V_b = P_b, lam_b = p_b + P_b z_b (P1 results).
+    for (int b = m + g.rank(); b < m + nb; b += g.size()) {
+      const double* v = value_ptr(b);
+      double* c = crec(b);
+      double Pz[NX];
+      mv<NX, NX>(v, c + CondL::z, Pz);
+      copy<NX * NX>(v, c + CondL::V);
+#pragma unroll
+      for (int j = 0; j < NX; ++j) c[CondL::lam + j] = v[NX * NX + j] + Pz[j];
+    }
+    g.sync();
+    // (3) shared nodes, leaves-first: Vs, lams, V, lam, W; diagonal blocks of H and h.
+    for (int d = D - 2; d >= 0; --d) {
+      const int sb = t.depth_begin[d], se = t.depth_begin[d + 1], L = t.depth_len[d];
+      for (int sg = sb + g.rank(); sg < se; sg += g.size()) {
+        const SegIdx sq = seg_idx(sg);
+        for (int k = L - 1; k >= 0; --k) {
+          const int i = node_at(sq, k);
+          double* c = crec(i);
+          double Vs[NX * NX], ls[NX];
+#pragma unroll
+          for (int q = 0; q < NX * NX; ++q) Vs[q] = 0.0;
+#pragma unroll
+          for (int q = 0; q < NX; ++q) ls[q] = 0.0;
+          const int c0 = t.first_child[i], nc = t.nchild[i];
+          for (int ch = c0; ch < c0 + nc; ++ch) {  // children in index order
+            const double* cc = crec(ch);
+#pragma unroll
+            for (int q = 0; q < NX * NX; ++q) Vs[q] += cc[CondL::V + q];
+#pragma unroll
+            for (int q = 0; q < NX; ++q) ls[q] += cc[CondL::lam + q];
+          }
+          double A[NX * NX], Bm[NX * NU], Q[NX * NX], R[NU * NU], M[NU * NX], q[NX], r[NU];
+          load_AB(i, A, Bm);
+          load_QRMqr(i, Q, R, M, q, r);
+          double AtV[NX * NX], V[NX * NX], BtV[NU * NX], Hd[NU * NU], W[NX * NU], t1[NX], t2[NU], t3[NU];
+          mtm<NX, NX, NX>(A, Vs, AtV);
+          mm<NX, NX, NX>(AtV, A, V);
+#pragma unroll
+          for (int e = 0; e < NX * NX; ++e) V[e] += Q[e];
+          symmetrize<NX>(V);
+          mm<NX, NX, NU>(AtV, Bm, W);
+#pragma unroll
+          for (int a = 0; a < NU; ++a)
+#pragma unroll
+            for (int j = 0; j < NX; ++j) W[j + a * NX] += M[a + j * NU];
+          mtm<NU, NX, NX>(Bm, Vs, BtV);
+          mm<NU, NX, NU>(BtV, Bm, Hd);
+#pragma unroll
+          for (int e = 0; e < NU * NU; ++e) Hd[e] += R[e];
+#pragma unroll
+          for (int a = 0; a < NU; ++a) Hd[a + a * NU] += reg;  // regularized R (solver.hpp:212-222)
+          symmetrize<NU>(Hd);
+          // lam = q + Q z + A' lams ; h_i = B' lams + M z + r
+          mv<NX, NX>(Q, c + CondL::z, t1);
+          double Atl[NX];
+          mtv<NX, NX>(A, ls, Atl);
+#pragma unroll
+          for (int j = 0; j < NX; ++j) c[CondL::lam + j] = (q[j] + t1[j]) + Atl[j];
+          mtv<NU, NX>(Bm, ls, t2);
+          mv<NU, NX>(M, c + CondL::z, t3);
+#pragma unroll
+          for (int a = 0; a < NU; ++a) h[i * NU + a] = (t2[a] + t3[a]) + r[a];
+          copy<NX * NX>(V, c + CondL::V);
+          copy<NX * NU>(W, c + CondL::W);
+#pragma unroll
+          for (int a = 0; a < NU; ++a)
+#pragma unroll
+            for (int b2 = 0; b2 < NU; ++b2) H[(i * NU + a) + static_cast<size_t>(i * NU + b2) * n] = Hd[a + b2 * NU];
+        }
+      }
+      g.sync();
+    }
+    // (4) off-diagonal blocks: every shared node b against each ancestor a.
+    for (int b = 1 + g.rank(); b < m; b += g.size()) {
+      const double* W = crec(b) + CondL::W;
+      double T[NX * NX];
+#pragma unroll
+      for (int q = 0; q < NX * NX; ++q) T[q] = (q % (NX + 1)) == 0 ? 1.0 : 0.0;
+      for (int y = b, a = t.parent[b]; a >= 0; y = a, a = t.parent[a]) {
+        double A[NX * NX], Bm[NX * NU], S[NX * NU], Hab[NU * NU], T2[NX * NX];
+        load_AB(a, A, Bm);
+        mm<NX, NX, NU>(T, Bm, S);    // dx_b / du_a
+        mtm<NU, NX, NU>(S, W, Hab);  // (a, b) block
+#pragma unroll
+        for (int r = 0; r < NU; ++r)
+#pragma unroll
+          for (int c2 = 0; c2 < NU; ++c2) {
+            H[(a * NU + r) + static_cast<size_t>(b * NU + c2) * n] = Hab[r + c2 * NU];
+            H[(b * NU + c2) + static_cast<size_t>(a * NU + r) * n] = Hab[r + c2 * NU];
+          }
+        mm<NX, NX, NX>(T, A, T2);
+        copy<NX * NX>(T2, T);
+      }
+    }
+    g.sync();
+    // (5) solve_dense.
+    const int err = dense_solve();
+    // (6) open-loop policies of the shared nodes.
+    if (err == kBwdOk) {
+      const double* u = cu();
+      for (int i = g.rank(); i < m; i += g.size()) {
+#pragma unroll
+        for (int q = 0; q < NU * NX; ++q) pol(i)[PL::K + q] = 0.0;
+#pragma unroll
+        for (int a = 0; a < NU; ++a) pol(i)[PL::k + a] = u[i * NU + a];
+      }
+    }
+    g.sync();
+    return err;
+  }
+
   __device__ int backward(double reg, double* max_ff) {
     int err = kBwdOk;
-    for (int d = t.ndepth - 1; d >= 0; --d) {
+    // Condensed strategy: only the leaf segments (P1) take the tree scan.
+    const bool condensed = o.condensed && t.n_shared > 0;
+    for (int d = t.ndepth - 1; d >= (condensed ? t.ndepth - 1 : 0); --d) {
       const int L = t.depth_len[d];
       if (seq_depth(d)) {
         const int e = riccati_sweep_depth(d, reg);
@@ -867,6 +1195,10 @@ struct Solver {
       err = err ? err : e;
       }
     }
+    if (condensed && err == kBwdOk) {
+      g.sync();
+      err = condensed_p2(reg);
+    }
     // Policies of scanned chain nodes from their successor's value
     // (feedback_from_values, lqr_scan.hpp:146); max_feedforward.
     double mff = 0.0;
@@ -874,7 +1206,7 @@ struct Solver {
       if (is_leaf(i)) continue;
       const int s = t.node_seg[i], k = t.node_pos[i];
       if constexpr (!kSeqOnly) {
-        if (!seq_seg(s) && k + 1 < seg_len(s)) {
+        if (!seq_seg(s) && k + 1 < seg_len(s) && !(condensed && i < t.n_shared)) {
           const int nxt = seg_node(s, k + 1);
           const double* v = value_of(nxt);
           const int e = feedback<NX, NU>(stage(i), reg, w.defect + nxt * NX, v + BL::P, v + BL::p,

@@ -44,6 +44,7 @@ struct DevOptions {  // SolverOptions (solver.hpp:28-58), device copy
   int fwd_scan_min; // segments of >= this length take the forward prefix scan (0: walk everywhere)
   int nonlinear_ls; // 1: ForwardMode::nonlinear_rollout trials (sssilqr, solver.hpp:463-467)
   int chunk_bwd;    // 1: blocks of >= 256 threads sweep long segments with the chunked scan
+  int condensed;    // 1: BackwardStrategy::scan_condensed (hypmsilqr): P2 by condensing + dense solve
 };
 
 // Suspended solve() loop state (batch scheduling): a solve can stop at the top
@@ -103,6 +104,8 @@ struct Topo {
   const int* seg_depth;      // [nseg] depth level of each segment
   int has_constraints;
   int max_con;               // constraint rows stored per node (eta stride)
+  int n_shared;              // nodes 0..n_shared-1 have step <= N_b (the shared segment), 0 for a path
+  int n_bound;               // boundary nodes n_shared.. (step N_b + 1: heads of the deepest segments)
 };
 
 // Per-instance device state (layout strides depend on NX, NU; see lqr.cuh).
@@ -124,6 +127,7 @@ struct Work {
   DevResult* result;
   double* prof;  // optional [kProfSlots] per-phase device time (ns), leader-accumulated
   DevResume* resume;  // optional suspend / resume state
+  double* cond;       // condensed strategy scratch (per-node records, H, H copy, h, u, pivots), else null
 };
 
 }  // namespace bmpc_b200
