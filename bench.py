@@ -110,11 +110,6 @@ def dist_env():
     return rank, world, local
 
 
-def build_problems(B, rank, count):
-    spec = B.intersection_spec(63, 10.0, 0.1)
-    return [B.build_intersection_case(spec, 2, 2, perturb_seed=42 + rank * count + i) for i in range(count)]
-
-
 def host_info():
     """Cores this process may run on (affinity / cgroup aware) and the CPU model."""
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
@@ -215,14 +210,18 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = B.Context(local, stream=stream.cuda_stream)
+    from paper_2506_13624_b200.sharding import ShardedBatch
+
     count = args.instances
-    probs = build_problems(B, rank, count)
-    batch = B.Batch(ctx, probs)
+    spec = B.intersection_spec(63, 10.0, 0.1)
+    # This rank's contiguous shard of the job's world * count instances
+    # (bmpc_shard_range): seeds 42 + global index.
+    sharded = ShardedBatch(ctx, lambda b, k: [B.build_intersection_case(spec, 2, 2, perturb_seed=42 + b + i)
+                                              for i in range(k)], world * count, world, rank)
+    batch, probs = sharded.batch, sharded.problems
     n, nx, nu = batch.n, batch.nx, batch.nu
     h2d_setup = batch.set_models()
     torch.cuda.synchronize()
-    gather_buf = torch.empty(count * n * (nx + nu), dtype=torch.float64, device="cuda") if world > 1 else None
-    recv = [torch.empty_like(gather_buf) for _ in range(world)] if (world > 1 and rank == 0) else None
 
     def barrier():
         if world > 1:
@@ -231,8 +230,7 @@ def main():
     def step():
         batch.solve()
         if world > 1:  # final gather of every trajectory to rank 0 over NVLink
-            batch.pack_results(gather_buf.data_ptr())
-            dist.gather(gather_buf, recv, dst=0)
+            sharded.gather(device="cuda")
 
     for _ in range(args.warmup):
         step()
@@ -249,8 +247,7 @@ def main():
             batch.solve()
             kev[s][1].record(stream)
             if world > 1:
-                batch.pack_results(gather_buf.data_ptr())
-                dist.gather(gather_buf, recv, dst=0)
+                sharded.gather(device="cuda")
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = ctx.launches - launches0

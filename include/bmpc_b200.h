@@ -242,6 +242,39 @@ int bmpc_batch_records(bmpc_batch* batch, int instance, bmpc_record* records, in
 /* Kernel launches the batch solve issues (1) and the launch configuration. */
 int bmpc_batch_info(const bmpc_batch* batch, int* threads_per_block, int* blocks, int* regs_per_thread);
 
+/* ------------------------------------------- multi-device batched solves */
+/* The reference's batched throughput path is a thread pool of independent
+ * solve() calls (parallel_sweep, tools/bench.cpp:259-269). Here the instance
+ * space is split into contiguous shards, one per ctx (device):
+ * shard g = [g*count/n, (g+1)*count/n). No data-path collective: each device
+ * solves its shard with its own launches; the only exchange is the final
+ * gather of the packed trajectories to the first ctx's device. */
+int bmpc_shard_range(int count, int n_shards, int g, int* begin, int* n);
+typedef struct bmpc_multi bmpc_multi;
+/* ctxs[n_ctx] (several ctxs may share a device); the template as in
+ * bmpc_batch_create. */
+int bmpc_multi_create(bmpc_ctx* const* ctxs, int n_ctx, const bmpc_tree* tree, int count,
+                      const bmpc_model_desc* model_template, int max_records, bmpc_multi** out);
+void bmpc_multi_destroy(bmpc_multi* multi);
+int bmpc_multi_set_models(bmpc_multi* multi, const bmpc_model_desc* models, size_t* h2d_bytes);
+int bmpc_multi_set_initial_states(bmpc_multi* multi, const double* x0, size_t* h2d_bytes);
+/* Launches every shard's solve, asynchronously on each ctx's stream. */
+int bmpc_multi_solve(bmpc_multi* multi, const bmpc_options* opts);
+/* Final gather: d_dst is device memory on ctxs[0]'s device holding
+ * count * node * (nx + nu) doubles ([x | u] per instance, global order).
+ * Each shard's pack kernel stores its instances straight into d_dst over
+ * peer-to-peer (NVLink/NVSwitch) mappings; devices that cannot map device 0
+ * pack locally and copy peer-to-peer. Synchronizes every shard. */
+int bmpc_multi_gather(bmpc_multi* multi, double* d_dst, size_t* bytes);
+/* Host results in global instance order (as bmpc_batch_results). */
+int bmpc_multi_results(bmpc_multi* multi, double* x_out, double* u_out, bmpc_report* reports, size_t* d2h_bytes);
+/* Shard g's batch (borrowed; NULL for an empty shard) and its range. */
+int bmpc_multi_shard(bmpc_multi* multi, int g, bmpc_batch** batch, int* begin, int* n);
+/* One-shot: create + set_models + solve + results + destroy. */
+int bmpc_solve_batch(bmpc_ctx* const* ctxs, int n_ctx, const bmpc_tree* tree, int count,
+                     const bmpc_model_desc* models, const bmpc_options* opts, double* x_out, double* u_out,
+                     bmpc_report* reports);
+
 /* Measured FP64 FMA throughput of this device (TFLOP/s): the roofline
  * denominator of the FP64-bound solve path. */
 int bmpc_fp64_peak_tflops(bmpc_ctx* ctx, double* tflops);

@@ -538,6 +538,77 @@ class Batch:
             self._h = None
 
 
+def shard_range(count: int, n_shards: int, g: int) -> tuple:
+    """Contiguous shard g of `count` instances over n_shards devices / ranks:
+    [g*count/n, (g+1)*count/n) (bmpc_shard_range; host-only, no GPU needed)."""
+    b, n = C.c_int(), C.c_int()
+    _check(lib().bmpc_shard_range(int(count), int(n_shards), int(g), C.byref(b), C.byref(n)))
+    return b.value, n.value
+
+
+class MultiBatch:
+    """Independent instances sharded contiguously over several contexts
+    (devices) of ONE process (bmpc_multi_*): each device solves its shard with
+    its own launches, concurrently; the final gather packs every shard's
+    trajectories straight into one buffer on the first context's device over
+    peer-to-peer (NVLink). The reference's analogue is the thread pool of
+    independent solve() calls, parallel_sweep (tools/bench.cpp:259-269)."""
+
+    def __init__(self, ctxs: Sequence[Context], problems: Sequence[BmpcProblem], max_records: int = 0):
+        self.ctxs = list(ctxs)
+        self.count = len(problems)
+        self.problems = list(problems)
+        p0 = problems[0]
+        self.n, self.nx, self.nu = p0.tree.node_count, p0.state_dim, p0.input_dim
+        arr = (C.c_void_p * len(self.ctxs))(*[c._h.value for c in self.ctxs])
+        h = C.c_void_p()
+        _check(lib().bmpc_multi_create(arr, len(self.ctxs), p0.tree._h, self.count, C.byref(p0.model),
+                                       int(max_records), C.byref(h)))
+        self._h = h
+        self._models = (_Model * self.count)(*[p.model for p in problems])
+
+    def set_models(self) -> int:
+        b = C.c_size_t()
+        _check(lib().bmpc_multi_set_models(self._h, self._models, C.byref(b)))
+        return b.value
+
+    def set_initial_states(self, x0: np.ndarray) -> int:
+        x0 = np.ascontiguousarray(x0, dtype=np.float64).reshape(self.count, self.nx)
+        b = C.c_size_t()
+        _check(lib().bmpc_multi_set_initial_states(self._h, _ptr(x0), C.byref(b)))
+        return b.value
+
+    def solve(self, options: Optional[SolverOptions] = None):
+        opts = (options or SolverOptions())._c()
+        _check(lib().bmpc_multi_solve(self._h, C.byref(opts)))
+
+    def gather(self, d_dst_ptr: int) -> int:
+        """Pack every shard's [x | u] into the device buffer d_dst_ptr on the
+        first context's device (count * n * (nx + nu) doubles); returns bytes."""
+        b = C.c_size_t()
+        _check(lib().bmpc_multi_gather(self._h, C.c_void_p(d_dst_ptr), C.byref(b)))
+        return b.value
+
+    def results(self, x: Optional[np.ndarray] = None, u: Optional[np.ndarray] = None):
+        for name, a, shape in (("x", x, (self.count, self.n, self.nx)), ("u", u, (self.count, self.n, self.nu))):
+            if a is not None and (a.dtype != np.float64 or a.shape != shape or not a.flags.c_contiguous):
+                raise ValueError(f"{name} must be a C-contiguous float64 array of shape {shape}")
+        reps = (_Report * self.count)()
+        b = C.c_size_t()
+        _check(lib().bmpc_multi_results(self._h, _ptr(x), _ptr(u), reps, C.byref(b)))
+        return [_report(r) for r in reps], b.value
+
+    def shard(self, g: int) -> tuple:
+        begin, n = C.c_int(), C.c_int()
+        _check(lib().bmpc_multi_shard(self._h, int(g), None, C.byref(begin), C.byref(n)))
+        return begin.value, n.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib_handle is not None:
+            _lib_handle.bmpc_multi_destroy(self._h)
+            self._h = None
+
+
 def lqr_tree(tree: TreeTopology, nx: int, nu: int, stage: np.ndarray, defect: np.ndarray, leaf: np.ndarray,
              reg: float = 0.0, dx0: Optional[np.ndarray] = None, grid: bool = False,
              ctx: Optional[Context] = None) -> dict:

@@ -1380,6 +1380,174 @@ int bmpc_batch_pack_results(bmpc_batch* b, double* d_dst, size_t* bytes) {
   return BMPC_OK;
 }
 
+// ------------------------------------------------ multi-device batches
+struct bmpc_multi {
+  std::vector<bmpc_ctx*> ctxs;
+  std::vector<bmpc_batch*> shards;  // nullptr for an empty shard
+  std::vector<int> begin, cnt;
+  int count{0}, n{0}, nx{0}, nu{0};
+  ~bmpc_multi() {
+    for (bmpc_batch* b : shards)
+      if (b) bmpc_batch_destroy(b);
+  }
+};
+
+int bmpc_shard_range(int count, int n_shards, int g, int* begin, int* n) {
+  if (count < 0 || n_shards < 1 || g < 0 || g >= n_shards || !begin || !n) return fail(BMPC_ERR_INVALID, "bad shard");
+  const long long b0 = static_cast<long long>(g) * count / n_shards;
+  const long long b1 = static_cast<long long>(g + 1) * count / n_shards;
+  *begin = static_cast<int>(b0);
+  *n = static_cast<int>(b1 - b0);
+  return BMPC_OK;
+}
+
+int bmpc_multi_create(bmpc_ctx* const* ctxs, int n_ctx, const bmpc_tree* tree, int count,
+                      const bmpc_model_desc* tmpl, int max_records, bmpc_multi** out) {
+  if (!ctxs || n_ctx < 1 || !tree || !tmpl || !out || count < 1) return fail(BMPC_ERR_INVALID, "bad multi arguments");
+  auto m = std::make_unique<bmpc_multi>();
+  m->count = count;
+  m->n = tree->node_count;
+  m->nx = tmpl->state_dim;
+  m->nu = tmpl->input_dim;
+  for (int g = 0; g < n_ctx; ++g) {
+    if (!ctxs[g]) return fail(BMPC_ERR_INVALID, "null ctx");
+    int b0 = 0, c = 0;
+    bmpc_shard_range(count, n_ctx, g, &b0, &c);
+    bmpc_batch* b = nullptr;
+    if (c > 0) {
+      const int rc = bmpc_batch_create(ctxs[g], tree, c, tmpl, max_records, &b);
+      if (rc != BMPC_OK) return rc;
+    }
+    m->ctxs.push_back(ctxs[g]);
+    m->shards.push_back(b);
+    m->begin.push_back(b0);
+    m->cnt.push_back(c);
+  }
+  *out = m.release();
+  return BMPC_OK;
+}
+
+void bmpc_multi_destroy(bmpc_multi* m) { delete m; }
+
+int bmpc_multi_set_models(bmpc_multi* m, const bmpc_model_desc* models, size_t* h2d_bytes) {
+  if (!m || !models) return fail(BMPC_ERR_INVALID, "null argument");
+  size_t tot = 0;
+  for (size_t g = 0; g < m->shards.size(); ++g) {
+    if (!m->shards[g]) continue;
+    size_t b = 0;
+    const int rc = bmpc_batch_set_models(m->shards[g], models + m->begin[g], &b);
+    if (rc != BMPC_OK) return rc;
+    tot += b;
+  }
+  if (h2d_bytes) *h2d_bytes = tot;
+  return BMPC_OK;
+}
+
+int bmpc_multi_set_initial_states(bmpc_multi* m, const double* x0, size_t* h2d_bytes) {
+  if (!m || !x0) return fail(BMPC_ERR_INVALID, "null argument");
+  size_t tot = 0;
+  for (size_t g = 0; g < m->shards.size(); ++g) {
+    if (!m->shards[g]) continue;
+    size_t b = 0;
+    const int rc =
+        bmpc_batch_set_initial_states(m->shards[g], x0 + static_cast<size_t>(m->begin[g]) * m->nx, &b);
+    if (rc != BMPC_OK) return rc;
+    tot += b;
+  }
+  if (h2d_bytes) *h2d_bytes = tot;
+  return BMPC_OK;
+}
+
+int bmpc_multi_solve(bmpc_multi* m, const bmpc_options* opts) {
+  if (!m) return fail(BMPC_ERR_INVALID, "null argument");
+  for (bmpc_batch* b : m->shards) {  // asynchronous: every device runs its shard concurrently
+    if (!b) continue;
+    const int rc = bmpc_batch_solve(b, opts);
+    if (rc != BMPC_OK) return rc;
+  }
+  return BMPC_OK;
+}
+
+int bmpc_multi_gather(bmpc_multi* m, double* d_dst, size_t* bytes) {
+  try {
+    if (!m || !d_dst) return fail(BMPC_ERR_INVALID, "null argument");
+    const int dev0 = m->ctxs[0]->device;
+    const size_t per = static_cast<size_t>(m->n) * (m->nx + m->nu);
+    for (size_t g = 0; g < m->shards.size(); ++g) {
+      bmpc_batch* b = m->shards[g];
+      if (!b) continue;
+      const int dev = m->ctxs[g]->device;
+      double* dst = d_dst + static_cast<size_t>(m->begin[g]) * per;
+      ck(cudaSetDevice(dev), "cudaSetDevice");
+      int can = dev == dev0 ? 1 : 0;
+      if (dev != dev0) {
+        ck(cudaDeviceCanAccessPeer(&can, dev, dev0), "peer query");
+        if (can) {
+          const cudaError_t e = cudaDeviceEnablePeerAccess(dev0, 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+          else if (e != cudaSuccess) can = 0, cudaGetLastError();
+        }
+      }
+      if (can) {  // the pack kernel's stores land in device 0's buffer (NVLink P2P)
+        ck(launch_pack_results(b->works.as<Work>(), b->count, b->plan->n, b->nx, b->nu, dst, b->ctx->stream), "pack");
+      } else {
+        if (!b->d_pack.p) b->d_pack = DevBuf(static_cast<size_t>(b->count) * per * sizeof(double));
+        ck(launch_pack_results(b->works.as<Work>(), b->count, b->plan->n, b->nx, b->nu, b->d_pack.as<double>(),
+                               b->ctx->stream),
+           "pack");
+        ck(cudaMemcpyPeerAsync(dst, dev0, b->d_pack.p, dev, static_cast<size_t>(b->count) * per * sizeof(double),
+                               b->ctx->stream),
+           "peer copy");
+      }
+      ++b->ctx->launches;
+    }
+    for (size_t g = 0; g < m->shards.size(); ++g)
+      if (m->shards[g]) ck(cudaStreamSynchronize(m->ctxs[g]->stream), "sync");
+    if (bytes) *bytes = static_cast<size_t>(m->count) * per * sizeof(double);
+    return BMPC_OK;
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
+}
+
+int bmpc_multi_results(bmpc_multi* m, double* x_out, double* u_out, bmpc_report* reports, size_t* d2h_bytes) {
+  if (!m) return fail(BMPC_ERR_INVALID, "null argument");
+  size_t tot = 0;
+  for (size_t g = 0; g < m->shards.size(); ++g) {
+    if (!m->shards[g]) continue;
+    const size_t b0 = static_cast<size_t>(m->begin[g]);
+    size_t b = 0;
+    const int rc = bmpc_batch_results(m->shards[g], x_out ? x_out + b0 * m->n * m->nx : nullptr,
+                                      u_out ? u_out + b0 * m->n * m->nu : nullptr, reports ? reports + b0 : nullptr,
+                                      &b);
+    if (rc != BMPC_OK) return rc;
+    tot += b;
+  }
+  if (d2h_bytes) *d2h_bytes = tot;
+  return BMPC_OK;
+}
+
+int bmpc_multi_shard(bmpc_multi* m, int g, bmpc_batch** batch, int* begin, int* n) {
+  if (!m || g < 0 || g >= static_cast<int>(m->shards.size())) return fail(BMPC_ERR_INVALID, "bad shard");
+  if (batch) *batch = m->shards[static_cast<size_t>(g)];
+  if (begin) *begin = m->begin[static_cast<size_t>(g)];
+  if (n) *n = m->cnt[static_cast<size_t>(g)];
+  return BMPC_OK;
+}
+
+int bmpc_solve_batch(bmpc_ctx* const* ctxs, int n_ctx, const bmpc_tree* tree, int count,
+                     const bmpc_model_desc* models, const bmpc_options* opts, double* x_out, double* u_out,
+                     bmpc_report* reports) {
+  if (!models) return fail(BMPC_ERR_INVALID, "null models");
+  bmpc_multi* m = nullptr;
+  int rc = bmpc_multi_create(ctxs, n_ctx, tree, count, &models[0], 0, &m);
+  if (rc != BMPC_OK) return rc;
+  std::unique_ptr<bmpc_multi> guard(m);
+  if ((rc = bmpc_multi_set_models(m, models, nullptr)) != BMPC_OK) return rc;
+  if ((rc = bmpc_multi_solve(m, opts)) != BMPC_OK) return rc;
+  return bmpc_multi_results(m, x_out, u_out, reports, nullptr);
+}
+
 int bmpc_debug_grid_sync_us(bmpc_ctx* ctx, int blocks, int threads, int iters, double* us) {
   if (!ctx || !us) return fail(BMPC_ERR_INVALID, "null argument");
   cudaSetDevice(ctx->device);
