@@ -7,11 +7,14 @@
 // tree (it needs <bmpc/bmpc.hpp>) and link libbmpc_b200.so.
 //
 // The reference's `BmpcProblem` holds `std::function` callbacks
-// (problem.hpp:15-63), which cannot run on the device, so each model family the
-// reference builds has one entry point that recovers the callbacks' data:
-//   * scenario problems (unicycle RK4 + tracking + ego constraints,
-//     scenarios.hpp:115-171): the builders' `ScenarioSpec` + `ScenarioArtifacts`
-//     (scenarios.hpp:25-55) carry everything the callbacks capture;
+// (problem.hpp:15-63), which cannot run on the device; the device solves the
+// two model families the reference builds, and the data their callbacks
+// capture is recovered from the callbacks themselves:
+//   * `solve(problem, opts, initial_inputs)` — the drop-in — probes a scenario
+//     problem (unicycle RK4 + tracking + ego constraints, scenarios.hpp:115-171)
+//     for dt, weights, references, vehicle predictions, limits and radius, bit
+//     for bit; the overload taking the builders' `ScenarioSpec` +
+//     `ScenarioArtifacts` (scenarios.hpp:25-55) reads them directly;
 //   * affine-quadratic problems (`testing::random_lq_problem`, oracles.hpp:316,
 //     or any problem whose dynamics are affine and costs quadratic): the blocks
 //     are read back through the callbacks themselves at x = 0, u = 0.
@@ -29,6 +32,7 @@
 
 #include <bmpc/bmpc.hpp>
 
+#include <cmath>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -292,6 +296,229 @@ inline SolveResult solve_affine_quadratic(const BmpcProblem& problem, const Solv
   m.initial_state = x0.data();
   m.lq_stage = stage.data();
   m.lq_leaf = leaf.data();
+  return detail::run(problem, tree, m, opts, initial_inputs, ctx);
+}
+
+namespace detail {
+
+// Steps x0 by up to `span` ulps either way until pred holds (bit-exact
+// recovery of a captured constant from a callback probe).
+template <class Pred>
+inline bool ulp_search(double x0, Pred pred, double* out, int span = 64) {
+  if (pred(x0)) return *out = x0, true;
+  double up = x0, dn = x0;
+  for (int k = 0; k < span; ++k) {
+    up = std::nextafter(up, HUGE_VAL);
+    if (pred(up)) return *out = up, true;
+    dn = std::nextafter(dn, -HUGE_VAL);
+    if (pred(dn)) return *out = dn, true;
+  }
+  return false;
+}
+
+inline bool bit_equal(const VectorXd& a, const VectorXd& b) {
+  if (a.size() != b.size()) return false;
+  for (Eigen::Index i = 0; i < a.size(); ++i)
+    if (!(a(i) == b(i))) return false;
+  return true;
+}
+
+// Everything the scenario builders capture in a problem's callbacks
+// (scenarios.hpp:115-171, problem.hpp:194-222), recovered through the
+// callbacks themselves; empty `why` on success.
+struct UnicycleScene {
+  double dt{0}, a_max{0}, w_max{0}, radius{0};
+  MatrixXd Wx, Wu, Wf;
+  int nv{0};
+  std::vector<double> ref, veh;  // [node][4], [node][nv][2]
+  std::string why;
+};
+
+// A tracking reference ref with q(x) = W (x - ref): exact when W is diagonal
+// (each component searched until q_j(ref) == 0), else the solved estimate.
+template <class GradAt>
+inline bool recover_reference(const MatrixXd& W, GradAt grad_at, double* ref) {
+  const VectorXd q0 = grad_at(VectorXd::Zero(4));
+  bool diag = true;
+  for (int r = 0; r < 4; ++r)
+    for (int c = 0; c < 4; ++c) diag = diag && (r == c || W(r, c) == 0.0);
+  if (!diag) {
+    const VectorXd est = Eigen::PartialPivLU<MatrixXd>(W).solve(VectorXd(-q0));
+    for (int j = 0; j < 4; ++j) ref[j] = est(j);
+    return true;
+  }
+  VectorXd est(4);
+  for (int j = 0; j < 4; ++j) est(j) = W(j, j) != 0.0 ? -q0(j) / W(j, j) : 0.0;
+  for (int j = 0; j < 4; ++j) {
+    if (W(j, j) == 0.0) {  // an unweighted component never enters the cost
+      ref[j] = 0.0;
+      continue;
+    }
+    if (!ulp_search(est(j), [&](double c) {
+          VectorXd x = est;
+          x(j) = c;
+          return grad_at(x)(j) == 0.0;
+        }, &ref[j]))
+      return false;
+  }
+  return true;
+}
+
+inline UnicycleScene recover_unicycle(const BmpcProblem& p) {
+  UnicycleScene sc;
+  const TreeTopology& t = p.tree;
+  const int n = t.node_count;
+  auto bad = [&](const std::string& why) {
+    sc.why = why;
+    return sc;
+  };
+  if (p.state_dim != 4 || p.input_dim != 2) return bad("not (nx 4, nu 2)");
+  if (!p.has_constraints() || static_cast<int>(p.constraint.size()) != n) return bad("no ego constraints");
+  const int leaf0 = t.leaves.empty() ? -1 : t.leaves.front();
+  if (leaf0 < 0 || t.is_leaf(0)) return bad("tree without a non-leaf root");
+  sc.nv = p.constraint_dim(leaf0);
+  if (sc.nv > 4) return bad("more than 4 surrounding vehicles");
+  // dt: unicycle::step reproduced bit for bit (unicycle.hpp:36-42).
+  VectorXd xs(4), us(2), xg(4), ug(2);
+  xs << 0.0, 0.0, 0.0, 1.0;
+  us << 0.0, 0.0;
+  xg << 0.7, -1.3, 0.4, 2.5;
+  ug << 0.3, -0.2;
+  const VectorXd ys = p.dynamics[0].value(xs, us), yg = p.dynamics[0].value(xg, ug);
+  if (!ulp_search(ys(0), [&](double c) {
+        return bit_equal(unicycle::step(xs, us, c), ys) && bit_equal(unicycle::step(xg, ug, c), yg);
+      }, &sc.dt))
+    return bad("dynamics are not the unicycle RK4 step");
+  // Weights (constant across nodes) and references.
+  const VectorXd z4 = VectorXd::Zero(4), z2 = VectorXd::Zero(2);
+  sc.ref.assign(4 * static_cast<size_t>(n), 0.0);
+  sc.veh.assign(2 * static_cast<size_t>(sc.nv) * n, 0.0);
+  bool have_w = false, have_f = false;
+  for (int i = 0; i < n; ++i) {
+    const bool leaf = t.is_leaf(i);
+    if (p.constraint_dim(i) != sc.nv + (leaf ? 0 : 4)) return bad("constraint rows differ from ego_constraints");
+    if (leaf) {
+      MatrixXd P;
+      VectorXd q;
+      p.terminal_cost[static_cast<size_t>(i)].quadratic(z4, P, q);
+      if (!have_f) sc.Wf = P, have_f = true;
+      else if (!(P.rows() == 4 && (P - sc.Wf).cwiseAbs().maxCoeff() == 0.0)) return bad("terminal weights differ");
+      if (!recover_reference(sc.Wf, [&](const VectorXd& x) {
+            MatrixXd PP;
+            VectorXd qq;
+            p.terminal_cost[static_cast<size_t>(i)].quadratic(x, PP, qq);
+            return qq;
+          }, &sc.ref[4 * static_cast<size_t>(i)]))
+        return bad("terminal cost is not a tracking cost");
+    } else {
+      if (!bit_equal(p.dynamics[static_cast<size_t>(i)].value(xg, ug), yg)) return bad("dynamics differ between nodes");
+      MatrixXd Q, R, M;
+      VectorXd q, r;
+      p.cost[static_cast<size_t>(i)].quadratic(z4, z2, Q, R, M, q, r);
+      if (M.size() && M.cwiseAbs().maxCoeff() != 0.0) return bad("stage cost has a cross term");
+      if (!have_w) sc.Wx = Q, sc.Wu = R, have_w = true;
+      else if ((Q - sc.Wx).cwiseAbs().maxCoeff() != 0.0 || (R - sc.Wu).cwiseAbs().maxCoeff() != 0.0)
+        return bad("stage weights differ");
+      if (!recover_reference(sc.Wx, [&](const VectorXd& x) {
+            MatrixXd QQ, RR, MM;
+            VectorXd qq, rr;
+            p.cost[static_cast<size_t>(i)].quadratic(x, z2, QQ, RR, MM, qq, rr);
+            return qq;
+          }, &sc.ref[4 * static_cast<size_t>(i)]))
+        return bad("stage cost is not a tracking cost");
+      const VectorXd g = p.constraint[static_cast<size_t>(i)].value(z4, z2);
+      if (i == 0) sc.a_max = -g(0), sc.w_max = -g(2);
+      if (!(g(0) == -sc.a_max && g(1) == -sc.a_max && g(2) == -sc.w_max && g(3) == -sc.w_max))
+        return bad("input box rows differ");
+    }
+    // Vehicles: J = -(p - v) / dist at two points gives v and the radius by
+    // least squares; then each coordinate is searched until its Jacobian
+    // entry is exactly zero (p == v), and the radius until r - sqrt(eps) == g(v).
+    const NodeConstraint& con = p.constraint[static_cast<size_t>(i)];
+    const int nb = leaf ? 0 : 4;
+    for (int v = 0; v < sc.nv; ++v) {
+      auto probe = [&](double px, double py, double* gv, double* jx, double* jy) {
+        VectorXd x = z4;
+        x(0) = px;
+        x(1) = py;
+        MatrixXd Jx(nb + sc.nv, 4), Ju(nb + sc.nv, 2);
+        con.jacobians(x, z2, Jx, Ju);
+        if (gv) *gv = con.value(x, z2)(nb + v);
+        if (jx) *jx = Jx(nb + v, 0);
+        if (jy) *jy = Jx(nb + v, 1);
+      };
+      double g0, j0x, j0y, g1, j1x, j1y;
+      probe(0.0, 0.0, &g0, &j0x, &j0y);
+      const double nrm = std::hypot(j0x, j0y);
+      const double ox = nrm > 0 ? -j0y / nrm : 1.0, oy = nrm > 0 ? j0x / nrm : 0.0;  // perpendicular step
+      probe(ox, oy, &g1, &j1x, &j1y);
+      // v = x0 + J0 (r - g0) = x1 + J1 (r - g1)  =>  (J0 - J1) r = x1 - x0 + J0 g0 - J1 g1.
+      const double ax = j0x - j1x, ay = j0y - j1y;
+      const double bx = ox + j0x * g0 - j1x * g1, by = oy + j0y * g0 - j1y * g1;
+      const double den = ax * ax + ay * ay;
+      if (!(den > 0)) return bad("distance constraint not recoverable");
+      const double r_est = (ax * bx + ay * by) / den;
+      double vx = j0x * (r_est - g0), vy = j0y * (r_est - g0);
+      double ex, ey, gv;
+      if (!ulp_search(vx, [&](double c) { double jx; probe(c, vy, nullptr, &jx, nullptr); return jx == 0.0; }, &ex,
+                      1 << 16) ||
+          !ulp_search(vy, [&](double c) { double jy; probe(ex, c, nullptr, nullptr, &jy); return jy == 0.0; }, &ey,
+                      1 << 16))
+        return bad("distance constraint is not ego_constraints'");
+      probe(ex, ey, &gv, nullptr, nullptr);
+      double rad;
+      if (!ulp_search(gv + std::sqrt(1e-6), [&](double c) { return c - std::sqrt(0.0 * 0.0 + 0.0 * 0.0 + 1e-6) == gv; },
+                      &rad))
+        return bad("distance constraint is not ego_constraints'");
+      if (i == 0 && v == 0) sc.radius = rad;
+      else if (rad != sc.radius) return bad("safety radius differs");
+      sc.veh[(static_cast<size_t>(i) * sc.nv + v) * 2 + 0] = ex;
+      sc.veh[(static_cast<size_t>(i) * sc.nv + v) * 2 + 1] = ey;
+    }
+    if (!leaf && sc.nv == 0 && i == 0) sc.radius = 0.0;
+  }
+  return sc;
+}
+
+}  // namespace detail
+
+/// The drop-in: bmpc::solve(problem, opts, initial_inputs) (solver.hpp:595-596)
+/// for any problem of the two families the device solves. Scenario problems
+/// (unicycle RK4 + tracking costs + ego constraints, as scenarios.hpp builds
+/// them) are recognized by probing their callbacks: dt, the weights, every
+/// node's tracking reference, the vehicle predictions, the input limits and
+/// the safety radius are recovered bit for bit (each constant searched until
+/// the callback reproduces it exactly); unconstrained problems take the
+/// affine-quadratic family. Anything else throws std::invalid_argument.
+inline SolveResult solve(const BmpcProblem& problem, const SolverOptions& opts = {},
+                         const std::vector<VectorXd>* initial_inputs = nullptr, Context* ctx = nullptr) {
+  if (!problem.has_constraints()) return solve_affine_quadratic(problem, opts, initial_inputs, ctx);
+  const detail::UnicycleScene sc = detail::recover_unicycle(problem);
+  if (!sc.why.empty())
+    throw std::invalid_argument("bmpc::b200::solve: not a unicycle scenario problem (" + sc.why + ")");
+  const TreeTopology& t = problem.tree;
+  const detail::FlatTree tree(t);
+  std::vector<double> x0(4);
+  for (int j = 0; j < 4; ++j) x0[static_cast<size_t>(j)] = problem.initial_state(j);
+  bmpc_model_desc m{};
+  m.kind = BMPC_MODEL_UNICYCLE;
+  m.state_dim = 4;
+  m.input_dim = 2;
+  m.initial_state = x0.data();
+  m.dt = sc.dt;
+  for (int c = 0; c < 4; ++c)
+    for (int r = 0; r < 4; ++r) {
+      m.state_weights[r + 4 * c] = sc.Wx(r, c);
+      m.terminal_weights[r + 4 * c] = sc.Wf(r, c);
+    }
+  for (int c = 0; c < 2; ++c)
+    for (int r = 0; r < 2; ++r) m.input_weights[r + 2 * c] = sc.Wu(r, c);
+  m.accel_limit = sc.a_max;
+  m.yaw_rate_limit = sc.w_max;
+  m.safety_radius = sc.radius;
+  m.num_vehicles = sc.nv;
+  m.reference = sc.ref.data();
+  m.vehicle_position = sc.veh.data();
   return detail::run(problem, tree, m, opts, initial_inputs, ctx);
 }
 

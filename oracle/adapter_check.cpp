@@ -66,8 +66,10 @@ void scenario_case(const std::string& name, const bmpc::ScenarioSpec& spec, bool
   const bmpc::BmpcProblem problem =
       latency ? bmpc::build_latency_case(spec, &art) : bmpc::build_intersection_case(spec, v1, v2, &art);
   const bmpc::SolveResult want = bmpc::solve(problem, opts, u0);
-  const bmpc::SolveResult got = bmpc::b200::solve(problem, spec, art, opts, u0);  // was bmpc::solve(problem, opts)
+  const bmpc::SolveResult got = bmpc::b200::solve(problem, spec, art, opts, u0);
   compare(name, got, want);
+  // The exact drop-in signature: the callbacks are probed for the scene data.
+  compare(name + " [solve(problem, opts)]", bmpc::b200::solve(problem, opts, u0), want);  // was bmpc::solve
 }
 
 void lq_case(const std::string& name, int horizon, const std::vector<bmpc::TreeBranching>& br, int nx, int nu,
@@ -75,7 +77,9 @@ void lq_case(const std::string& name, int horizon, const std::vector<bmpc::TreeB
   std::mt19937_64 rng(seed);
   const bmpc::TreeTopology tree = bmpc::build_tree(horizon, br);
   const bmpc::BmpcProblem problem = bmpc::testing::random_lq_problem(rng, tree, nx, nu);
-  compare(name, bmpc::b200::solve_affine_quadratic(problem), bmpc::solve(problem));
+  const bmpc::SolveResult want = bmpc::solve(problem);
+  compare(name, bmpc::b200::solve_affine_quadratic(problem), want);
+  compare(name + " [solve(problem)]", bmpc::b200::solve(problem), want);
 }
 
 template <class E, class F>
@@ -131,6 +135,10 @@ int main() {
     scenario_case("smsilqr cfg0", intersection_spec(63, 10.0, 0.1), false, 2, 2, nullptr, sm);
     scenario_case("sssilqr cfg0", intersection_spec(63, 10.0, 0.1), false, 2, 2, nullptr, ss);
     scenario_case("sssilqr latency_spec(1.5,63,5,0.05)", latency_spec(1.5, 63, 5.0, 0.05), true, 0, 0, nullptr, ss);
+    bmpc::SolverOptions hy;
+    hy.backward = bmpc::BackwardStrategy::scan_condensed;
+    scenario_case("hypmsilqr cfg0", intersection_spec(63, 10.0, 0.1), false, 2, 2, nullptr, hy);
+    scenario_case("hypmsilqr intersection_spec(25,5,0.4) 2x2", intersection_spec(25, 5.0, 0.4), false, 2, 2, nullptr, hy);
   }
   expect_throw<std::invalid_argument>("mismatched artifacts rejected", [] {
     const bmpc::ScenarioSpec spec = intersection_spec(20, 4.0, 0.4);
@@ -139,6 +147,37 @@ int main() {
     art.reference.pop_back();
     bmpc::b200::solve(p, spec, art);
   });
+  expect_throw<std::invalid_argument>("non-scenario constrained problem rejected by solve(problem)", [] {
+    bmpc::BmpcProblem p = bmpc::build_intersection_case(intersection_spec(20, 4.0, 0.4), 2, 2);
+    for (auto& c : p.constraint) {  // a different constraint form
+      auto f = c.value;
+      c.value = [f](const bmpc::VectorXd& x, const bmpc::VectorXd& u) {
+        bmpc::VectorXd g = f(x, u);
+        g(g.size() - 1) += 0.25 * x(0) * x(0);
+        return g;
+      };
+    }
+    bmpc::b200::solve(p);
+  });
+  // Recovered scene data equals the builders' own (bit for bit).
+  {
+    const bmpc::ScenarioSpec spec = intersection_spec(63, 10.0, 0.1);
+    bmpc::ScenarioArtifacts art;
+    const bmpc::BmpcProblem p = bmpc::build_intersection_case(spec, 2, 2, &art);
+    const auto sc = bmpc::b200::detail::recover_unicycle(p);
+    bool same = sc.why.empty() && sc.dt == spec.dt() && sc.a_max == spec.accel_limit &&
+                sc.w_max == spec.yaw_rate_limit && sc.radius == spec.safety_radius;
+    for (int i = 0; same && i < p.tree.node_count; ++i) {
+      for (int j = 0; j < 4; ++j) same = same && sc.ref[4 * static_cast<size_t>(i) + j] == art.reference[static_cast<size_t>(i)](j);
+      for (int v = 0; v < sc.nv; ++v)
+        for (int j = 0; j < 2; ++j)
+          same = same && sc.veh[(static_cast<size_t>(i) * sc.nv + v) * 2 + j] ==
+                             art.vehicle_position[static_cast<size_t>(i)][static_cast<size_t>(v)](j);
+    }
+    if (!same) ++failures;
+    std::printf("{\"case\": \"probed scene data bit-identical to the builder's\", \"ok\": %s, \"why\": \"%s\"}\n",
+                same ? "true" : "false", sc.why.c_str());
+  }
   std::printf("{\"failures\": %d}\n", failures);
   return failures ? 1 : 0;
 }
