@@ -95,6 +95,29 @@ typedef struct bmpc_model_desc {
 #define BMPC_SCENARIO_INTERSECTION 0 /* build_intersection_case (scenarios.hpp:296) */
 #define BMPC_SCENARIO_LATENCY 1      /* build_latency_case (scenarios.hpp:398) */
 #define BMPC_SCENARIO_MULTISTAGE 2   /* multi-stage intersection (cfg2/cfg3) */
+/* ScenarioSpec (scenarios.hpp:15-47): surrounding vehicles, tuning and
+ * timing of a scene. The JSON form is scenario_spec_to_json /
+ * scenario_spec_from_json (serialization.hpp:128-197). */
+#define BMPC_MAX_TARGETS 8
+typedef struct bmpc_vehicle {
+  double position[2];
+  double heading, speed;
+  int n_targets;
+  double target_speeds[BMPC_MAX_TARGETS];
+} bmpc_vehicle;
+typedef struct bmpc_scenario_spec {
+  double total_time;
+  int n_shared; /* 1 or 2 */
+  double shared_times[2];
+  int horizon;
+  double ego_start[4];
+  int n_vehicles; /* <= 4 */
+  bmpc_vehicle vehicles[4];
+  double state_weights[4], input_weights[2], terminal_weights[4];
+  double accel_limit, yaw_rate_limit, safety_radius, prediction_tau;
+  double reference_turn_rate, backup_deceleration, continue_deceleration;
+} bmpc_scenario_spec;
+
 typedef struct bmpc_scenario {
   int family;
   int horizon;
@@ -106,6 +129,10 @@ typedef struct bmpc_scenario {
   int branch_arity[8];
   int perturb;           /* perturb the measured initial state ... */
   unsigned long long perturb_seed; /* ... with std::mt19937_64(perturb_seed) */
+  /* Full scene (vehicles, weights, limits, timing) as build_intersection_case /
+   * build_latency_case take it; NULL = the family's reference preset
+   * (intersection_spec / latency_spec) from the timing fields above. */
+  const bmpc_scenario_spec* spec;
 } bmpc_scenario;
 
 typedef struct bmpc_problem_data {
@@ -303,6 +330,22 @@ int bmpc_debug_grid_sync_us(bmpc_ctx* ctx, int blocks, int threads, int iters, d
 int bmpc_lqr_tree(bmpc_ctx* ctx, const bmpc_tree* tree, int nx, int nu, const double* stage, const double* defect,
                   const double* leaf, double reg, const double* dx0, int grid, double* K, double* k, double* P,
                   double* p, double* dx, double* du, double* scalars);
+
+/* Backward strategy of subsequent bmpc_lqr_tree calls on this ctx:
+ * BMPC_BACKWARD_SCAN_TREE_RICCATI (default) or BMPC_BACKWARD_SCAN_CONDENSED
+ * (the shared segment condensed into a dense QP; its nodes get K = 0, k = u,
+ * backward_pass, solver.hpp:297-307). */
+int bmpc_ctx_set_lqr_strategy(bmpc_ctx* ctx, int backward);
+
+/* Batched scan-element primitives (lqr_scan.hpp), one GPU thread per element:
+ *   op 0  init_bwd_element (:28-49): a = count records [A B c Q R M q r]
+ *         (column-major; R gets + reg on its diagonal), out = elements;
+ *   op 1  combine_bwd (:80-111): out = a (+) b, elements [P p C A c]
+ *         (3 nx^2 + 2 nx doubles each, unpadded);
+ *   op 2  combine_fwd (:171-173): out = a (+) b, elements [A c] (nx^2 + nx).
+ * An element whose R is not positive definite comes back as NaN. */
+int bmpc_lqr_elements(bmpc_ctx* ctx, int op, int nx, int nu, int count, const double* a, const double* b, double reg,
+                      double* out);
 
 #ifdef __cplusplus
 }

@@ -27,6 +27,21 @@ int main(int argc, char** argv) {
     bmpc::build_latency_case(spec, &artifacts);
     doc["kind"] = "latency";
     doc["spec"] = bmpc::scenario_spec_to_json(spec);
+  } else if (scenario == "spec-intersection" || scenario == "spec-latency") {
+    // A scene from JSON (scenario_spec_from_json, serialization.hpp:156-197),
+    // built by the reference builder: argv[2] = spec JSON, argv[3..4] = v1 v2.
+    const bmpc::ScenarioSpec spec = bmpc::scenario_spec_from_json(bmpc::json::parse(argv[2]));
+    if (scenario == "spec-intersection") {
+      const int v1 = std::stoi(argv[3]), v2 = std::stoi(argv[4]);
+      bmpc::build_intersection_case(spec, v1, v2, &artifacts);
+      doc["kind"] = "intersection";
+      doc["v1_count"] = v1;
+      doc["v2_count"] = v2;
+    } else {
+      bmpc::build_latency_case(spec, &artifacts);
+      doc["kind"] = "latency";
+    }
+    doc["spec"] = bmpc::scenario_spec_to_json(spec);
   } else if (scenario == "report") {  // report_to_json of the cfg0 solve (acceptance_test.cpp:93-102)
     const bmpc::BmpcProblem problem =
         bmpc::build_intersection_case(bmpc::intersection_spec(63, 10.0, 0.1), 2, 2);

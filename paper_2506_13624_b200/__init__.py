@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import dataclasses
+import math
 import os
 from typing import Optional, Sequence
 
@@ -51,11 +52,25 @@ class _Model(C.Structure):
                 ("lq_stage", C.c_void_p), ("lq_leaf", C.c_void_p)]
 
 
+class _Vehicle(C.Structure):
+    _fields_ = [("position", C.c_double * 2), ("heading", C.c_double), ("speed", C.c_double),
+                ("n_targets", C.c_int), ("target_speeds", C.c_double * 8)]
+
+
+class _SpecC(C.Structure):  # bmpc_scenario_spec
+    _fields_ = [("total_time", C.c_double), ("n_shared", C.c_int), ("shared_times", C.c_double * 2),
+                ("horizon", C.c_int), ("ego_start", C.c_double * 4), ("n_vehicles", C.c_int),
+                ("vehicles", _Vehicle * 4), ("state_weights", C.c_double * 4), ("input_weights", C.c_double * 2),
+                ("terminal_weights", C.c_double * 4)] + \
+               [(n, C.c_double) for n in ("accel_limit", "yaw_rate_limit", "safety_radius", "prediction_tau",
+                                          "reference_turn_rate", "backup_deceleration", "continue_deceleration")]
+
+
 class _Scenario(C.Structure):
     _fields_ = [("family", C.c_int), ("horizon", C.c_int), ("total_time", C.c_double),
                 ("shared_time", C.c_double * 2), ("v1", C.c_int), ("v2", C.c_int), ("n_branchings", C.c_int),
                 ("branch_step", C.c_int * 8), ("branch_arity", C.c_int * 8), ("perturb", C.c_int),
-                ("perturb_seed", C.c_ulonglong)]
+                ("perturb_seed", C.c_ulonglong), ("spec", C.POINTER(_SpecC))]
 
 
 class _ProblemData(C.Structure):
@@ -182,31 +197,100 @@ def build_tree(horizon: int, branchings: Sequence[tuple] = ()) -> TreeTopology:
 
 # ----------------------------------------------------------------- problems
 @dataclasses.dataclass
+class SurroundingVehicle:
+    """SurroundingVehicle (scenarios.hpp:15-22): constant heading, speed
+    converging toward the per-scenario target."""
+    position: tuple = (0.0, 0.0)
+    heading: float = 0.0
+    speed: float = 0.0
+    target_speeds: tuple = ()
+
+
+@dataclasses.dataclass
 class ScenarioSpec:
-    """Subset of ScenarioSpec (scenarios.hpp:25-47) the builders consume."""
-    family: int
+    """ScenarioSpec (scenarios.hpp:25-47) with the reference's defaults, plus
+    the multistage builder's branchings. `family` records which preset made
+    the spec; the builder called decides the family."""
+    family: int = SCENARIO_INTERSECTION
     horizon: int = 63
     total_time: float = 10.0
     shared_times: tuple = (0.1,)
     branchings: tuple = ()  # multistage: ((step, arity), ...)
+    ego_start: tuple = (0.0, -20.0, math.pi / 2.0, 5.0)
+    vehicles: tuple = ()
+    state_weights: tuple = (1.0, 1.0, 0.1, 0.1)
+    input_weights: tuple = (0.5, 0.5)
+    terminal_weights: tuple = (1.0, 1.0, 0.1, 0.1)
+    accel_limit: float = 3.0
+    yaw_rate_limit: float = 0.5
+    safety_radius: float = 3.0
+    prediction_tau: float = 1.5
+    reference_turn_rate: float = 0.4
+    backup_deceleration: float = 3.0
+    continue_deceleration: float = 2.5
 
     def dt(self) -> float:
         return self.total_time / self.horizon
 
+    def _c(self) -> "_SpecC":
+        c = _SpecC()
+        c.total_time = float(self.total_time)
+        if not 1 <= len(self.shared_times) <= 2:
+            raise ValueError("ScenarioSpec: one or two shared times")
+        c.n_shared = len(self.shared_times)
+        for i, t in enumerate(self.shared_times):
+            c.shared_times[i] = float(t)
+        c.horizon = int(self.horizon)
+        for i in range(4):
+            c.ego_start[i] = float(self.ego_start[i])
+        if len(self.vehicles) > 4:
+            raise ValueError("ScenarioSpec: at most 4 surrounding vehicles")
+        c.n_vehicles = len(self.vehicles)
+        for k, v in enumerate(self.vehicles):
+            cv = c.vehicles[k]
+            cv.position[0], cv.position[1] = float(v.position[0]), float(v.position[1])
+            cv.heading, cv.speed = float(v.heading), float(v.speed)
+            if len(v.target_speeds) > 8:
+                raise ValueError("ScenarioSpec: at most 8 target speeds per vehicle")
+            cv.n_targets = len(v.target_speeds)
+            for i, t in enumerate(v.target_speeds):
+                cv.target_speeds[i] = float(t)
+        for i in range(4):
+            c.state_weights[i] = float(self.state_weights[i])
+            c.terminal_weights[i] = float(self.terminal_weights[i])
+        for i in range(2):
+            c.input_weights[i] = float(self.input_weights[i])
+        for k in ("accel_limit", "yaw_rate_limit", "safety_radius", "prediction_tau", "reference_turn_rate",
+                  "backup_deceleration", "continue_deceleration"):
+            setattr(c, k, float(getattr(self, k)))
+        return c
+
 
 def intersection_spec(horizon: int = 63, total_time: float = 10.0, shared_time: float = 0.1) -> ScenarioSpec:
-    return ScenarioSpec(SCENARIO_INTERSECTION, horizon, total_time, (shared_time,))
+    """intersection_spec (scenarios.hpp:178-197): the ego turns left across an
+    oncoming vehicle while following a slower lead vehicle."""
+    return ScenarioSpec(SCENARIO_INTERSECTION, horizon, total_time, (shared_time,),
+                        ego_start=(0.0, -20.0, math.pi / 2.0, 5.0),
+                        vehicles=(SurroundingVehicle((-3.5, 30.0), -math.pi / 2.0, 8.0, (8.0, 2.0, 5.0, 3.5)),
+                                  SurroundingVehicle((0.0, -10.0), math.pi / 2.0, 5.0, (5.0, 1.0, 3.0, 2.0))))
 
 
 def latency_spec(shared_time_1: float, horizon: int = 255, total_time: float = 5.0,
                  shared_time_0: float = 0.05) -> ScenarioSpec:
-    return ScenarioSpec(SCENARIO_LATENCY, horizon, total_time, (shared_time_0, shared_time_1))
+    """latency_spec (scenarios.hpp:300-317): cruising behind a lead vehicle."""
+    return ScenarioSpec(SCENARIO_LATENCY, horizon, total_time, (shared_time_0, shared_time_1),
+                        ego_start=(0.0, 0.0, 0.0, 10.0),
+                        vehicles=(SurroundingVehicle((30.0, 0.0), 0.0, 8.0, (8.0, 0.0)),))
 
 
-def multistage_spec(horizon: int, branchings: Sequence[tuple], total_time: float = 10.0) -> ScenarioSpec:
+def multistage_spec(horizon: int, branchings: Sequence[tuple], total_time: float = 10.0,
+                    base: Optional[ScenarioSpec] = None) -> ScenarioSpec:
     """cfg2/cfg3 trees: one uniform branching (step, arity) per stage; at stage
-    j vehicle j mod 2 reveals its speed target."""
-    return ScenarioSpec(SCENARIO_MULTISTAGE, horizon, total_time, (0.1,), tuple(tuple(b) for b in branchings))
+    j vehicle j mod 2 reveals its speed target. The scene
+    is intersection_spec's unless `base` gives another one."""
+    base = base or intersection_spec(horizon, total_time, 0.1)
+    return dataclasses.replace(base, family=SCENARIO_MULTISTAGE, horizon=horizon, total_time=total_time,
+                               branchings=tuple(tuple(b) for b in branchings))
 
 
 class BmpcProblem:
@@ -245,9 +329,11 @@ class BmpcProblem:
             self._data = None
 
 
-def _build_scenario(spec: ScenarioSpec, v1=2, v2=2, perturb_seed=None) -> BmpcProblem:
+def _build_scenario(spec: ScenarioSpec, family: int, v1=2, v2=2, perturb_seed=None) -> BmpcProblem:
     s = _Scenario()
-    s.family = spec.family
+    s.family = family
+    spec_c = spec._c()
+    s.spec = C.pointer(spec_c)
     s.horizon = spec.horizon
     s.total_time = spec.total_time
     st = list(spec.shared_times) + [0.0, 0.0]
@@ -269,17 +355,19 @@ def _build_scenario(spec: ScenarioSpec, v1=2, v2=2, perturb_seed=None) -> BmpcPr
 
 
 def build_intersection_case(spec: ScenarioSpec, v1_count: int, v2_count: int, perturb_seed=None) -> BmpcProblem:
-    """build_intersection_case (scenarios.hpp:296-372)."""
-    return _build_scenario(spec, v1_count, v2_count, perturb_seed)
+    """build_intersection_case (scenarios.hpp:219-295) of any scene (two
+    vehicles with enough target speeds)."""
+    return _build_scenario(spec, SCENARIO_INTERSECTION, v1_count, v2_count, perturb_seed)
 
 
 def build_latency_case(spec: ScenarioSpec, perturb_seed=None) -> BmpcProblem:
-    """build_latency_case (scenarios.hpp:398-479)."""
-    return _build_scenario(spec, perturb_seed=perturb_seed)
+    """build_latency_case (scenarios.hpp:321-402) of any scene (one vehicle
+    with two target speeds, two shared times)."""
+    return _build_scenario(spec, SCENARIO_LATENCY, perturb_seed=perturb_seed)
 
 
 def build_multistage_case(spec: ScenarioSpec, perturb_seed=None) -> BmpcProblem:
-    return _build_scenario(spec, perturb_seed=perturb_seed)
+    return _build_scenario(spec, SCENARIO_MULTISTAGE, perturb_seed=perturb_seed)
 
 
 def lq_problem(tree: TreeTopology, nx: int, nu: int, x0: np.ndarray, stage: np.ndarray,
@@ -536,6 +624,30 @@ class Batch:
         if getattr(self, "_h", None) and _lib_handle is not None:
             _lib_handle.bmpc_batch_destroy(self._h)
             self._h = None
+
+
+def set_lqr_strategy(ctx: Context, backward: str):
+    """Backward strategy of subsequent lqr_tree calls on ctx:
+    "scan-tree-riccati" (default) or "scan-condensed" (bmpc_ctx_set_lqr_strategy)."""
+    code = {"scan-tree-riccati": 0, "scan-condensed": 1}[backward]
+    _check(lib().bmpc_ctx_set_lqr_strategy(ctx._h, code))
+
+
+def lqr_elements(op: str, nx: int, nu: int, a: np.ndarray, b: Optional[np.ndarray] = None, reg: float = 0.0,
+                 ctx: Optional[Context] = None) -> np.ndarray:
+    """Batched scan-element primitives on the GPU (bmpc_lqr_elements):
+    "init_bwd" of packed [A B c Q R M q r] records (rows of a), "combine_bwd"
+    / "combine_fwd" of element rows a (+) b (lqr_scan.hpp:28-111, 171-173)."""
+    ctx = ctx or default_context()
+    code = {"init_bwd": 0, "combine_bwd": 1, "combine_fwd": 2}[op]
+    a = np.ascontiguousarray(a, np.float64)
+    count = a.shape[0]
+    width = nx * nx + nx if code == 2 else 3 * nx * nx + 2 * nx
+    bb = None if b is None else np.ascontiguousarray(b, np.float64)
+    out = np.zeros((count, width))
+    _check(lib().bmpc_lqr_elements(ctx._h, code, int(nx), int(nu), int(count), _ptr(a), _ptr(bb), C.c_double(reg),
+                                   _ptr(out)))
+    return out
 
 
 def shard_range(count: int, n_shards: int, g: int) -> tuple:

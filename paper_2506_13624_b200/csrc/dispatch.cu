@@ -111,10 +111,21 @@ int solve_grid_blocks(int nx, int nu, int threads) {
 }
 
 cudaError_t launch_lqr_tree(int nx, int nu, bool grid, const Topo* d_topo, const Work* d_work, double reg,
-                            double* d_scalars, double* red, int blocks, int threads, cudaStream_t stream, int seq_max) {
-#define X(a, b)           \
-  if (nx == a && nu == b) \
-    return LqrLaunch<a, b>::lqr_tree(grid, d_topo, d_work, reg, d_scalars, red, blocks, threads, stream, seq_max);
+                            double* d_scalars, double* red, int blocks, int threads, cudaStream_t stream, int seq_max,
+                            int condensed) {
+#define X(a, b)                                                                                           \
+  if (nx == a && nu == b)                                                                                 \
+    return LqrLaunch<a, b>::lqr_tree(grid, d_topo, d_work, reg, d_scalars, red, blocks, threads, stream, seq_max, \
+                                     condensed);
+  BMPC_LQR_DIMS(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_lqr_elements(int nx, int nu, int op, int count, const double* a, const double* b, double reg,
+                                double* out, cudaStream_t stream) {
+#define X(c, d) \
+  if (nx == c && nu == d) return LqrLaunch<c, d>::elements(op, count, a, b, reg, out, stream);
   BMPC_LQR_DIMS(X)
 #undef X
   return cudaErrorInvalidValue;

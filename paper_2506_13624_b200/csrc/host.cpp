@@ -281,6 +281,36 @@ void perturb(std::vector<double>& x0, unsigned long long seed) {
   x0[3] += dv(rng);
 }
 
+// A caller-provided ScenarioSpec (bmpc_scenario_spec).
+Spec spec_from(const bmpc_scenario_spec& c) {
+  Spec s;
+  s.total_time = c.total_time;
+  if (c.n_shared < 1 || c.n_shared > 2) throw std::invalid_argument("scenario spec: 1 or 2 shared times");
+  s.shared_times.assign(c.shared_times, c.shared_times + c.n_shared);
+  s.horizon = c.horizon;
+  std::copy(c.ego_start, c.ego_start + 4, s.ego);
+  if (c.n_vehicles < 0 || c.n_vehicles > kMaxVehicles) throw std::invalid_argument("scenario spec: at most 4 vehicles");
+  for (int v = 0; v < c.n_vehicles; ++v) {
+    const bmpc_vehicle& cv = c.vehicles[v];
+    if (cv.n_targets < 0 || cv.n_targets > BMPC_MAX_TARGETS)
+      throw std::invalid_argument("scenario spec: at most 8 target speeds per vehicle");
+    s.vehicles.push_back({cv.position[0], cv.position[1], cv.heading, cv.speed,
+                          std::vector<double>(cv.target_speeds, cv.target_speeds + cv.n_targets)});
+  }
+  std::copy(c.state_weights, c.state_weights + 4, s.state_w);
+  std::copy(c.input_weights, c.input_weights + 2, s.input_w);
+  std::copy(c.terminal_weights, c.terminal_weights + 4, s.terminal_w);
+  s.accel_limit = c.accel_limit;
+  s.yaw_rate_limit = c.yaw_rate_limit;
+  s.safety_radius = c.safety_radius;
+  s.prediction_tau = c.prediction_tau;
+  s.reference_turn_rate = c.reference_turn_rate;
+  s.backup_deceleration = c.backup_deceleration;
+  s.continue_deceleration = c.continue_deceleration;
+  if (!(s.horizon > 0) || !(s.total_time > 0)) throw std::invalid_argument("scenario spec: horizon and total time > 0");
+  return s;
+}
+
 ProblemData* build_scenario(const bmpc_scenario& sc) {
   auto pd = std::make_unique<ProblemData>();
   Spec spec;
@@ -288,13 +318,14 @@ ProblemData* build_scenario(const bmpc_scenario& sc) {
   std::vector<double> weights;  // max_arity 16
   constexpr int kMaxA = 16;
   if (sc.family == BMPC_SCENARIO_INTERSECTION) {
-    spec = intersection_spec(sc.horizon, sc.total_time, sc.shared_time[0]);
+    spec = sc.spec ? spec_from(*sc.spec) : intersection_spec(sc.horizon, sc.total_time, sc.shared_time[0]);
     const int leaves = sc.v1 * sc.v2;
     const bool ok = leaves == 1 || leaves == 2 || leaves == 4 || leaves == 6 || leaves == 9 || leaves == 12;
     if (!ok || sc.v1 < 1 || sc.v2 < 1)
       throw std::invalid_argument("build_intersection_case: leaf count " + std::to_string(leaves) +
                                   " not in {1, 2, 4, 6, 9, 12}");
-    if (sc.v1 > 4 || sc.v2 > 4)
+    if (spec.vehicles.size() != 2 || static_cast<int>(spec.vehicles[0].targets.size()) < sc.v1 ||
+        static_cast<int>(spec.vehicles[1].targets.size()) < sc.v2)
       throw std::invalid_argument("build_intersection_case: need 2 vehicles with enough targets");
     const int branch_step = static_cast<int>(std::lround(spec.shared_times.at(0) / spec.dt()));
     if (leaves > 1) {
@@ -306,9 +337,12 @@ ProblemData* build_scenario(const bmpc_scenario& sc) {
       for (int a = 0; a < leaves; ++a) weights[static_cast<size_t>(a)] = 1.0 / leaves;
     }
   } else if (sc.family == BMPC_SCENARIO_LATENCY) {
-    spec = latency_spec(sc.shared_time[1], sc.horizon, sc.total_time, sc.shared_time[0]);
-    if (!(spec.shared_times[0] < spec.shared_times[1]) || !(spec.shared_times[1] < spec.total_time))
+    spec = sc.spec ? spec_from(*sc.spec) : latency_spec(sc.shared_time[1], sc.horizon, sc.total_time, sc.shared_time[0]);
+    if (spec.shared_times.size() != 2 || !(spec.shared_times[0] < spec.shared_times[1]) ||
+        !(spec.shared_times[1] < spec.total_time))
       throw std::invalid_argument("build_latency_case: need T_sh0 < T_sh1 < T");
+    if (spec.vehicles.size() != 1 || spec.vehicles[0].targets.size() != 2)
+      throw std::invalid_argument("build_latency_case: need one vehicle with 2 targets");
     const int k0 = static_cast<int>(std::lround(spec.shared_times[0] / spec.dt()));
     const int k1 = static_cast<int>(std::lround(spec.shared_times[1] / spec.dt()));
     if (k0 < 0 || k0 >= k1 || k1 >= spec.horizon)
@@ -318,12 +352,15 @@ ProblemData* build_scenario(const bmpc_scenario& sc) {
     weights.assign(2 * kMaxA, 0.0);
     weights[0] = weights[1] = weights[kMaxA] = weights[kMaxA + 1] = 0.5;
   } else if (sc.family == BMPC_SCENARIO_MULTISTAGE) {
-    spec = intersection_spec(sc.horizon, sc.total_time, 0.1);
+    spec = sc.spec ? spec_from(*sc.spec) : intersection_spec(sc.horizon, sc.total_time, 0.1);
     if (sc.n_branchings < 0 || sc.n_branchings > 8) throw std::invalid_argument("multistage: 0..8 branchings");
+    if (spec.vehicles.size() != 2) throw std::invalid_argument("multistage: need 2 vehicles");
     weights.assign(static_cast<size_t>(std::max(sc.n_branchings, 1)) * kMaxA, 0.0);
     for (int b = 0; b < sc.n_branchings; ++b) {
-      if (sc.branch_arity[b] < 2 || sc.branch_arity[b] > 4)
-        throw std::invalid_argument("multistage: arity must be in [2, 4] (4 speed targets per vehicle)");
+      const size_t targets = spec.vehicles[static_cast<size_t>(b % 2)].targets.size();
+      if (sc.branch_arity[b] < 2 || static_cast<size_t>(sc.branch_arity[b]) > targets)
+        throw std::invalid_argument("multistage: arity must be in [2, " + std::to_string(targets) +
+                                    "] (the revealing vehicle's speed targets)");
       steps.push_back(sc.branch_step[b]);
       arities.push_back(sc.branch_arity[b]);
       for (int a = 0; a < sc.branch_arity[b]; ++a)
@@ -674,6 +711,7 @@ struct bmpc_ctx {
   // safe, e.g. garbage-collected language bindings at interpreter exit).
   int live_batches{0};
   bool destroy_pending{false};
+  int lqr_backward{0};  // bmpc_lqr_tree strategy: 0 tree scan, 1 condensed shared segment
 };
 
 static void ctx_free(bmpc_ctx* c) {
@@ -1665,6 +1703,38 @@ int bmpc_solve(bmpc_ctx* ctx, const bmpc_tree* tree, const bmpc_model_desc* mode
   return BMPC_OK;
 }
 
+int bmpc_ctx_set_lqr_strategy(bmpc_ctx* c, int backward) {
+  if (!c || (backward != BMPC_BACKWARD_SCAN_TREE_RICCATI && backward != BMPC_BACKWARD_SCAN_CONDENSED))
+    return fail(BMPC_ERR_INVALID, "lqr strategy must be scan_tree_riccati or scan_condensed");
+  c->lqr_backward = backward;
+  return BMPC_OK;
+}
+
+int bmpc_lqr_elements(bmpc_ctx* ctx, int op, int nx, int nu, int count, const double* a, const double* b, double reg,
+                      double* out) {
+  try {
+    if (!ctx || !a || !out || count < 0 || op < 0 || op > 2 || (op > 0 && !b)) return fail(BMPC_ERR_INVALID, "bad arguments");
+    if (!lqr_dims_supported(nx, nu)) return fail(BMPC_ERR_UNSUPPORTED, "dims not compiled in");
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const size_t lq = lq_stage_size(nx, nu), be = 3 * static_cast<size_t>(nx) * nx + 2 * nx,
+                 fe = static_cast<size_t>(nx) * nx + nx;
+    const size_t in_a = op == 0 ? lq : (op == 1 ? be : fe), in_b = op == 0 ? 0 : in_a, out_e = op == 2 ? fe : be;
+    const size_t C = static_cast<size_t>(count);
+    DevBuf da(std::max<size_t>(C * in_a, 1) * sizeof(double)), db(std::max<size_t>(C * in_b, 1) * sizeof(double)),
+        dout(std::max<size_t>(C * out_e, 1) * sizeof(double));
+    cudaStream_t s = ctx->stream;
+    ck(cudaMemcpyAsync(da.p, a, C * in_a * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
+    if (in_b) ck(cudaMemcpyAsync(db.p, b, C * in_b * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
+    ck(launch_lqr_elements(nx, nu, op, count, da.as<double>(), db.as<double>(), reg, dout.as<double>(), s), "launch");
+    ++ctx->launches;
+    ck(cudaMemcpyAsync(out, dout.p, C * out_e * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaStreamSynchronize(s), "sync");
+    return BMPC_OK;
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
+}
+
 int bmpc_lqr_tree(bmpc_ctx* ctx, const bmpc_tree* tree, int nx, int nu, const double* stage, const double* defect,
                   const double* leaf, double reg, const double* dx0, int grid, double* K, double* k, double* P,
                   double* p, double* dx, double* du, double* scalars) {
@@ -1718,15 +1788,24 @@ int bmpc_lqr_tree(bmpc_ctx* ctx, const bmpc_tree* tree, int nx, int nu, const do
     w.dx = base + off[8];
     w.du = base + off[9];
     w.value = base + off[10];
-    ck(cudaMemcpyAsync(d_work.p, &w, sizeof w, cudaMemcpyHostToDevice, s), "h2d");
-    DevBuf red;
+    DevBuf red, cond;
     int blocks = 0;
     if (grid) {
       blocks = lqr_grid_blocks(nx, nu, 256);
       red = DevBuf(2 * static_cast<size_t>(std::max(blocks, 1)) * kRedSlotsHost * sizeof(double));
     }
+    const int condensed = ctx->lqr_backward == BMPC_BACKWARD_SCAN_CONDENSED && plan->topo.n_shared > 0;
+    if (condensed) {  // per-node records + H, H copy, h, u, pivots (see batch_launch)
+      const size_t m = static_cast<size_t>(plan->topo.n_shared), nb = static_cast<size_t>(plan->topo.n_bound);
+      const size_t ni = m * nu;
+      if (ni > kCondMaxInputs) return fail(BMPC_ERR_UNSUPPORTED, "scan_condensed: shared segment too large");
+      const size_t rec = (static_cast<size_t>(nx) * nx + nx) * 2 + nx + static_cast<size_t>(nx) * nu;
+      cond = DevBuf(((m + nb) * ((rec + 1) & ~size_t{1}) + 2 * ni * ni + 4 * ni + 2) * sizeof(double));
+      w.cond = cond.as<double>();
+    }
+    ck(cudaMemcpyAsync(d_work.p, &w, sizeof w, cudaMemcpyHostToDevice, s), "h2d");
     ck(launch_lqr_tree(nx, nu, grid != 0, plan->d_topo.as<Topo>(), d_work.as<Work>(), reg, d_sc.as<double>(),
-                       red.as<double>(), blocks, 256, s, seq_max_for(ctx)),
+                       red.as<double>(), blocks, 256, s, seq_max_for(ctx), condensed),
        "lqr launch");
     ++ctx->launches;
     ck(cudaMemcpyAsync(h.data(), d_state.p, per * sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");

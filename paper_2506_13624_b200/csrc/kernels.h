@@ -30,7 +30,12 @@ template <int NX, int NU>
 struct LqrLaunch {
   static Strides strides();
   static cudaError_t lqr_tree(bool grid, const Topo* d_topo, const Work* d_work, double reg, double* d_scalars,
-                              double* red, int blocks, int threads, cudaStream_t stream, int seq_max);
+                              double* red, int blocks, int threads, cudaStream_t stream, int seq_max, int condensed);
+  // Batched scan-element primitives (one thread per element): op 0
+  // init_bwd_element of packed [A B c Q R M q r] records, op 1 combine_bwd,
+  // op 2 combine_fwd; elements unpadded (BwdLayout / FwdLayout ::size).
+  static cudaError_t elements(int op, int count, const double* a, const double* b, double reg, double* out,
+                              cudaStream_t stream);
   static int grid_blocks(int threads);
 };
 
@@ -72,7 +77,10 @@ cudaError_t launch_solve_grid(int nx, int nu, const Topo* d_topo, const ModelPar
 int solve_grid_blocks(int nx, int nu, int threads);
 int solve_cta_regs(int nx, int nu, int threads, int min_blocks, bool seq_only);
 cudaError_t launch_lqr_tree(int nx, int nu, bool grid, const Topo* d_topo, const Work* d_work, double reg,
-                            double* d_scalars, double* red, int blocks, int threads, cudaStream_t stream, int seq_max);
+                            double* d_scalars, double* red, int blocks, int threads, cudaStream_t stream, int seq_max,
+                            int condensed);
+cudaError_t launch_lqr_elements(int nx, int nu, int op, int count, const double* a, const double* b, double reg,
+                                double* out, cudaStream_t stream);
 int lqr_grid_blocks(int nx, int nu, int threads);
 
 size_t sizeof_topo();

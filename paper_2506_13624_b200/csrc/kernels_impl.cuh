@@ -75,10 +75,11 @@ __global__ void __launch_bounds__(256) solve_grid_kernel(const Topo* __restrict_
 }
 
 template <int NX, int NU, class G>
-__device__ void lqr_tree_body(G g, BlockCtx& ctx, double reg, double* scalars, int seq_max) {
+__device__ void lqr_tree_body(G g, BlockCtx& ctx, double reg, double* scalars, int seq_max, int condensed) {
   ModelParams dummy{};
   DevOptions o{};
   o.seq_max_len = seq_max;
+  o.condensed = condensed;
   o.fwd_scan_min = seq_max > 0 ? seq_max + 1 : 1;  // kernel-level API: forward mirrors the backward strategy
   o.keep_values = 1;
   o.chunk_bwd = 1;  // long segments in 256-thread blocks: the chunked sweep (tested against the oracle here)
@@ -92,7 +93,7 @@ __device__ void lqr_tree_body(G g, BlockCtx& ctx, double reg, double* scalars, i
 
 template <int NX, int NU>
 __global__ void __launch_bounds__(256) lqr_tree_cta_kernel(const Topo* topo, const Work* works, double reg,
-                                                           double* scalars, int seq_max) {
+                                                           double* scalars, int seq_max, int condensed) {
   __shared__ RedSmem red;
   __shared__ BlockCtx ctx;
   if (threadIdx.x == 0) {
@@ -103,12 +104,13 @@ __global__ void __launch_bounds__(256) lqr_tree_cta_kernel(const Topo* topo, con
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   red.part = reinterpret_cast<double*>(dyn_smem);
   __syncthreads();
-  lqr_tree_body<NX, NU>(CtaGroup{&red}, ctx, reg, scalars, seq_max);
+  lqr_tree_body<NX, NU>(CtaGroup{&red}, ctx, reg, scalars, seq_max, condensed);
 }
 
 template <int NX, int NU>
 __global__ void __launch_bounds__(256) lqr_tree_grid_kernel(const Topo* topo, const Work* works, double reg,
-                                                            double* scalars, double* red_scratch, int seq_max) {
+                                                            double* scalars, double* red_scratch, int seq_max,
+                                                            int condensed) {
   __shared__ RedSmem red;
   __shared__ BlockCtx ctx;
   if (threadIdx.x == 0) {
@@ -119,7 +121,48 @@ __global__ void __launch_bounds__(256) lqr_tree_grid_kernel(const Topo* topo, co
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   red.part = reinterpret_cast<double*>(dyn_smem);
   __syncthreads();
-  lqr_tree_body<NX, NU>(GridGroup{&red, red_scratch, nullptr}, ctx, reg, scalars, seq_max);
+  lqr_tree_body<NX, NU>(GridGroup{&red, red_scratch, nullptr}, ctx, reg, scalars, seq_max, condensed);
+}
+
+// Batched scan-element primitives of lqr_scan.hpp (the `associativity`
+// suite's entry point, verification.hpp:110-137).
+template <int NX, int NU>
+__global__ void lqr_elements_kernel(int op, int count, const double* __restrict__ a, const double* __restrict__ b,
+                                    double reg, double* __restrict__ out) {
+  using E = BwdLayout<NX>;
+  using F = FwdLayout<NX>;
+  using S = LqStage<NX, NU>;
+  using SL = StageLayout<NX, NU>;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    if (op == 0) {  // init_bwd_element (lqr_scan.hpp:28-49)
+      const double* r = a + static_cast<size_t>(i) * S::size;
+      double st[SL::size];
+      copy<NX * NX>(r + S::A, st + SL::A);
+      copy<NX * NU>(r + S::B, st + SL::B);
+      copy<NX * NX>(r + S::Q, st + SL::Q);
+      copy<NU * NU>(r + S::R, st + SL::R);
+      copy<NU * NX>(r + S::M, st + SL::M);
+      copy<NX>(r + S::q, st + SL::q);
+      copy<NU>(r + S::r, st + SL::r);
+      double* e = out + static_cast<size_t>(i) * E::size;
+      if (init_bwd_element<NX, NU>(st, reg, r + S::c, e) != kBwdOk)
+        for (int k = 0; k < E::size; ++k) e[k] = NAN;  // the reference's LDLT(R) failure
+    } else if (op == 1) {  // combine_bwd (lqr_scan.hpp:80-111), first (+) second
+      combine_bwd<NX>(a + static_cast<size_t>(i) * E::size, b + static_cast<size_t>(i) * E::size,
+                      out + static_cast<size_t>(i) * E::size);
+    } else {  // combine_fwd (lqr_scan.hpp:171-173)
+      combine_fwd<NX>(a + static_cast<size_t>(i) * F::size, b + static_cast<size_t>(i) * F::size,
+                      out + static_cast<size_t>(i) * F::size);
+    }
+  }
+}
+
+template <int NX, int NU>
+cudaError_t LqrLaunch<NX, NU>::elements(int op, int count, const double* a, const double* b, double reg, double* out,
+                                        cudaStream_t stream) {
+  const int blocks = count > 0 ? (count + 127) / 128 : 1;
+  lqr_elements_kernel<NX, NU><<<blocks < 1184 ? blocks : 1184, 128, 0, stream>>>(op, count, a, b, reg, out);
+  return cudaGetLastError();
 }
 
 
@@ -180,14 +223,14 @@ Strides LqrLaunch<NX, NU>::strides() {
 template <int NX, int NU>
 cudaError_t LqrLaunch<NX, NU>::lqr_tree(bool grid, const Topo* d_topo, const Work* d_work, double reg,
                                         double* d_scalars, double* red, int blocks, int threads,
-                                        cudaStream_t stream, int seq_max) {
+                                        cudaStream_t stream, int seq_max, int condensed) {
   const size_t smem = team_smem_bytes<NX, NU>(threads);
   if (!grid) {
     allow_smem(lqr_tree_cta_kernel<NX, NU>, smem);
-    lqr_tree_cta_kernel<NX, NU><<<1, threads, smem, stream>>>(d_topo, d_work, reg, d_scalars, seq_max);
+    lqr_tree_cta_kernel<NX, NU><<<1, threads, smem, stream>>>(d_topo, d_work, reg, d_scalars, seq_max, condensed);
     return cudaGetLastError();
   }
-  void* args[] = {&d_topo, &d_work, &reg, &d_scalars, &red, &seq_max};
+  void* args[] = {&d_topo, &d_work, &reg, &d_scalars, &red, &seq_max, &condensed};
   const int nb = blocks > 0 ? blocks : max_coresident(lqr_tree_grid_kernel<NX, NU>, threads, smem);
   return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lqr_tree_grid_kernel<NX, NU>), dim3(nb),
                                      dim3(threads), args, smem, stream);

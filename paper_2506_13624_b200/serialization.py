@@ -4,17 +4,17 @@ same keys and value types, for the GPU solver's Python interface:
 * tree spec      tree_spec_to_json / tree_from_json        (serialization.hpp:16-35)
 * solver options solver_options_from_json / _to_json       (serialization.hpp:37-85)
 * solve report   report_to_json                            (serialization.hpp:88-126)
-* scenario spec  scenario_spec_to_json                     (serialization.hpp:128-154)
+* scenario spec  scenario_spec_to_json / _from_json        (serialization.hpp:128-197)
 * problem dump   scenario_artifacts_to_json                (serialization.hpp:200-219)
 
 nlohmann::json objects are key-sorted maps, so `dumps` sorts keys; every
 double round-trips exactly (shortest representation both sides).
 """
+import dataclasses
 import json
-import math
 
-from . import (SCENARIO_INTERSECTION, SCENARIO_LATENCY, STATUS_NAMES, BmpcProblem, ScenarioSpec, SolveReport,
-               SolverOptions, TreeTopology, build_tree)
+from . import (STATUS_NAMES, BmpcProblem, ScenarioSpec, SolveReport, SolverOptions, SurroundingVehicle,
+               TreeTopology, build_tree)
 
 RECORD_KEYS = ("cost", "cost_al", "defect_l1", "violation", "alpha", "mu", "merit_before", "merit_after",
                "model_decrease", "max_feedforward", "regularization", "accepted", "outer")
@@ -118,31 +118,60 @@ def report_to_json(report: SolveReport) -> dict:
 
 
 # ---------------------------------------------------------------- scenarios
-_SPEC_DEFAULTS = {"state_weights": [1.0, 1.0, 0.1, 0.1], "input_weights": [0.5, 0.5],
-                  "terminal_weights": [1.0, 1.0, 0.1, 0.1], "accel_limit": 3.0, "yaw_rate_limit": 0.5,
-                  "safety_radius": 3.0, "prediction_tau": 1.5, "reference_turn_rate": 0.4,
-                  "backup_deceleration": 3.0, "continue_deceleration": 2.5}  # ScenarioSpec, scenarios.hpp:25-47
+_SPEC_SCALARS = ("accel_limit", "yaw_rate_limit", "safety_radius", "prediction_tau", "reference_turn_rate",
+                 "backup_deceleration", "continue_deceleration")
 
 
 def scenario_spec_to_json(spec: ScenarioSpec) -> dict:
-    """scenario_spec_to_json (serialization.hpp:128-154) of the specs the
-    builders take: intersection_spec (scenarios.hpp:178-197: ego and the
-    oncoming / lead vehicles) and latency_spec (scenarios.hpp:300-317)."""
-    if spec.family == SCENARIO_LATENCY:
-        ego = [0.0, 0.0, 0.0, 10.0]
-        veh = [{"position": [30.0, 0.0], "heading": 0.0, "speed": 8.0, "target_speeds": [8.0, 0.0]}]
-    elif spec.family == SCENARIO_INTERSECTION:
-        ego = [0.0, -20.0, math.pi / 2.0, 5.0]
-        veh = [{"position": [-3.5, 30.0], "heading": -math.pi / 2.0, "speed": 8.0,
-                "target_speeds": [8.0, 2.0, 5.0, 3.5]},
-               {"position": [0.0, -10.0], "heading": math.pi / 2.0, "speed": 5.0,
-                "target_speeds": [5.0, 1.0, 3.0, 2.0]}]
-    else:
-        raise ValueError("scenario_spec_to_json: the multistage family has no reference spec")
-    d = dict(_SPEC_DEFAULTS)
-    d.update({"total_time": float(spec.total_time), "shared_times": [float(t) for t in spec.shared_times],
-              "horizon": int(spec.horizon), "ego_start": ego, "vehicles": veh})
+    """scenario_spec_to_json (serialization.hpp:128-154): every field of the
+    scene the builders take (timing, ego start, surrounding vehicles with
+    their target speeds, tracking weights, limits, prediction constant and the
+    reference shaping parameters)."""
+    d = {"total_time": float(spec.total_time), "shared_times": [float(t) for t in spec.shared_times],
+         "horizon": int(spec.horizon), "ego_start": [float(v) for v in spec.ego_start],
+         "vehicles": [{"position": [float(v.position[0]), float(v.position[1])], "heading": float(v.heading),
+                       "speed": float(v.speed), "target_speeds": [float(t) for t in v.target_speeds]}
+                      for v in spec.vehicles],
+         "state_weights": [float(v) for v in spec.state_weights],
+         "input_weights": [float(v) for v in spec.input_weights],
+         "terminal_weights": [float(v) for v in spec.terminal_weights]}
+    for k in _SPEC_SCALARS:
+        d[k] = float(getattr(spec, k))
     return d
+
+
+def scenario_spec_from_json(j: dict) -> ScenarioSpec:
+    """scenario_spec_from_json (serialization.hpp:156-197): starts from the
+    ScenarioSpec defaults (scenarios.hpp:25-47: no vehicles) and takes every
+    key present; vectors must have their full length (the reference's
+    .at(i) throws std::out_of_range, here IndexError)."""
+    spec = ScenarioSpec()
+    kw = {}
+    if "total_time" in j:
+        kw["total_time"] = float(j["total_time"])
+    if "shared_times" in j:
+        kw["shared_times"] = tuple(float(t) for t in j["shared_times"])
+    if "horizon" in j:
+        kw["horizon"] = int(j["horizon"])
+    if "ego_start" in j:
+        e = j["ego_start"]
+        kw["ego_start"] = (float(e[0]), float(e[1]), float(e[2]), float(e[3]))
+    if "vehicles" in j:
+        kw["vehicles"] = tuple(SurroundingVehicle((float(v["position"][0]), float(v["position"][1])),
+                                                  float(v["heading"]), float(v["speed"]),
+                                                  tuple(float(t) for t in v["target_speeds"]))
+                               for v in j["vehicles"])
+    for key in ("state_weights", "terminal_weights"):
+        if key in j:
+            w = j[key]
+            kw[key] = (float(w[0]), float(w[1]), float(w[2]), float(w[3]))
+    if "input_weights" in j:
+        w = j["input_weights"]
+        kw["input_weights"] = (float(w[0]), float(w[1]))
+    for k in _SPEC_SCALARS:
+        if k in j:
+            kw[k] = float(j[k])
+    return dataclasses.replace(spec, **kw)
 
 
 def scenario_artifacts_to_json(problem: BmpcProblem) -> dict:
@@ -161,5 +190,6 @@ def scenario_artifacts_to_json(problem: BmpcProblem) -> dict:
 
 
 __all__ = ["dumps", "tree_spec_to_json", "tree_from_json", "solver_options_from_json", "solver_options_to_json",
-           "report_to_json", "scenario_spec_to_json", "scenario_artifacts_to_json", "tree_branchings",
+           "report_to_json", "scenario_spec_to_json", "scenario_spec_from_json", "scenario_artifacts_to_json",
+           "tree_branchings",
            "RECORD_KEYS", "TIME_KEYS"]

@@ -10,19 +10,20 @@ a brute-force KKT solve of the tree QP — or with the other GPU strategy:
     tree-qp         GPU tree solve vs dense KKT solve of the tree QP                 1e-7  (:225-261)
     cross-strategy  GPU scan vs GPU team sweep vs host Riccati (dx, du)              1e-6  (:263-300)
 
+    associativity   GPU combine_bwd / combine_fwd, (a+b)+c vs a+(b+c)             1e-9  (:110-137)
+    condensing      GPU condensed shared segment vs GPU tree scan vs host Riccati 1e-7  (:141-223)
+
 `mutate="scan-sign"` flips the sign of the dynamics offsets fed to the GPU
 scan only (verification.hpp:31-36); scan-riccati must then fail (harness
-sanity). The reference's `associativity` and `condensing` suites exercise
-single combine calls and the condensed strategy, which have no GPU entry
-point here; they are reported as not run. Random data: numpy
-default_rng(seed) with the reference's distributions (oracles.hpp:39-83).
+sanity). Random data: numpy default_rng(seed) with the reference's
+distributions (oracles.hpp:39-83).
 """
 import dataclasses
 from typing import List, Optional, Sequence
 
 import numpy as np
 
-from . import Context, build_tree, default_context, lqr_tree, set_seq_max_len
+from . import Context, build_tree, default_context, lqr_elements, lqr_tree, set_lqr_strategy, set_seq_max_len
 
 SUITES = ("scan-riccati", "forward", "associativity", "condensing", "tree-qp", "cross-strategy")
 _SWEEP_ALL = 1 << 30  # seq_max_len: every segment takes the team Riccati sweep
@@ -246,6 +247,85 @@ def check_tree_qp(ctx: Context, seed: int = 12349) -> CheckResult:
     return res
 
 
+# Element dims compiled for the kernel-level primitives (the reference draws
+# nx in [2, 4], nu in [1, 3]; these are its combinations the library builds).
+_ASSOC_DIMS = ((2, 1), (2, 2), (3, 2), (4, 1), (4, 2))
+
+
+def _rel1(a, b) -> float:
+    """relative_error (oracles.hpp): |a - b| / max(1, |b|)."""
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1.0))
+
+
+def check_associativity(ctx: Context, seed: int = 12347, triples: int = 1000) -> CheckResult:
+    """(a (+) b) (+) c vs a (+) (b (+) c) for the backward elements of random
+    stages (init_bwd_element) and for random forward affine maps, every
+    combination on the GPU (bmpc_lqr_elements)."""
+    res = CheckResult("associativity", False, 0.0, 1e-9)
+    rng = np.random.default_rng(seed)
+    per = max(1, triples // len(_ASSOC_DIMS))
+    for nx, nu in _ASSOC_DIMS:
+        st = np.stack([random_stage(rng, nx, nu) for _ in range(3 * per)])
+        e = lqr_elements("init_bwd", nx, nu, st, ctx=ctx)
+        a, b, c = e[:per], e[per:2 * per], e[2 * per:]
+        left = lqr_elements("combine_bwd", nx, nu, lqr_elements("combine_bwd", nx, nu, a, b, ctx=ctx), c, ctx=ctx)
+        right = lqr_elements("combine_bwd", nx, nu, a, lqr_elements("combine_bwd", nx, nu, b, c, ctx=ctx), ctx=ctx)
+        n2 = nx * nx
+        blocks = ((0, n2), (n2, n2 + nx), (n2 + nx, 2 * n2 + nx), (2 * n2 + nx, 3 * n2 + nx),
+                  (3 * n2 + nx, 3 * n2 + 2 * nx))  # P p C A c
+        for t in range(per):
+            for lo, hi in blocks:
+                res.max_error = max(res.max_error, _rel1(left[t, lo:hi], right[t, lo:hi]))
+        f = np.concatenate([rng.uniform(-1, 1, (3 * per, nx * nx)), rng.uniform(-1, 1, (3 * per, nx))], axis=1)
+        fa, fb, fc = f[:per], f[per:2 * per], f[2 * per:]
+        fl = lqr_elements("combine_fwd", nx, nu, lqr_elements("combine_fwd", nx, nu, fa, fb, ctx=ctx), fc, ctx=ctx)
+        fr = lqr_elements("combine_fwd", nx, nu, fa, lqr_elements("combine_fwd", nx, nu, fb, fc, ctx=ctx), ctx=ctx)
+        for t in range(per):
+            res.max_error = max(res.max_error, _rel1(fl[t, :n2], fr[t, :n2]), _rel1(fl[t, n2:], fr[t, n2:]))
+    res.detail = "%d triples per combinator on the GPU" % (per * len(_ASSOC_DIMS))
+    res.passed = res.max_error <= res.tolerance
+    return res
+
+
+def check_condensing(ctx: Context, seed: int = 12348) -> CheckResult:
+    """The condensed shared segment (scan_condensed, solver.hpp:297-307) on
+    the GPU: its open-loop inputs k = u at every shared node must equal the
+    inputs of the tree Riccati solution along its rollout (the same strictly
+    convex QP) — against the GPU tree scan and the host Riccati recursion —
+    on the reference's three small trees and on a path condensed against a
+    late branching (verification.hpp:141-223: path 1e-8, tree 1e-7)."""
+    res = CheckResult("condensing", False, 0.0, 1e-7)
+    rng = np.random.default_rng(seed)
+    trees = [build_tree(6, [(4, 2, [0.5, 0.5])]), build_tree(5, [(2, 3, [0.3, 0.4, 0.3])]),
+             build_tree(6, [(2, 2, [0.5, 0.5]), (4, 2, [0.25, 0.75])]), build_tree(7, [(6, 2, [0.5, 0.5])])]
+    shared_nodes = 0
+    try:
+        for tree in trees:
+            nx, nu = 3, 2
+            stage, defect, leaf = random_tree_models(rng, tree, nx, nu)
+            x0 = rng.uniform(-1, 1, nx)
+            set_lqr_strategy(ctx, "scan-condensed")
+            cond = lqr_tree(tree, nx, nu, stage, defect, leaf, 0.0, x0, ctx=ctx)
+            set_lqr_strategy(ctx, "scan-tree-riccati")
+            scan = lqr_tree(tree, nx, nu, stage, defect, leaf, 0.0, x0, ctx=ctx)
+            _, _, K, k = host_riccati(tree, nx, nu, stage, defect, leaf)
+            _, hdu = host_rollout(tree, nx, nu, stage, defect, K, k, x0)
+            m = int(tree.step_begin[tree.last_branch_step + 1])  # nodes with step <= N_b
+            for i in range(m):
+                u = cond["k"][i]
+                assert np.all(cond["K"][i] == 0.0), "condensed policies must be open loop"
+                res.max_error = max(res.max_error, _rel1(u, scan["du"][i]), _rel1(u, hdu[i]))
+            for i in range(tree.node_count):  # the rollouts coincide everywhere
+                res.max_error = max(res.max_error, _rel1(cond["dx"][i], scan["dx"][i]))
+            shared_nodes += m
+    finally:
+        set_lqr_strategy(ctx, "scan-tree-riccati")
+    res.detail = "%d shared nodes on 4 trees vs GPU tree scan and host Riccati" % shared_nodes
+    res.passed = res.max_error <= res.tolerance
+    return res
+
+
 def check_cross_strategy(ctx: Context, seed: int = 12350) -> CheckResult:
     res = CheckResult("cross-strategy", False, 0.0, 1e-6)
     rng = np.random.default_rng(seed)
@@ -283,9 +363,10 @@ def run_suites(names: Sequence[str] = (), mutate: Optional[str] = None, ctx: Opt
         out.append(check_scan_vs_riccati(ctx, seed, mutate_scan_sign=mutate == "scan-sign"))
     if wants("forward"):
         out.append(check_forward_scan(ctx, seed + 1))
-    for n in ("associativity", "condensing"):
-        if wants(n) and names:  # explicitly requested: say why it does not run
-            out.append(CheckResult(n, True, 0.0, 0.0, "no GPU entry point (see tests/test_oracle.py)"))
+    if wants("associativity"):
+        out.append(check_associativity(ctx, seed + 2))
+    if wants("condensing"):
+        out.append(check_condensing(ctx, seed + 3))
     if wants("tree-qp"):
         out.append(check_tree_qp(ctx, seed + 4))
     if wants("cross-strategy"):

@@ -165,3 +165,26 @@ def test_run_presets_match_reference(tmp_path, monkeypatch, solver):
     assert row[-1] == "converged"
     assert int(row[6]) == rep["inner_iterations"]
     assert abs(float(row[7]) - rep["final_cost"]) <= 1e-8 * max(1.0, abs(rep["final_cost"]))
+
+
+@pytest.mark.gpu
+def test_run_is_reproducible_except_timing(tmp_path):
+    """cli_reproducible (tests/CMakeLists.txt:39-44): the same config and seed
+    run twice give identical CSVs once the timing columns are cut away
+    (`cut -d, -f1-9,16`: keep columns 1-9 and 16). Custom (random LQ, seeded
+    mt19937_64) and scenario sweeps, with the hypmsilqr preset too."""
+    cfgs = [{"experiment": "custom", "solver": "pmsilqr", "horizons": [10], "leaf_counts": [2], "repetitions": 1,
+             "seed": 3},
+            {"experiment": "horizon-sweep", "horizons": [31, 63], "repetitions": 2},
+            {"experiment": "horizon-sweep", "horizons": [63], "solver": "hypmsilqr"}]
+    for n, cfg in enumerate(cfgs):
+        runs = []
+        for rep in ("a", "b"):
+            out = tmp_path / f"r{n}{rep}.csv"
+            p = tmp_path / "c.json"
+            p.write_text(json.dumps(dict(cfg, output=str(out))))
+            assert cli.run_command(str(p), out=io.StringIO(), err=io.StringIO()) == 0
+            lines = out.read_text().splitlines()
+            runs.append([",".join(r.split(",")[:9] + [r.split(",")[15]]) for r in lines])
+        assert runs[0] == runs[1]
+        assert len(runs[0]) >= 2 and runs[0][1].endswith("converged")

@@ -59,12 +59,58 @@ def test_solver_options_flat_keys():  # test_serialization.cpp:25-43
     assert back == B.SolverOptions(reg_init=1e-3, alpha_levels=7)
 
 
-def test_scenario_spec_json():  # test_serialization.cpp:45-57 (the fields the builders take)
-    j = S.scenario_spec_to_json(B.intersection_spec(31, 5.0, 0.2))
+def test_scenario_spec_json():  # test_serialization.cpp:45-57 (round trip of every field)
+    spec = B.intersection_spec(31, 5.0, 0.2)
+    j = S.scenario_spec_to_json(spec)
     assert j["horizon"] == 31 and j["total_time"] == 5.0 and j["shared_times"] == [0.2]
     assert len(j["vehicles"]) == 2 and j["ego_start"][1] == -20.0
-    with pytest.raises(ValueError):
-        S.scenario_spec_to_json(B.multistage_spec(10, [(1, 2)]))
+    back = S.scenario_spec_from_json(json.loads(S.dumps(j)))
+    assert S.scenario_spec_to_json(back) == j
+    # Defaults are ScenarioSpec{}'s (no vehicles), not a preset's.
+    d = S.scenario_spec_from_json({"horizon": 12})
+    assert d.horizon == 12 and d.vehicles == () and d.total_time == 10.0 and d.shared_times == (0.1,)
+    with pytest.raises(IndexError):  # the reference's .at(3) throws out_of_range
+        S.scenario_spec_from_json({"ego_start": [0.0, 1.0, 2.0]})
+
+
+@pytest.mark.parametrize("kind", ["intersection", "latency"])
+def test_scenario_spec_from_json_builds_reference_problem(kind):
+    """A scene given as JSON — its own vehicles, target speeds, weights, limits
+    and timing — built by the in-library builders equals the reference
+    builders' problem from the same JSON (oracle/_ref/gen_ref spec-*,
+    tests/make_golden_specs.py): spec round trip and every node's step,
+    parent, weight, tracking reference and vehicle predictions."""
+    with gzip.open(os.path.join(GOLDEN, f"gen_spec_{kind}.json.gz"), "rt") as f:
+        ref = json.load(f)
+    spec = S.scenario_spec_from_json(ref["input_spec"])
+    assert S.scenario_spec_to_json(spec) == ref["spec"]
+    if kind == "intersection":
+        p = B.build_intersection_case(spec, ref["v1_count"], ref["v2_count"])
+    else:
+        p = B.build_latency_case(spec)
+    got = S.scenario_artifacts_to_json(p)
+    assert got["tree"] == ref["problem"]["tree"]
+    assert len(got["nodes"]) == len(ref["problem"]["nodes"])
+    for a, b in zip(got["nodes"], ref["problem"]["nodes"]):
+        assert a == b
+    w = p.model
+    assert tuple(w.state_weights)[::5] == spec.state_weights and w.safety_radius == spec.safety_radius
+    np.testing.assert_array_equal(p.initial_state, spec.ego_start)
+
+
+def test_scenario_builders_reject_bad_scenes():
+    spec = B.intersection_spec()
+    one = B.ScenarioSpec(vehicles=spec.vehicles[:1])
+    with pytest.raises(ValueError, match="need 2 vehicles with enough targets"):
+        B.build_intersection_case(one, 2, 2)
+    short = B.dataclasses.replace(spec, vehicles=(spec.vehicles[0], B.SurroundingVehicle((0.0, -10.0), 1.5, 5.0,
+                                                                                          (5.0, 1.0))))
+    with pytest.raises(ValueError, match="need 2 vehicles with enough targets"):
+        B.build_intersection_case(short, 2, 3)  # 6 leaves: the lead vehicle needs 3 target speeds
+    lat = B.latency_spec(0.5)
+    with pytest.raises(ValueError, match="need one vehicle with 2 targets"):
+        B.build_latency_case(B.ScenarioSpec(shared_times=lat.shared_times, total_time=5.0, horizon=255,
+                                            vehicles=spec.vehicles))
 
 
 def test_report_iteration_arrays():  # test_serialization.cpp:59-76
