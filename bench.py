@@ -277,13 +277,16 @@ def main():
     x0_host = np.array([p.initial_state for p in probs])
     e2e_steps = max(1, min(args.steps, 3))
 
-    def e2e_run(full_upload):
+    def e2e_run(full_upload, scene=False):
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         h2d = d2h = 0
         for _ in range(e2e_steps):
-            h2d = batch.set_models() if full_upload else batch.set_initial_states(x0_host)
+            if scene:  # device-side scene generation from the spec, then the measured states
+                h2d = batch.set_scenes(spec) + batch.set_initial_states(x0_host)
+            else:
+                h2d = batch.set_models() if full_upload else batch.set_initial_states(x0_host)
             batch.solve()
             _, d2h = batch.results(xh, uh, want_reports=True, as_array=True)
         te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
@@ -291,6 +294,7 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         return world * count * e2e_steps / float(te.item()), h2d, d2h
 
+    e2e_scene, h2d_scene, _ = e2e_run(False, scene=True)
     e2e_full, h2d_full, _ = e2e_run(True)
     e2e_value, h2d, d2h = e2e_run(False)
 
@@ -321,6 +325,10 @@ def main():
             "e2e_full_upload": {"value": e2e_full, "unit": UNIT, "h2d_bytes_per_step": int(h2d_full),
                                 "d2h_bytes_per_step": int(d2h),
                                 "call": "set_models(every instance's node data) + solve + results"},
+            "e2e_scene": {"value": e2e_scene, "unit": UNIT, "h2d_bytes_per_step": int(h2d_scene),
+                          "d2h_bytes_per_step": int(d2h),
+                          "call": "set_scenes(scene spec: references and predictions generated on the GPU) + "
+                                  "set_initial_states + solve + results"},
             "gpu_launches": int(launches),
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic,

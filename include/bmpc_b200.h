@@ -249,6 +249,20 @@ int bmpc_batch_set_models(bmpc_batch* batch, const bmpc_model_desc* models, size
  * h2d_bytes (optional) receives the bytes copied. */
 int bmpc_batch_set_initial_states(bmpc_batch* batch, const double* x0, size_t* h2d_bytes);
 int bmpc_batch_replicate(bmpc_batch* batch);
+/* Device-side scene generation (the receding-horizon call where the ego state
+ * and the surrounding vehicles change every control step): from scene specs
+ * (one per instance, or n_specs = 1 for all), the device computes every
+ * node's tracking reference (left_turn_reference / the latency references,
+ * scenarios.hpp:201-214, 416-441), the vehicle predictions
+ * (predict_vehicles, :87-113, with the family's branch choices), the model
+ * scalars and x0 = ego_start. Each spec must imply the batch's tree (same
+ * horizon and branch steps); family as in bmpc_scenario. h2d_bytes receives
+ * the bytes uploaded (the specs and model scalars only). Async. */
+int bmpc_batch_set_scenes(bmpc_batch* batch, int family, const bmpc_scenario_spec* specs, int n_specs, int v1,
+                          int v2, size_t* h2d_bytes);
+/* Per-node scene data of one instance (device -> host): reference [node][4],
+ * vehicles [node][num_vehicles][2], x0 [nx]; any pointer may be NULL. */
+int bmpc_batch_scene(bmpc_batch* batch, int instance, double* reference, double* vehicles, double* x0);
 /* Per-instance thread-block shape: `threads` per block with at least
  * `min_blocks` resident per SM (compiled variants only). */
 int bmpc_batch_set_launch(bmpc_batch* batch, int threads, int min_blocks);

@@ -594,6 +594,26 @@ class Batch:
             return np.ctypeslib.as_array(reps), b.value
         return [_report(r) for r in reps], b.value
 
+    def set_scenes(self, specs, family: int = SCENARIO_INTERSECTION, v1: int = 2, v2: int = 2) -> int:
+        """Device-side scene generation (bmpc_batch_set_scenes): every node's
+        tracking reference and vehicle predictions, the model scalars and
+        x0 = ego_start computed on the GPU from one ScenarioSpec per instance
+        (or a single shared one); returns the H2D bytes (the specs only)."""
+        specs = [specs] if isinstance(specs, ScenarioSpec) else list(specs)
+        arr = (_SpecC * len(specs))(*[s._c() for s in specs])
+        b = C.c_size_t()
+        _check(lib().bmpc_batch_set_scenes(self._h, int(family), arr, len(specs), int(v1), int(v2), C.byref(b)))
+        return b.value
+
+    def scene(self, instance: int) -> dict:
+        """The per-node scene data of one instance (reference, vehicles, x0)."""
+        nv = self.problems[0].model.num_vehicles
+        ref = np.zeros((self.n, 4))
+        veh = np.zeros((self.n, nv, 2))
+        x0 = np.zeros(self.nx)
+        _check(lib().bmpc_batch_scene(self._h, int(instance), _ptr(ref), _ptr(veh) if nv else None, _ptr(x0)))
+        return {"reference": ref, "vehicles": veh, "initial_state": x0}
+
     def set_initial_states(self, x0: np.ndarray) -> int:
         """Upload new initial states [count, nx] over the resident scenario data
         (bmpc_batch_set_initial_states); returns H2D bytes."""

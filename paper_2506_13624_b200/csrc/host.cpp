@@ -769,6 +769,7 @@ struct bmpc_batch {
   ~bmpc_batch() {
     if (h_stage) cudaFreeHost(h_stage);
     if (h_pack) cudaFreeHost(h_pack);
+    if (h_specs) cudaFreeHost(h_specs);
   }
   int cta_min_blocks{1};
   // Schedule of batches with more instances than SMs (see probe_for):
@@ -778,6 +779,13 @@ struct bmpc_batch {
   bool grid_mode{false};
   int grid_blocks{0};
   DevBuf cond;  // condensed-strategy scratch, allocated by the first scan_condensed solve
+  // Device-side scenario generation (bmpc_batch_set_scenes): tree arrays,
+  // branch choices, per-instance spec upload and vehicle-speed scratch.
+  DevBuf scene_ints, scene_specs, scene_speed;
+  int scene_nb{-1}, tree_horizon{0};
+  std::vector<int> branch_steps, branch_arity;
+  bmpc_scenario_spec* h_specs{nullptr};  // pinned
+  size_t h_specs_cap{0};
 };
 
 namespace {
@@ -1163,6 +1171,156 @@ int bmpc_batch_set_models(bmpc_batch* b, const bmpc_model_desc* models, size_t* 
     ck(cudaMemcpyAsync(b->mps.p, b->h_mps.data(), b->h_mps.size() * sizeof(ModelParams), cudaMemcpyHostToDevice, s),
        "h2d");
     if (h2d_bytes) *h2d_bytes = bytes_data + C * x0s * sizeof(double) + b->h_mps.size() * sizeof(ModelParams);
+    return BMPC_OK;
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
+}
+
+int bmpc_batch_set_scenes(bmpc_batch* b, int family, const bmpc_scenario_spec* specs, int n_specs, int v1, int v2,
+                          size_t* h2d_bytes) {
+  try {
+    if (!b || !specs || (n_specs != 1 && n_specs != b->count)) return fail(BMPC_ERR_INVALID, "bad arguments");
+    if (b->kind != BMPC_MODEL_UNICYCLE) return fail(BMPC_ERR_INVALID, "scenes need a unicycle batch");
+    if (family != BMPC_SCENARIO_INTERSECTION && family != BMPC_SCENARIO_LATENCY && family != BMPC_SCENARIO_MULTISTAGE)
+      return fail(BMPC_ERR_INVALID, "unknown scenario family");
+    ck(cudaSetDevice(b->ctx->device), "cudaSetDevice");
+    cudaStream_t s = b->ctx->stream;
+    const Plan& pl = *b->plan;
+    const int n = pl.n;
+    // The tree the batch was created with: its horizon, branch steps and arities.
+    if (b->scene_nb < 0) {
+      // Rebuild the host tree arrays from the plan (BFS: children contiguous).
+      std::vector<int> ts(static_cast<size_t>(n), 0), fc(static_cast<size_t>(n), -1), cc(static_cast<size_t>(n), 0);
+      std::vector<int> par(static_cast<size_t>(n), -1);
+      ck(cudaMemcpy(par.data(), pl.topo.parent, n * sizeof(int), cudaMemcpyDeviceToHost), "d2h");
+      ck(cudaMemcpy(fc.data(), pl.topo.first_child, n * sizeof(int), cudaMemcpyDeviceToHost), "d2h");
+      ck(cudaMemcpy(cc.data(), pl.topo.nchild, n * sizeof(int), cudaMemcpyDeviceToHost), "d2h");
+      for (int i = 1; i < n; ++i) ts[static_cast<size_t>(i)] = ts[static_cast<size_t>(par[static_cast<size_t>(i)])] + 1;
+      const int horizon = n ? ts[static_cast<size_t>(n) - 1] : 0;
+      std::vector<int> sb(static_cast<size_t>(horizon) + 2, 0);
+      for (int i = 0; i < n; ++i) sb[static_cast<size_t>(ts[static_cast<size_t>(i)]) + 1] = i + 1;
+      for (int k = 1; k <= horizon + 1; ++k) sb[static_cast<size_t>(k)] = std::max(sb[static_cast<size_t>(k)], sb[static_cast<size_t>(k) - 1]);
+      b->branch_steps.clear();
+      b->branch_arity.clear();
+      for (int i = 0; i < n; ++i)
+        if (cc[static_cast<size_t>(i)] > 1 &&
+            (b->branch_steps.empty() || b->branch_steps.back() != ts[static_cast<size_t>(i)])) {
+          b->branch_steps.push_back(ts[static_cast<size_t>(i)]);
+          b->branch_arity.push_back(cc[static_cast<size_t>(i)]);
+        }
+      b->tree_horizon = horizon;
+      const int nb = static_cast<int>(b->branch_steps.size());
+      bmpc_tree t{};
+      t.node_count = n;
+      t.time_step = ts.data();
+      t.first_child = fc.data();
+      t.child_count = cc.data();
+      const auto ch = branch_choices(t, b->branch_steps);
+      std::vector<int> ints;
+      ints.insert(ints.end(), sb.begin(), sb.end());
+      for (int i = 0; i < n; ++i)
+        for (int k = 0; k < nb; ++k) ints.push_back(ch[static_cast<size_t>(i)][static_cast<size_t>(k)]);
+      b->scene_ints = DevBuf(std::max<size_t>(ints.size(), 1) * sizeof(int));
+      ck(cudaMemcpy(b->scene_ints.p, ints.data(), ints.size() * sizeof(int), cudaMemcpyHostToDevice), "h2d");
+      b->scene_nb = nb;
+      b->scene_speed = DevBuf(static_cast<size_t>(b->count) * n * kMaxVehicles * sizeof(double));
+    }
+    const int nb = b->scene_nb;
+    // Every spec must give the batch's tree: same horizon and branch steps (the builders' rounding).
+    for (int i = 0; i < n_specs; ++i) {
+      const bmpc_scenario_spec& sp = specs[i];
+      if (sp.horizon != b->tree_horizon || sp.n_vehicles != b->nv)
+        return fail(BMPC_ERR_INVALID, "scene " + std::to_string(i) + ": horizon / vehicle count differ from the batch");
+      if (sp.n_vehicles < 0 || sp.n_vehicles > kMaxVehicles || sp.n_shared < 1 || sp.n_shared > 2 || !(sp.total_time > 0))
+        return fail(BMPC_ERR_INVALID, "scene " + std::to_string(i) + ": invalid spec");
+      for (int v = 0; v < sp.n_vehicles; ++v)
+        if (sp.vehicles[v].n_targets < 0 || sp.vehicles[v].n_targets > BMPC_MAX_TARGETS)
+          return fail(BMPC_ERR_INVALID, "scene " + std::to_string(i) + ": invalid target count");
+      const double dt = sp.total_time / sp.horizon;
+      std::vector<int> steps;
+      if (family == BMPC_SCENARIO_INTERSECTION) {
+        if (sp.n_vehicles != 2 || sp.vehicles[0].n_targets < v1 || sp.vehicles[1].n_targets < v2 || v1 < 1 || v2 < 1)
+          return fail(BMPC_ERR_INVALID, "build_intersection_case: need 2 vehicles with enough targets");
+        if (v1 * v2 > 1) steps.push_back(static_cast<int>(std::lround(sp.shared_times[0] / dt)));
+        if ((v1 * v2 > 1) != (nb == 1) || (nb == 1 && b->branch_arity[0] != v1 * v2))
+          return fail(BMPC_ERR_INVALID, "scene " + std::to_string(i) + ": v1 * v2 differs from the batch tree's arity");
+      } else if (family == BMPC_SCENARIO_LATENCY) {
+        if (sp.n_shared != 2 || sp.n_vehicles != 1 || sp.vehicles[0].n_targets != 2)
+          return fail(BMPC_ERR_INVALID, "build_latency_case: need one vehicle with 2 targets and T_sh0 < T_sh1 < T");
+        steps = {static_cast<int>(std::lround(sp.shared_times[0] / dt)),
+                 static_cast<int>(std::lround(sp.shared_times[1] / dt))};
+      } else {
+        if (sp.n_vehicles != 2) return fail(BMPC_ERR_INVALID, "multistage: need 2 vehicles");
+        steps = b->branch_steps;  // the batch tree's stages; stage j reveals vehicle j mod 2's target
+        for (int j = 0; j < nb; ++j)
+          if (sp.vehicles[j % 2].n_targets < b->branch_arity[static_cast<size_t>(j)])
+            return fail(BMPC_ERR_INVALID, "multistage: a revealing vehicle has fewer targets than the arity");
+      }
+      if (steps != b->branch_steps)
+        return fail(BMPC_ERR_INVALID, "scene " + std::to_string(i) + ": its branch steps differ from the batch's tree");
+    }
+    // Per-instance model scalars (host copies -> one upload), then the specs.
+    for (int i = 0; i < b->count; ++i) {
+      const bmpc_scenario_spec& sp = specs[n_specs == 1 ? 0 : i];
+      ModelParams& mp = b->h_mps[static_cast<size_t>(i)];
+      mp.dt = sp.total_time / sp.horizon;
+      std::memset(mp.Wx, 0, sizeof mp.Wx);
+      std::memset(mp.Wu, 0, sizeof mp.Wu);
+      std::memset(mp.Wf, 0, sizeof mp.Wf);
+      for (int j = 0; j < 4; ++j) mp.Wx[5 * j] = sp.state_weights[j], mp.Wf[5 * j] = sp.terminal_weights[j];
+      for (int j = 0; j < 2; ++j) mp.Wu[3 * j] = sp.input_weights[j];
+      mp.a_max = sp.accel_limit;
+      mp.w_max = sp.yaw_rate_limit;
+      mp.radius = sp.safety_radius;
+      mp.w_diag = std::getenv("BMPC_DENSE_MODEL") ? 0 : 1;
+    }
+    ck(cudaStreamSynchronize(s), "staging reuse");
+    if (b->h_specs_cap < static_cast<size_t>(n_specs)) {
+      if (b->h_specs) cudaFreeHost(b->h_specs);
+      ck(cudaMallocHost(&b->h_specs, static_cast<size_t>(n_specs) * sizeof(bmpc_scenario_spec)), "pinned");
+      b->h_specs_cap = static_cast<size_t>(n_specs);
+      b->scene_specs = DevBuf(static_cast<size_t>(n_specs) * sizeof(bmpc_scenario_spec));
+    }
+    std::memcpy(b->h_specs, specs, static_cast<size_t>(n_specs) * sizeof(bmpc_scenario_spec));
+    const size_t spec_bytes = static_cast<size_t>(n_specs) * sizeof(bmpc_scenario_spec);
+    ck(cudaMemcpyAsync(b->scene_specs.p, b->h_specs, spec_bytes, cudaMemcpyHostToDevice, s), "h2d");
+    ck(cudaMemcpyAsync(b->mps.p, b->h_mps.data(), b->h_mps.size() * sizeof(ModelParams), cudaMemcpyHostToDevice, s),
+       "h2d");
+    SceneTree tr{};
+    tr.n = n;
+    tr.nb = nb;
+    tr.first_child = pl.topo.first_child;
+    tr.child_count = pl.topo.nchild;
+    tr.step_begin = b->scene_ints.as<int>();
+    tr.choices = b->scene_ints.as<int>() + (b->tree_horizon + 2);
+    ck(launch_scene(family, b->count, b->scene_specs.as<bmpc_scenario_spec>(), n_specs == 1 ? 1 : 0, tr,
+                    std::max(v2, 1), b->model_data.as<double>(), b->node_data_doubles, align2(static_cast<size_t>(n) * 4),
+                    b->scene_speed.as<double>(), b->x0.as<double>(), align2(static_cast<size_t>(b->nx)), s),
+       "scene");
+    ++b->ctx->launches;
+    if (h2d_bytes) *h2d_bytes = spec_bytes + b->h_mps.size() * sizeof(ModelParams);
+    return BMPC_OK;
+  } catch (const std::exception& e) {
+    return fail(BMPC_ERR_CUDA, e.what());
+  }
+}
+
+int bmpc_batch_scene(bmpc_batch* b, int instance, double* reference, double* vehicles, double* x0) {
+  try {
+    if (!b || instance < 0 || instance >= b->count || b->kind != BMPC_MODEL_UNICYCLE)
+      return fail(BMPC_ERR_INVALID, "bad instance");
+    ck(cudaSetDevice(b->ctx->device), "cudaSetDevice");
+    ck(cudaStreamSynchronize(b->ctx->stream), "sync");
+    const size_t n = static_cast<size_t>(b->plan->n);
+    const double* md = b->model_data.as<double>() + static_cast<size_t>(instance) * b->node_data_doubles;
+    if (reference) ck(cudaMemcpy(reference, md, n * 4 * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+    if (vehicles && b->nv)
+      ck(cudaMemcpy(vehicles, md + align2(n * 4), n * b->nv * 2 * sizeof(double), cudaMemcpyDeviceToHost), "d2h");
+    if (x0)
+      ck(cudaMemcpy(x0, b->x0.as<double>() + static_cast<size_t>(instance) * align2(static_cast<size_t>(b->nx)),
+                    b->nx * sizeof(double), cudaMemcpyDeviceToHost),
+         "d2h");
     return BMPC_OK;
   } catch (const std::exception& e) {
     return fail(BMPC_ERR_CUDA, e.what());

@@ -7,6 +7,8 @@
 
 #include <cuda_runtime.h>
 
+#include "bmpc_b200.h"
+
 namespace bmpc_b200 {
 
 struct Topo;
@@ -90,6 +92,22 @@ size_t sizeof_dev_result();
 size_t sizeof_dev_record();
 
 constexpr int kRedSlotsHost = 64;
+
+// scene.cu: device-side scenario generation (bmpc_batch_set_scenes).
+using SceneSpec = bmpc_scenario_spec;
+using SceneVehicle = bmpc_vehicle;
+constexpr int kSceneIntersection = BMPC_SCENARIO_INTERSECTION, kSceneLatency = BMPC_SCENARIO_LATENCY,
+              kSceneMultistage = BMPC_SCENARIO_MULTISTAGE;
+struct SceneTree {
+  int n, nb;               // nodes, branchings
+  const int* first_child;  // [n]
+  const int* child_count;  // [n]
+  const int* step_begin;   // [horizon + 2]
+  const int* choices;      // [n][nb] child index taken at each branching on the node's path, -1 before it
+};
+cudaError_t launch_scene(int family, int count, const SceneSpec* d_specs, int shared_spec, const SceneTree& tree,
+                         int v2_count, double* model_data, size_t node_data_doubles, size_t veh_offset,
+                         double* speed_scratch, double* x0_out, size_t x0_stride, cudaStream_t stream);
 
 // util.cu
 cudaError_t launch_order_by_key(const DevResume* d_resume, int count, int* d_order, cudaStream_t stream);
