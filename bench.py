@@ -36,15 +36,20 @@ METRIC = "BMPC solve latency (ms) vs horizon×scenarios; batched solves/sec at 1
 UNIT = "solves/s"
 WORKLOAD = "cfg4: batched intersection_spec(63,10,0.1) 2x2 (250 nodes) x 4096 instances per GPU, perturbed x0"
 PER_GPU = 4096
-# Algorithmic work per non-leaf node per inner iteration:
-# linearize 1.575 + init 0.4 + 2 combines 3.0 + feedback 0.35 + fwd 0.482
-# + EC 0.086 + evaluate x2 0.4 + line search 11 x 0.212 = 8.6 kflop.
-# The line search stops at the first round holding an accepted step size
-# (same result), so its share is counted per step size actually evaluated:
-# F_PASS per pass + F_ALPHA per evaluated alpha.
-F_NODE = 8.6e3
-F_ALPHA = 0.212e3
-F_PASS = F_NODE - 11 * F_ALPHA
+# Algorithmic FP64 work per non-leaf node per inner pass, MEASURED on the
+# reference path (oracle/flop_count.cpp: the unmodified reference compiled
+# against the Eigen shim with its opt-in flop counter, cfg0;
+# profiles/r2_flop_count.json): linearize 1543.4, evaluate 117.4 (x2),
+# backward 3451.8 (tree scan: init_bwd_element + combine_bwd) or 803.7
+# (sequential Riccati — what the GPU's team sweep executes), forward 463.8,
+# expected change 84.8, and 129.6 per line-search trial. The line search stops
+# at the first round holding an accepted step size (same result), so its share
+# is counted per step size actually evaluated: F_PASS per pass + F_ALPHA per
+# evaluated alpha. roofline.achieved uses the work-efficient count (the
+# algorithm the GPU runs); the reference-arithmetic count is reported beside it.
+F_ALPHA = 129.6
+F_PASS = 1543.4 + 2 * 117.4 + 803.7 + 463.8 + 84.8          # work-efficient (sequential Riccati backward)
+F_PASS_REF = 1543.4 + 2 * 117.4 + 3451.8 + 463.8 + 84.8      # reference arithmetic (tree-scan backward)
 
 
 def parse():
@@ -265,6 +270,7 @@ def main():
     nl = int((probs[0].tree.child_count > 0).sum())
     alpha_evals = float(sum(r.alpha_evals for r in reps))
     flops_per_launch = nl * (F_PASS * float(passes.sum()) + F_ALPHA * alpha_evals)
+    flops_ref_arith = nl * (F_PASS_REF * float(passes.sum()) + F_ALPHA * alpha_evals)
 
     # e2e: public API with host buffers, copies inside the timed region. cfg4
     # instances share the scenario (references, predictions) and differ in the
@@ -336,7 +342,11 @@ def main():
                          "traffic_source": "DRAM bytes read+written by every launch of one step, one ncu session "
                                            "(profiles/traffic.json, tools/traffic.py)",
                          "kernel_ms": kernel_ms,
-                         "algorithmic_flops_per_launch": flops_per_launch},
+                         "algorithmic_flops_per_launch": flops_per_launch,
+                         "flops_source": "per-phase FP64 flops of the reference path measured with the Eigen-shim "
+                                         "flop counter (oracle/flop_count.cpp, profiles/r2_flop_count.json); "
+                                         "work-efficient count (sequential Riccati backward, as the GPU runs it)",
+                         "achieved_reference_arithmetic": flops_ref_arith / (kernel_ms * 1e-3) / 1e12},
             "clocks": clocks.summary(),
         }
         if world == 1:
