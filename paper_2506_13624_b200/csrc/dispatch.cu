@@ -66,10 +66,10 @@ bool cta_variant_supported(int nx, int nu, int threads, int min_blocks) {
 cudaError_t launch_solve_cta(int nx, int nu, const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
                              const DevOptions& opts, int count, int threads, int min_blocks, bool seq_only,
                              cudaStream_t stream) {
-  if (opts.nonlinear_ls) {  // single-shooting kernels: one shape per (nx, nu)
+  if (opts.nonlinear_ls || opts.condensed) {  // kernels with an optional path: one shape per (nx, nu)
 #define X(a, b)           \
   if (nx == a && nu == b) \
-    return SolveLaunch<a, b>::solve_cta_nonlinear(d_topo, d_mp, d_work, opts, count, seq_only, stream);
+    return SolveLaunch<a, b>::solve_cta_special(d_topo, d_mp, d_work, opts, count, seq_only, stream);
     BMPC_SOLVE_DIMS(X)
 #undef X
     return cudaErrorInvalidValue;
@@ -94,8 +94,8 @@ cudaError_t launch_solve_grid(int nx, int nu, const Topo* d_topo, const ModelPar
                               const DevOptions& opts, double* red, int blocks, int threads, cudaStream_t stream) {
 #define X(a, b)                                                                                              \
   if (nx == a && nu == b)                                                                                    \
-    return opts.nonlinear_ls                                                                                 \
-               ? SolveLaunch<a, b>::solve_grid_nonlinear(d_topo, d_mp, d_work, opts, red, blocks, threads, stream) \
+    return (opts.nonlinear_ls || opts.condensed)                                                            \
+               ? SolveLaunch<a, b>::solve_grid_special(d_topo, d_mp, d_work, opts, red, blocks, threads, stream) \
                : SolveLaunch<a, b>::solve_grid(d_topo, d_mp, d_work, opts, red, blocks, threads, stream);
   BMPC_SOLVE_DIMS(X)
 #undef X

@@ -1438,9 +1438,10 @@ static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_input
   d.seq_wide_max = kSeqWideMax;
   d.ls_block = ls_block_for(b->ctx);
   d.fwd_scan_min = std::getenv("BMPC_FWD_SCAN_MIN") ? std::atoi(std::getenv("BMPC_FWD_SCAN_MIN")) : 0;
-  // Chunked (time-parallel) backward sweep in wide blocks, opt-in (BMPC_CHUNK_BWD=1): measured slower
-  // than the team sweep on every shape (cfg0 alone, 256 threads: 129 vs 80 us per pass).
-  d.chunk_bwd = std::getenv("BMPC_CHUNK_BWD") ? std::atoi(std::getenv("BMPC_CHUNK_BWD")) : 0;
+  // The chunked (time-parallel) backward sweep is compiled only into the
+  // kernel-level LQR entry (bmpc_lqr_tree): measured slower than the team
+  // sweep in the solve kernels (cfg0 alone, 256 threads: 129 vs 80 us per pass).
+  d.chunk_bwd = 0;
   // Strategy enums (solver.hpp:23-26; presets bench.cpp:60-83).
   if (o.backward < 0 || o.backward > 2 || o.forward < 0 || o.forward > 1 || o.line_search < 0 || o.line_search > 1)
     return fail(BMPC_ERR_INVALID, "unknown backward / forward / line_search strategy");

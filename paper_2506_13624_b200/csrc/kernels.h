@@ -57,12 +57,14 @@ struct SolveLaunch {
   static cudaError_t solve_grid(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
                                 const DevOptions& opts, double* red, int blocks, int threads, cudaStream_t stream);
   static int grid_blocks(int threads);
-  // Single-shooting line search compiled in (DevOptions::nonlinear_ls).
-  static cudaError_t solve_cta_nonlinear(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
-                                         const DevOptions& opts, int count, bool seq_only, cudaStream_t stream);
-  static cudaError_t solve_grid_nonlinear(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
-                                          const DevOptions& opts, double* red, int blocks, int threads,
-                                          cudaStream_t stream);
+  // Kernels with an optional path compiled in (DevOptions::nonlinear_ls: the
+  // single-shooting line search; DevOptions::condensed: the condensed shared
+  // segment), so the default kernels keep their register allocation.
+  static cudaError_t solve_cta_special(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
+                                       const DevOptions& opts, int count, bool seq_only, cudaStream_t stream);
+  static cudaError_t solve_grid_special(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
+                                        const DevOptions& opts, double* red, int blocks, int threads,
+                                        cudaStream_t stream);
 };
 
 // Dispatch over the compiled dimension sets (dispatch.cu).

@@ -24,7 +24,7 @@ struct BlockCtx {
 
 // THREADS x MINB trade registers for resident instances per SM:
 // registers/thread <= 65536 / (THREADS * MINB).
-template <int NX, int NU, int THREADS, int MINB, bool SEQ, bool NL = false>
+template <int NX, int NU, int THREADS, int MINB, bool SEQ, int FEAT = 0>
 __global__ void __launch_bounds__(THREADS, MINB) solve_cta_kernel(const Topo* __restrict__ topo,
                                                         const ModelParams* __restrict__ mps,
                                                         const Work* __restrict__ works, DevOptions opts,
@@ -44,14 +44,14 @@ __global__ void __launch_bounds__(THREADS, MINB) solve_cta_kernel(const Topo* __
   __syncthreads();
   // One warp per segment team when the block is wide enough (>= 4 teams).
   constexpr int kTeam = (THREADS >= 128 && team_size<NX, NU>() == 16) ? 32 : 0;
-  Solver<NX, NU, CtaGroupT<THREADS>, SEQ, kTeam, NL> s(CtaGroupT<THREADS>{&red}, ctx.topo, ctx.mp, ctx.work, opts);
+  Solver<NX, NU, CtaGroupT<THREADS>, SEQ, kTeam, FEAT> s(CtaGroupT<THREADS>{&red}, ctx.topo, ctx.mp, ctx.work, opts);
   s.tsm = dyn_smem + red_smem_bytes(THREADS);
   s.wbuf = reinterpret_cast<double*>(s.tsm);
   s.wcap = THREADS;
   s.solve();
 }
 
-template <int NX, int NU, bool NL = false>
+template <int NX, int NU, int FEAT = 0>
 __global__ void __launch_bounds__(256) solve_grid_kernel(const Topo* __restrict__ topo,
                                                          const ModelParams* __restrict__ mps,
                                                          const Work* __restrict__ works, DevOptions opts,
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) solve_grid_kernel(const Topo* __restrict_
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   red.part = reinterpret_cast<double*>(dyn_smem);
   __syncthreads();
-  Solver<NX, NU, GridGroup, false, 0, NL> s(GridGroup{&red, red_scratch, nullptr}, ctx.topo, ctx.mp, ctx.work, opts);
+  Solver<NX, NU, GridGroup, false, 0, FEAT> s(GridGroup{&red, red_scratch, nullptr}, ctx.topo, ctx.mp, ctx.work, opts);
   s.tsm = dyn_smem + red_smem_bytes(blockDim.x);
   s.wbuf = reinterpret_cast<double*>(s.tsm);
   s.wcap = blockDim.x;
@@ -84,7 +84,7 @@ __device__ void lqr_tree_body(G g, BlockCtx& ctx, double reg, double* scalars, i
   o.keep_values = 1;
   o.chunk_bwd = 1;  // long segments in 256-thread blocks: the chunked sweep (tested against the oracle here)
   extern __shared__ __align__(16) unsigned char dyn_smem[];
-  Solver<NX, NU, G> s(g, ctx.topo, dummy, ctx.work, o);
+  Solver<NX, NU, G, false, 0, kFeatCond | kFeatChunk> s(g, ctx.topo, dummy, ctx.work, o);
   s.tsm = dyn_smem + red_smem_bytes(blockDim.x);
   s.wbuf = reinterpret_cast<double*>(s.tsm);
   s.wcap = blockDim.x;
@@ -277,35 +277,56 @@ cudaError_t SolveLaunch<NX, NU>::solve_grid(const Topo* d_topo, const ModelParam
                                      dim3(threads), args, smem, stream);
 }
 
-// Single-shooting (ForwardMode::nonlinear_rollout) solves: one 256-thread
-// shape per (nx, nu), FIFO over the batch, and the whole-GPU kernel.
-template <int NX, int NU>
-cudaError_t SolveLaunch<NX, NU>::solve_cta_nonlinear(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
-                                                     const DevOptions& opts, int count, bool seq_only,
-                                                     cudaStream_t stream) {
+// Solves with an optional path (single-shooting line search, condensed shared
+// segment): one 256-thread shape per (nx, nu), FIFO over the batch, and the
+// whole-GPU kernel; FEAT selects the compiled-in paths.
+template <int NX, int NU, int FEAT>
+static cudaError_t launch_cta_feat(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
+                                   const DevOptions& opts, int count, bool seq_only, cudaStream_t stream) {
   constexpr int T = 256;
   const size_t smem = team_smem_bytes<NX, NU>(T);
   if (seq_only && team_size<NX, NU>() > 0) {
-    allow_smem(solve_cta_kernel<NX, NU, T, 1, true, true>, smem);
-    solve_cta_kernel<NX, NU, T, 1, true, true><<<count, T, smem, stream>>>(d_topo, d_mp, d_work, opts, count);
+    allow_smem(solve_cta_kernel<NX, NU, T, 1, true, FEAT>, smem);
+    solve_cta_kernel<NX, NU, T, 1, true, FEAT><<<count, T, smem, stream>>>(d_topo, d_mp, d_work, opts, count);
   } else {
-    allow_smem(solve_cta_kernel<NX, NU, T, 1, false, true>, smem);
-    solve_cta_kernel<NX, NU, T, 1, false, true><<<count, T, smem, stream>>>(d_topo, d_mp, d_work, opts, count);
+    allow_smem(solve_cta_kernel<NX, NU, T, 1, false, FEAT>, smem);
+    solve_cta_kernel<NX, NU, T, 1, false, FEAT><<<count, T, smem, stream>>>(d_topo, d_mp, d_work, opts, count);
   }
   return cudaGetLastError();
 }
 
-template <int NX, int NU>
-cudaError_t SolveLaunch<NX, NU>::solve_grid_nonlinear(const Topo* d_topo, const ModelParams* d_mp,
-                                                      const Work* d_work, const DevOptions& opts, double* red,
-                                                      int blocks, int threads, cudaStream_t stream) {
+template <int NX, int NU, int FEAT>
+static cudaError_t launch_grid_feat(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
+                                    const DevOptions& opts, double* red, int blocks, int threads,
+                                    cudaStream_t stream) {
   DevOptions o = opts;
   void* args[] = {&d_topo, &d_mp, &d_work, &o, &red};
   const size_t smem = team_smem_bytes<NX, NU>(threads);
-  const int fit = max_coresident(solve_grid_kernel<NX, NU, true>, threads, smem);
+  const int fit = max_coresident(solve_grid_kernel<NX, NU, FEAT>, threads, smem);
   if (blocks > fit) blocks = fit;  // co-residency of this variant (red holds >= blocks rows)
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(solve_grid_kernel<NX, NU, true>), dim3(blocks),
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(solve_grid_kernel<NX, NU, FEAT>), dim3(blocks),
                                      dim3(threads), args, smem, stream);
+}
+
+template <int NX, int NU>
+cudaError_t SolveLaunch<NX, NU>::solve_cta_special(const Topo* d_topo, const ModelParams* d_mp, const Work* d_work,
+                                                   const DevOptions& opts, int count, bool seq_only,
+                                                   cudaStream_t stream) {
+  if (opts.nonlinear_ls && opts.condensed)
+    return launch_cta_feat<NX, NU, kFeatNL | kFeatCond>(d_topo, d_mp, d_work, opts, count, seq_only, stream);
+  if (opts.condensed) return launch_cta_feat<NX, NU, kFeatCond>(d_topo, d_mp, d_work, opts, count, seq_only, stream);
+  return launch_cta_feat<NX, NU, kFeatNL>(d_topo, d_mp, d_work, opts, count, seq_only, stream);
+}
+
+template <int NX, int NU>
+cudaError_t SolveLaunch<NX, NU>::solve_grid_special(const Topo* d_topo, const ModelParams* d_mp,
+                                                    const Work* d_work, const DevOptions& opts, double* red,
+                                                    int blocks, int threads, cudaStream_t stream) {
+  if (opts.nonlinear_ls && opts.condensed)
+    return launch_grid_feat<NX, NU, kFeatNL | kFeatCond>(d_topo, d_mp, d_work, opts, red, blocks, threads, stream);
+  if (opts.condensed)
+    return launch_grid_feat<NX, NU, kFeatCond>(d_topo, d_mp, d_work, opts, red, blocks, threads, stream);
+  return launch_grid_feat<NX, NU, kFeatNL>(d_topo, d_mp, d_work, opts, red, blocks, threads, stream);
 }
 
 template <int NX, int NU>

@@ -183,8 +183,16 @@ __device__ __forceinline__ void red_acc(const G& g, int k, double v, bool is_sum
 // kNL: the single-shooting line search (ForwardMode::nonlinear_rollout) is
 // compiled in — only into the kernels launched for that mode, so the
 // multiple-shooting solve loop keeps its register allocation.
-template <int NX, int NU, class G, bool kSeqOnly = false, int kTeam = 0, bool kNL = false>
+// kFeat: optional paths compiled in only where they are launched, so the
+// default solve kernels keep their register allocation and instruction
+// footprint: bit 0 the single-shooting line search, bit 1 the condensed
+// shared segment (scan_condensed), bit 2 the chunked backward sweep.
+constexpr int kFeatNL = 1, kFeatCond = 2, kFeatChunk = 4;
+template <int NX, int NU, class G, bool kSeqOnly = false, int kTeam = 0, int kFeat = 0>
 struct Solver {
+  static constexpr bool kNL = (kFeat & kFeatNL) != 0;
+  static constexpr bool kCond = (kFeat & kFeatCond) != 0;
+  static constexpr bool kChunk = (kFeat & kFeatChunk) != 0;
   using SL = StageLayout<NX, NU>;
   using BL = BwdLayout<NX>;
   using FL = FwdLayout<NX>;
@@ -730,7 +738,7 @@ struct Solver {
   // cost + reg, or the branch-node step over the summed children), then the
   // chain nodes tail -> head. Produces values (w.value) and policies.
   __device__ int riccati_sweep_depth(int d, double reg) {
-    if constexpr (!std::is_same<G, GridGroup>::value) {
+    if constexpr (kChunk && !std::is_same<G, GridGroup>::value) {
       if (chunk_count(d) > 1) return chunked_bwd_depth(d, reg);
     }
     int err = kBwdOk;
@@ -1136,7 +1144,7 @@ struct Solver {
   __device__ int backward(double reg, double* max_ff) {
     int err = kBwdOk;
     // Condensed strategy: only the leaf segments (P1) take the tree scan.
-    const bool condensed = o.condensed && t.n_shared > 0;
+    const bool condensed = kCond && o.condensed && t.n_shared > 0;
     for (int d = t.ndepth - 1; d >= (condensed ? t.ndepth - 1 : 0); --d) {
       const int L = t.depth_len[d];
       if (seq_depth(d)) {
@@ -1195,9 +1203,11 @@ struct Solver {
       err = err ? err : e;
       }
     }
-    if (condensed && err == kBwdOk) {
-      g.sync();
-      err = condensed_p2(reg);
+    if constexpr (kCond) {
+      if (condensed && err == kBwdOk) {
+        g.sync();
+        err = condensed_p2(reg);
+      }
     }
     // Policies of scanned chain nodes from their successor's value
     // (feedback_from_values, lqr_scan.hpp:146); max_feedforward.
