@@ -801,13 +801,15 @@ void default_launch_shape(bmpc_batch* b) {
     if (env && std::sscanf(env, "%dx%d", &et, &em) == 2 && cta_variant_supported(b->nx, b->nu, et, em)) *t = et, *m = em;
   };
   // One instance per SM or fewer: 256 threads each (lowest latency). More:
-  // (4,2) batches take the measured cfg4 schedule (tools/probe_exp.sh):
-  // 64x8 probe and main launches (highest pass throughput) with a 150-pass
-  // budget, survivors finished by 256-thread blocks that run nearly alone.
+  // (4,2) batches take the measured cfg4 schedule (tools/shape_sweep.py):
+  // 64x4 probe and main launches with a 150-pass budget, survivors finished
+  // by 256-thread blocks that run nearly alone. With the compact stage
+  // records 64x4 (255 registers, 4 blocks per SM) beats 64x8 (128 registers,
+  // 2 KB spills): 155.0 vs 162.7 ms per cfg4 step (64x6: 156.4).
   int t = 256, m = 1;
   if (b->nx == 4 && b->nu == 2 && b->count > std::max(1, b->ctx->sms)) {
     t = 64;
-    m = 8;
+    m = 4;
     b->main_budget = 150;
   }
   env_shape("BMPC_CTA", &t, &m);

@@ -361,6 +361,23 @@ struct UniRec {
   }
 };
 
+// Compact structured records (the batch kernels' layout for diagonal-weight
+// unicycle problems): only the kVar variable entries, kCompactStride doubles
+// per node, in UniRec order; the constant entries are implied.
+constexpr int kCompactStride = 24;
+// UniRec::pos as a constant-bank table for runtime entry indices, and its
+// inverse over the dense StageLayout<4, 2> offsets (-1: a constant entry).
+static __constant__ int kUniPosTab[UniRec::kVar] = {
+    UniRec::pos(0),  UniRec::pos(1),  UniRec::pos(2),  UniRec::pos(3),  UniRec::pos(4),  UniRec::pos(5),
+    UniRec::pos(6),  UniRec::pos(7),  UniRec::pos(8),  UniRec::pos(9),  UniRec::pos(10), UniRec::pos(11),
+    UniRec::pos(12), UniRec::pos(13), UniRec::pos(14), UniRec::pos(15), UniRec::pos(16), UniRec::pos(17),
+    UniRec::pos(18), UniRec::pos(19), UniRec::pos(20), UniRec::pos(21)};
+__host__ __device__ constexpr int uni_var_of(int k) {
+  for (int e = 0; e < UniRec::kVar; ++e)
+    if (UniRec::pos(e) == k) return e;
+  return -1;
+}
+
 // Constant value at dense offset k of a non-leaf structured record.
 __device__ __forceinline__ double unicycle_stage_constant(double dt, int k) {
   using L = StageLayout<4, 2>;
@@ -503,17 +520,19 @@ __device__ __forceinline__ bool unicycle_linearize_structured(const ModelParams&
 // linearize (solver.hpp:76-136) of one node: weighted, AL-augmented
 // Gauss-Newton stage record (non-leaf) or terminal (P, p) in the Q/q slots.
 // Returns false on a non-finite expansion.
+// compact: structured records in the compact layout (kCompactStride, UniRec order).
 template <int NX, int NU>
 __device__ __forceinline__ bool node_linearize(const ModelParams& mp, int node, bool leaf, double w, const double* x,
-                                               const double* u, const double* eta, double rho, double* rec) {
+                                               const double* u, const double* eta, double rho, double* rec,
+                                               bool compact = false) {
   using L = StageLayout<NX, NU>;
   if constexpr (NX == 4 && NU == 2) {
-    if (mp.kind == kModelUnicycle && mp.w_diag) {  // constants written once per solve
+    if (mp.kind == kModelUnicycle && mp.w_diag) {  // constants written once per solve (or implied)
       double v[UniRec::kVar];
       const bool ok = unicycle_linearize_structured(mp, node, leaf, w, x, u, eta, rho, v);
 #pragma unroll
       for (int e = 0; e < UniRec::kVar; ++e)
-        if (!leaf || (e >= 8 && e < 14) || (e >= 16 && e < 20)) rec[UniRec::pos(e)] = v[e];
+        if (!leaf || (e >= 8 && e < 14) || (e >= 16 && e < 20)) rec[compact ? e : UniRec::pos(e)] = v[e];
       return ok;
     }
     if (mp.kind == kModelUnicycle) {

@@ -219,7 +219,33 @@ struct Solver {
   // Unicycle with diagonal weights: stage records hold UniRec's variable
   // entries per pass over per-solve constants (model.cuh).
   __device__ bool structured() const { return NX == 4 && NU == 2 && mp.kind == kModelUnicycle && mp.w_diag; }
-  __device__ double* stage(int i) const { return w.stage + static_cast<size_t>(i) * SL::stride; }
+  // Compact structured records in the default batch kernels (kSeqOnly, no
+  // optional paths): 22 doubles per node instead of the 58-double dense
+  // record, so a pass touches ~1.5 cache lines of stage data per node
+  // instead of ~4 (the main launch's working set exceeds the L2).
+  __device__ bool compact() const {
+    if constexpr (kSeqOnly && kFeat == 0 && NX == 4 && NU == 2) return structured();
+    return false;
+  }
+  __device__ double* stage(int i) const {
+    return w.stage + static_cast<size_t>(i) * (compact() ? kCompactStride : SL::stride);
+  }
+  // Dense-layout entry k of a record r (compact records: the variable entry or the implied constant).
+  __device__ double rec_at(const double* r, int k) const {
+    if constexpr (NX == 4 && NU == 2) {
+      if (compact()) {
+        const int e = uni_var_of_rt(k);
+        return e >= 0 ? r[e] : unicycle_stage_constant(mp.dt, k);
+      }
+    }
+    return r[k];
+  }
+  __device__ static int uni_var_of_rt(int k) {
+    int e = -1;
+#pragma unroll
+    for (int q = 0; q < UniRec::kVar; ++q) e = (UniRec::pos(q) == k) ? q : e;
+    return e;
+  }
   __device__ double* bwd(int slot) const { return w.bwd + static_cast<size_t>(slot) * BL::stride; }
   __device__ double* fwd(int slot) const { return w.fwd + static_cast<size_t>(slot) * FL::stride; }
   __device__ double* pol(int i) const { return w.policy + static_cast<size_t>(i) * PL::stride; }
@@ -394,7 +420,7 @@ struct Solver {
       const bool leaf = is_leaf(i);
       const double* eta = w.eta + static_cast<size_t>(i) * t.max_con;
       const bool ok = node_linearize<NX, NU>(mp, i, leaf, t.weight[i], w.x + i * NX, w.u + i * NU, eta, g_rho,
-                                             stage(i));
+                                             stage(i), compact());
       double a, b, d, v;
       // Nominal evaluate terms and the edge defect parent -> i
       // (models.defect, solver.hpp:138-147) from one dynamics evaluation.
@@ -558,6 +584,9 @@ struct Solver {
     constexpr int PRE = (SL::size + TS - 1) / TS;
     int err = kBwdOk;
     __syncwarp(mask);
+    if constexpr (NX == 4 && NU == 2) {
+      if (compact()) return team_chain_compact<TS>(sq, k_hi, k_lo, reg, lane, mask, Fm);
+    }
     {
       const double* s0 = stage(node_at(sq, k_hi));
       for (int k = lane; k < SL::size; k += TS) Fm[F::S + k] = s0[k];
@@ -592,6 +621,61 @@ struct Solver {
           const int idx = lane + j * TS;
           if (idx < SL::size) Fm[F::S + idx] = pre[j];
         }
+        if (lane < NX) Fm[F::c + lane] = prec;
+      }
+    }
+    return err;
+  }
+
+  // team_chain over compact structured records: the constant entries of the
+  // dense record are staged once, then each step stages only the 22 variable
+  // entries (each lane's destination offsets held in registers).
+  template <int TS>
+  __device__ int team_chain_compact(const SegIdx& sq, int k_hi, int k_lo, double reg, int lane, unsigned mask,
+                                    double* Fm) {
+    using F = RicFlat<NX, NU>;
+    constexpr int PRE = (UniRec::kVar + TS - 1) / TS;
+    int err = kBwdOk;
+    for (int k = lane; k < SL::size; k += TS)
+      if (uni_var_of_rt(k) < 0) Fm[F::S + k] = unicycle_stage_constant(mp.dt, k);
+    int dst[PRE];
+#pragma unroll
+    for (int j = 0; j < PRE; ++j) {
+      const int idx = lane + j * TS;
+      dst[j] = idx < UniRec::kVar ? kUniPosTab[idx] : 0;
+    }
+    {
+      const double* s0 = stage(node_at(sq, k_hi));
+#pragma unroll
+      for (int j = 0; j < PRE; ++j)
+        if (lane + j * TS < UniRec::kVar) Fm[F::S + dst[j]] = s0[lane + j * TS];
+      if (lane < NX) Fm[F::c + lane] = w.defect[node_at(sq, k_hi + 1) * NX + lane];
+    }
+    const double* const stg = w.stage;
+    const double* const dfc = w.defect;
+    double* const vbase = w.value;
+    double* const pbase = w.policy;
+    for (int k = k_hi; k >= k_lo; --k) {
+      const int i = node_at(sq, k);
+      double pre[PRE];
+      double prec = 0.0;
+      if (k > k_lo) {
+        const double* sp = stg + static_cast<size_t>(node_at(sq, k - 1)) * kCompactStride;
+#pragma unroll
+        for (int j = 0; j < PRE; ++j) {
+          const int idx = lane + j * TS;
+          pre[j] = idx < UniRec::kVar ? sp[idx] : 0.0;
+        }
+        if (lane < NX) prec = dfc[i * NX + lane];
+      }
+      double* const vi = (k == 0 || o.keep_values) ? vbase + static_cast<size_t>(i) * VL::stride : nullptr;
+      const int e = team_riccati_step_u<NX, NU, TS>(reg, mask, Fm, lane, vi, pbase + static_cast<size_t>(i) * PL::stride);
+      err = err ? err : e;
+      if (k > k_lo) {
+        __syncwarp(mask);
+#pragma unroll
+        for (int j = 0; j < PRE; ++j)
+          if (lane + j * TS < UniRec::kVar) Fm[F::S + dst[j]] = pre[j];
         if (lane < NX) Fm[F::c + lane] = prec;
       }
     }
@@ -760,12 +844,12 @@ struct Solver {
           // step); the kernel-level API keeps every node's.
           const bool keep = o.keep_values || L == 1;
           for (int k = lane; k < NX * NX; k += kTS) {
-            const double v = stage(b)[SL::Q + k] + ((k % (NX + 1)) == 0 ? reg : 0.0);
+            const double v = rec_at(stage(b), SL::Q + k) + ((k % (NX + 1)) == 0 ? reg : 0.0);
             ric_put_P<NX, NU>(Fm, k, v);
             if (keep) val(b)[VL::P + k] = v;
           }
           for (int k = lane; k < NX; k += kTS) {
-            const double v = stage(b)[SL::q + k];
+            const double v = rec_at(stage(b), SL::q + k);
             Fm[F::p + k] = v;
             if (keep) val(b)[VL::p + k] = v;
           }
@@ -788,7 +872,7 @@ struct Solver {
             }
             Fm[F::p + k] = a;
           }
-          for (int k = lane; k < SL::size; k += kTS) Fm[F::S + k] = stage(b)[k];
+          for (int k = lane; k < SL::size; k += kTS) Fm[F::S + k] = rec_at(stage(b), k);
           if (lane < NX) Fm[F::c + lane] = 0.0;
           const int e = team_riccati_step_u<NX, NU, kTS>(reg, mask, Fm, lane,
                                                          (o.keep_values || L == 1) ? val(b) : nullptr, pol(b));
@@ -1426,11 +1510,19 @@ struct Solver {
   // EC terms of one node from a structured record (variable entries only):
   // the dense products below with the exact-zero terms dropped, same bits.
   __device__ void ec_structured(int i, const double* si, const double* dxi, double* a1, double* a2) {
+    const bool cmp = compact();
+    // Variable entry at dense offset K of either layout (K is a compile-time constant).
+    auto sv = [&](auto K) -> double {
+      constexpr int k = decltype(K)::value;
+      return cmp ? si[uni_var_of(k)] : si[k];
+    };
     const double d0 = dxi[0], d1 = dxi[1], d2 = dxi[2], d3 = dxi[3];
-    const double Q00 = si[SL::Q + 0], Q10 = si[SL::Q + 1], Q01 = si[SL::Q + 4], Q11 = si[SL::Q + 5];
-    const double Qdx[4] = {fma(Q01, d1, Q00 * d0), fma(Q11, d1, Q10 * d0), si[SL::Q + 10] * d2,
-                           si[SL::Q + 15] * d3};
-    const double qdx = dot<4>(si + SL::q, dxi);
+    const double Q00 = sv(std::integral_constant<int, SL::Q + 0>{}), Q10 = sv(std::integral_constant<int, SL::Q + 1>{}),
+                 Q01 = sv(std::integral_constant<int, SL::Q + 4>{}), Q11 = sv(std::integral_constant<int, SL::Q + 5>{});
+    const double Qdx[4] = {fma(Q01, d1, Q00 * d0), fma(Q11, d1, Q10 * d0),
+                           sv(std::integral_constant<int, SL::Q + 10>{}) * d2,
+                           sv(std::integral_constant<int, SL::Q + 15>{}) * d3};
+    const double qdx = dot<4>(si + (cmp ? uni_var_of(SL::q) : SL::q), dxi);
     const double xQx = dot<4>(dxi, Qdx);
     if (is_leaf(i)) {
       *a1 += qdx;
@@ -1446,9 +1538,10 @@ struct Solver {
       for (int j = 0; j < NU; ++j) dui[j] = du[j] + po[PL::k + j];
     }
     const double u0 = dui[0], u1 = dui[1];
-    const double Rdu[2] = {si[SL::R + 0] * u0, si[SL::R + 3] * u1};
+    const double Rdu[2] = {sv(std::integral_constant<int, SL::R + 0>{}) * u0,
+                           sv(std::integral_constant<int, SL::R + 3>{}) * u1};
     const double Mdx[2] = {0.0, 0.0};
-    *a1 += qdx + fma(si[SL::r + 1], u1, si[SL::r + 0] * u0);
+    *a1 += qdx + fma(sv(std::integral_constant<int, SL::r + 1>{}), u1, sv(std::integral_constant<int, SL::r + 0>{}) * u0);
     *a2 += (0.5 * xQx + dot<2>(dui, Mdx)) + 0.5 * dot<2>(dui, Rdu);
   }
 
@@ -1456,6 +1549,15 @@ struct Solver {
   __device__ void load_AB(int i, double* A, double* Bm) const {
     const double* si = stage(i);
     if constexpr (NX == 4 && NU == 2) {
+      if (compact()) {
+#pragma unroll
+        for (int k = 0; k < NX * NX; ++k)
+          A[k] = uni_var_of(SL::A + k) >= 0 ? si[uni_var_of(SL::A + k)] : unicycle_stage_constant(mp.dt, SL::A + k);
+#pragma unroll
+        for (int k = 0; k < NX * NU; ++k)
+          Bm[k] = uni_var_of(SL::B + k) >= 0 ? si[uni_var_of(SL::B + k)] : unicycle_stage_constant(mp.dt, SL::B + k);
+        return;
+      }
       if (structured()) {
         unicycle_load_AB(si, mp.dt, A, Bm);
         return;
@@ -1908,7 +2010,8 @@ struct Solver {
       for (int i = g.rank(); i < t.n * t.max_con; i += g.size()) w.eta[i] = 0.0;
       if constexpr (NX == 4 && NU == 2) {
         if (structured())  // constant part of every stage record, once per solve
-          for (int i = g.rank(); i < t.n; i += g.size()) unicycle_stage_constants(mp.dt, is_leaf(i), stage(i));
+          if (!compact())
+            for (int i = g.rank(); i < t.n; i += g.size()) unicycle_stage_constants(mp.dt, is_leaf(i), stage(i));
       }
       g_rho = o.penalty_init;
       if (!rollout()) {
