@@ -1444,6 +1444,9 @@ static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_input
   // kernel-level LQR entry (bmpc_lqr_tree): measured slower than the team
   // sweep in the solve kernels (cfg0 alone, 256 threads: 129 vs 80 us per pass).
   d.chunk_bwd = 0;
+  // Long segments in wide blocks (>= 128 threads, grid mode): the block-local
+  // forward scan; BMPC_FWD_BLOCK_SCAN=<min transitions> (0: the one-thread walk).
+  d.fwd_block_scan = std::getenv("BMPC_FWD_BLOCK_SCAN") ? std::atoi(std::getenv("BMPC_FWD_BLOCK_SCAN")) : 16;
   // Strategy enums (solver.hpp:23-26; presets bench.cpp:60-83).
   if (o.backward < 0 || o.backward > 2 || o.forward < 0 || o.forward > 1 || o.line_search < 0 || o.line_search > 1)
     return fail(BMPC_ERR_INVALID, "unknown backward / forward / line_search strategy");

@@ -1401,7 +1401,10 @@ struct Solver {
           tf0 = clock64();
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(nf0));
         }
-        forward_walk_depth(d);
+        if (block_scan_fwd(d))
+          forward_scan_block_depth(d);
+        else
+          forward_walk_depth(d);
         if (w.prof && threadIdx.x == 0) {
           long long nf1;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(nf1));
@@ -1583,6 +1586,97 @@ struct Solver {
       e[NX * NX + j] = Bk[j];
       e[NX * NX + NX + j] = w.defect[nxt * NX + j];
     }
+  }
+
+  // Block-local parallel forward pass (wide blocks, long segments): the
+  // closed-loop affine maps of a chunk of C transitions of each of ng
+  // segments are built one per thread, composed by a Hillis-Steele inclusive
+  // scan (log2 C levels, maps in registers, partners through shared memory)
+  // and applied to the chunk's incoming perturbation — linear_rollout's
+  // forward_scan (lqr_scan.hpp:177-187) done inside one block, without grid
+  // barriers: ~log2 C dependent compositions per chunk instead of C dependent
+  // steps. Under a GridGroup each block scans its own share of the depth's
+  // segments.
+  static constexpr int kFE = NX * NX + NX;  // affine map (A, b)
+  __device__ bool block_scan_fwd(int d) const {
+    return G::bdim() >= 128 && o.fwd_block_scan > 0 && t.depth_len[d] - 1 >= o.fwd_block_scan;
+  }
+  __device__ void forward_scan_block_depth(int d) {
+    const int L = t.depth_len[d], T = L - 1;
+    const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
+    const int nb = g.nblocks(), b = g.block();
+    const int lr = threadIdx.x, ls = G::bdim();
+    const int nmine = se - sb > b ? (se - sb - b + nb - 1) / nb : 0;
+    const int C = min(T, ls);
+    const int ng = max(1, ls / C);
+    double* maps = wbuf;                  // [ls][kFE]
+    double* carry = wbuf + ls * kFE;      // [ng][NX] (wbuf holds ls * kWE >= ls * kFE + ls * NX doubles)
+    for (int j0 = 0; j0 < nmine; j0 += ng) {
+      const int ngc = min(ng, nmine - j0);
+      for (int r = lr; r < ngc; r += ls) {
+        const SegIdx qs = seg_idx(sb + b + (j0 + r) * nb);
+        double h[NX];
+        head_dx(qs.head, h);
+#pragma unroll
+        for (int j = 0; j < NX; ++j) {
+          w.dx[qs.head * NX + j] = h[j];
+          carry[r * NX + j] = h[j];
+        }
+      }
+      __syncthreads();
+      const int r = lr / C, q = lr - r * C;
+      SegIdx qs{0, 0, 0};
+      if (r < ngc) qs = seg_idx(sb + b + (j0 + r) * nb);
+      for (int c0 = 0; c0 < T; c0 += C) {
+        const int cn = min(C, T - c0);
+        const bool act = r < ngc && q < cn;
+        double A[NX * NX], bb[NX];
+        if (act) {
+          double e[kWE];
+          walk_element(node_at(qs, c0 + q), node_at(qs, c0 + q + 1), e);
+#pragma unroll
+          for (int k = 0; k < NX * NX; ++k) A[k] = e[k];
+#pragma unroll
+          for (int j = 0; j < NX; ++j) bb[j] = e[NX * NX + j] + e[NX * NX + NX + j];
+        }
+        for (int off = 1; off < cn; off <<= 1) {
+          if (act) {
+#pragma unroll
+            for (int k = 0; k < NX * NX; ++k) maps[lr * kFE + k] = A[k];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) maps[lr * kFE + NX * NX + j] = bb[j];
+          }
+          __syncthreads();
+          if (act && q >= off) {  // (A, b) <- (A, b) o (Ap, bp): Ap first
+            const double* pm = maps + (lr - off) * kFE;
+            double An[NX * NX], bn[NX];
+            mm<NX, NX, NX>(A, pm, An);
+            mv<NX, NX>(A, pm + NX * NX, bn);
+#pragma unroll
+            for (int j = 0; j < NX; ++j) bb[j] = bn[j] + bb[j];
+#pragma unroll
+            for (int k = 0; k < NX * NX; ++k) A[k] = An[k];
+          }
+          __syncthreads();
+        }
+        double dxn[NX];
+        if (act) {
+          double t1[NX];
+          mv<NX, NX>(A, carry + r * NX, t1);
+#pragma unroll
+          for (int j = 0; j < NX; ++j) dxn[j] = t1[j] + bb[j];
+          const int node = node_at(qs, c0 + q + 1);
+#pragma unroll
+          for (int j = 0; j < NX; ++j) w.dx[node * NX + j] = dxn[j];
+        }
+        __syncthreads();
+        if (act && q == cn - 1)
+#pragma unroll
+          for (int j = 0; j < NX; ++j) carry[r * NX + j] = dxn[j];
+        __syncthreads();
+      }
+    }
+    g.sync();
   }
 
   __device__ void forward_walk_depth(int d) {

@@ -45,6 +45,7 @@ struct DevOptions {  // SolverOptions (solver.hpp:28-58), device copy
   int nonlinear_ls; // 1: ForwardMode::nonlinear_rollout trials (sssilqr, solver.hpp:463-467)
   int chunk_bwd;    // 1: blocks of >= 256 threads sweep long segments with the chunked scan
   int condensed;    // 1: BackwardStrategy::scan_condensed (hypmsilqr): P2 by condensing + dense solve
+  int fwd_block_scan;  // > 0: wide blocks roll segments of >= this many transitions out by a block-local affine-map scan
 };
 
 // Suspended solve() loop state (batch scheduling): a solve can stop at the top
