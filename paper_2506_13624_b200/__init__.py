@@ -798,6 +798,7 @@ def batch_phase_profile(batch: "Batch", instance: int = 0) -> dict:
         res["sweep_cycles_per_step"] = out[12] / out[13]
     res["walk_cycles"] = (out[14], out[15], out[11], out[18], out[19], out[20])  # head_dx, chunks, depths, ns, elements, chain
     res["sm_mhz"] = 1e3 * out[16] / out[17] if out[17] > 0 else 0.0  # effective SM clock of the solve
+    res["fwd_scan_cycles"] = (out[21], out[22], out[23])  # elements + barrier, run maps, scan + re-walk
     return res
 
 

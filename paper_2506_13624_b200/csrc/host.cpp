@@ -1442,11 +1442,13 @@ static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_input
   d.fwd_scan_min = std::getenv("BMPC_FWD_SCAN_MIN") ? std::atoi(std::getenv("BMPC_FWD_SCAN_MIN")) : 0;
   // The chunked (time-parallel) backward sweep is compiled only into the
   // kernel-level LQR entry (bmpc_lqr_tree): measured slower than the team
-  // sweep in the solve kernels (cfg0 alone, 256 threads: 129 vs 80 us per pass).
+  // sweep in the solve kernels (cfg0 alone, 256 threads: 129 vs 80 us per
+  // pass; cfg3-spread on the whole GPU: 147 vs 82 ms).
   d.chunk_bwd = 0;
-  // Long segments in wide blocks (>= 128 threads, grid mode): the block-local
-  // forward scan; BMPC_FWD_BLOCK_SCAN=<min transitions> (0: the one-thread walk).
-  d.fwd_block_scan = std::getenv("BMPC_FWD_BLOCK_SCAN") ? std::atoi(std::getenv("BMPC_FWD_BLOCK_SCAN")) : 16;
+  // Segments of >= 256 transitions in the wide non-lean kernels: the
+  // parallel forward scan (below that the one-thread walk is as fast: cfg3's
+  // 99/199-step segments); BMPC_FWD_BLOCK_SCAN=<min transitions> (0: walk).
+  d.fwd_block_scan = std::getenv("BMPC_FWD_BLOCK_SCAN") ? std::atoi(std::getenv("BMPC_FWD_BLOCK_SCAN")) : 256;
   // Strategy enums (solver.hpp:23-26; presets bench.cpp:60-83).
   if (o.backward < 0 || o.backward > 2 || o.forward < 0 || o.forward > 1 || o.line_search < 0 || o.line_search > 1)
     return fail(BMPC_ERR_INVALID, "unknown backward / forward / line_search strategy");

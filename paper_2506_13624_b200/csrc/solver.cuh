@@ -699,12 +699,17 @@ struct Solver {
   // Latency ~(Ck - 1 + J - 1) combinations + Ck steps instead of L - 1 steps:
   // the time-parallel form of the reference's P1 scan with only block
   // barriers between the phases.
+  // Chunk length: a combination costs ~2.5 Bellman steps, so the latency
+  // ~2.5 (Ck + J) + Ck with J = L / Ck is least near Ck = sqrt(0.7 L); J is
+  // capped by the teams the depth can give each segment (block teams in a
+  // CtaGroup, every block's in a GridGroup) so one round covers all chunks.
   static constexpr int kTC = team_size<NX, NU>();  // 16-lane teams (the allocated team slots)
   __device__ int chunk_count(int d) const {
-    if (kTC <= 0 || G::bdim() < 256 || !o.chunk_bwd) return 1;
+    if (kTC <= 0 || G::bdim() < 256 || o.chunk_bwd <= 0) return 1;
     const int L = t.depth_len[d], ns = t.depth_begin[d + 1] - t.depth_begin[d];
-    if (L < 8) return 1;
-    const int J = min((G::bdim() / kTC) / max(ns, 1), L / 4);
+    if (L < 8 || L < o.chunk_bwd) return 1;
+    const int ck = max(4, static_cast<int>(sqrtf(0.7f * static_cast<float>(L))));
+    const int J = min((g.size() / kTC) / max(ns, 1), min((L + ck - 1) / ck, L / 4));
     return J >= 2 ? J : 1;
   }
 
@@ -760,9 +765,9 @@ struct Solver {
         err = err ? err : e;
       });
       g.sync();
-      const int team = threadIdx.x / kTC, nteams = G::bdim() / kTC, lane = threadIdx.x % kTC;
+      const int team = g.rank() / kTC, nteams = g.size() / kTC, lane = threadIdx.x % kTC;
       const unsigned mask = kTC == 32 ? 0xffffffffu : (((1u << kTC) - 1u) << ((threadIdx.x & 31) / kTC * kTC));
-      unsigned char* slot = reinterpret_cast<unsigned char*>(tsm) + team * slot_bytes();
+      unsigned char* slot = reinterpret_cast<unsigned char*>(tsm) + (threadIdx.x / kTC) * slot_bytes();  // block-local slot
       TeamSmem<NX>& cs = *reinterpret_cast<TeamSmem<NX>*>(slot);
       // A: chunk elements.
       for (int q = team; q < ns * J; q += nteams) {
@@ -822,7 +827,7 @@ struct Solver {
   // cost + reg, or the branch-node step over the summed children), then the
   // chain nodes tail -> head. Produces values (w.value) and policies.
   __device__ int riccati_sweep_depth(int d, double reg) {
-    if constexpr (kChunk && !std::is_same<G, GridGroup>::value) {
+    if constexpr (kChunk) {
       if (chunk_count(d) > 1) return chunked_bwd_depth(d, reg);
     }
     int err = kBwdOk;
@@ -1308,6 +1313,18 @@ struct Solver {
           err = err ? err : e;
         }
       }
+      if constexpr (!kSeqOnly) {  // the parallel forward scan's element of transition (i, nxt)
+        const int d = t.seg_depth[s];
+        if (block_scan_fwd(d) && k + 1 < seg_len(s)) {
+          const int T = t.depth_len[d] - 1;
+          const FwdRuns fr = fwd_runs(T);
+          double e[kWE];
+          walk_element(i, seg_node(s, k + 1), e);
+          double* p = fwd(t.seg_scratch[s]) + fr.pos(k);
+#pragma unroll
+          for (int f = 0; f < kWE; ++f) p[f * fr.stride()] = e[f];
+        }
+      }
       double m = 0.0;
 #pragma unroll
       for (int j = 0; j < NU; ++j) m = fmax(m, fabs(pol(i)[PL::k + j]));
@@ -1588,92 +1605,186 @@ struct Solver {
     }
   }
 
-  // Block-local parallel forward pass (wide blocks, long segments): the
-  // closed-loop affine maps of a chunk of C transitions of each of ng
-  // segments are built one per thread, composed by a Hillis-Steele inclusive
-  // scan (log2 C levels, maps in registers, partners through shared memory)
-  // and applied to the chunk's incoming perturbation — linear_rollout's
-  // forward_scan (lqr_scan.hpp:177-187) done inside one block, without grid
-  // barriers: ~log2 C dependent compositions per chunk instead of C dependent
-  // steps. Under a GridGroup each block scans its own share of the depth's
-  // segments.
+  // Parallel forward pass of long segments (wide blocks of the non-lean
+  // kernels): linear_rollout's forward_scan (lqr_scan.hpp:177-187) with no
+  // group barrier inside instead of 2 log L grid-synchronised levels.
+  //   E) backward()'s closing policy loop (all threads) already wrote the
+  //      walk element (Acl, B k, defect) of every transition of the depth into
+  //      the segment's forward scratch, field-major (coalesced reads below);
+  //   S) block-locally, each segment gets whole warps and each thread
+  //      1) composes the affine maps x -> (Acl x + B k) + d of its run of
+  //         R <= 4 consecutive transitions,
+  //      2) the warp scans the run maps with shuffles (5 levels),
+  //      3) warp totals go through shared memory and each warp carries the
+  //         segment's incoming dx across the earlier warps' totals,
+  //      4) each thread takes its start state from lane - 1 and re-walks its
+  //         run with the walk's arithmetic, writing dx.
+  // Rounding differs from the one-thread walk, so the lean (population)
+  // kernels keep the walk.
   static constexpr int kFE = NX * NX + NX;  // affine map (A, b)
   __device__ bool block_scan_fwd(int d) const {
+    if constexpr (kSeqOnly) return false;
     return G::bdim() >= 128 && o.fwd_block_scan > 0 && t.depth_len[d] - 1 >= o.fwd_block_scan;
+  }
+  // Walk elements of a segment's T transitions in its forward scratch,
+  // field-major and run-major: with R = ceil(T / block) transitions per
+  // thread and W = ceil(T / R) threads, transition k = R t + q sits at
+  // position q W + t of each field (stride R W < T + R), so the threads of a
+  // warp read consecutive doubles.
+  struct FwdRuns {
+    int R, W;
+    __device__ int pos(int k) const { return (k % R) * W + k / R; }
+    __device__ int stride() const { return R * W; }
+  };
+  __device__ FwdRuns fwd_runs(int T) const {
+    const int R = max(1, (T + G::bdim() - 1) / G::bdim());
+    return {R, (T + R - 1) / R};
+  }
+  __device__ void load_walk_element(int base, const FwdRuns& fr, int k, double* e) const {
+    const double* p = fwd(base) + fr.pos(k);
+    const int st = fr.stride();
+#pragma unroll
+    for (int f = 0; f < kWE; ++f) e[f] = p[f * st];
+  }
+  // (A, b) <- E o (A, b) for the walk element e (Acl, B k, defect).
+  __device__ static void compose_walk(const double* e, double* A, double* bb) {
+    double An[NX * NX], bn[NX];
+    mm<NX, NX, NX>(e, A, An);
+    mv<NX, NX>(e, bb, bn);
+#pragma unroll
+    for (int j = 0; j < NX; ++j) bb[j] = (bn[j] + e[NX * NX + j]) + e[NX * NX + NX + j];
+#pragma unroll
+    for (int k = 0; k < NX * NX; ++k) A[k] = An[k];
   }
   __device__ void forward_scan_block_depth(int d) {
     const int L = t.depth_len[d], T = L - 1;
     const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
+    long long tp = 0;  // diagnostic phase clocks (thread 0 of the block): prof[21..23]
+    if (w.prof && threadIdx.x == 0) tp = clock64();
+    auto tick = [&](int slot) {
+      if (w.prof && threadIdx.x == 0) {
+        const long long now = clock64();
+        g.sm->prof[slot] += static_cast<double>(now - tp);
+        tp = now;
+      }
+    };
+    // E) the elements were written by backward()'s policy loop (scratch:
+    //    2L + 32 slots of FL::stride doubles >= kWE (T + R)).
+    const FwdRuns fr = fwd_runs(T);
+    tick(21);
     const int nb = g.nblocks(), b = g.block();
-    const int lr = threadIdx.x, ls = G::bdim();
+    const int ls = G::bdim(), lr = threadIdx.x, lane = lr & 31, warp = lr >> 5, nw = ls >> 5;
     const int nmine = se - sb > b ? (se - sb - b + nb - 1) / nb : 0;
-    const int C = min(T, ls);
-    const int ng = max(1, ls / C);
-    double* maps = wbuf;                  // [ls][kFE]
-    double* carry = wbuf + ls * kFE;      // [ng][NX] (wbuf holds ls * kWE >= ls * kFE + ls * NX doubles)
+    const int R = fr.R, span = T;                            // transitions per thread; one round
+    const int wps = (fr.W + 31) / 32;                        // warps per segment
+    const int ng = nw / wps;                                 // segments per round
+    double* tot = wbuf;                                      // [nw][kFE] warp totals
+    double* carry = wbuf + nw * kFE;                         // [ng][NX]
+    const int r = warp / wps, wg = warp - r * wps, tq = wg * 32 + lane;
     for (int j0 = 0; j0 < nmine; j0 += ng) {
       const int ngc = min(ng, nmine - j0);
-      for (int r = lr; r < ngc; r += ls) {
-        const SegIdx qs = seg_idx(sb + b + (j0 + r) * nb);
+      for (int rr = lr; rr < ngc; rr += ls) {
+        const SegIdx qs = seg_idx(sb + b + (j0 + rr) * nb);
         double h[NX];
         head_dx(qs.head, h);
 #pragma unroll
         for (int j = 0; j < NX; ++j) {
           w.dx[qs.head * NX + j] = h[j];
-          carry[r * NX + j] = h[j];
+          carry[rr * NX + j] = h[j];
         }
       }
       __syncthreads();
-      const int r = lr / C, q = lr - r * C;
+      const bool seg_ok = r < ng && r < ngc;
       SegIdx qs{0, 0, 0};
-      if (r < ngc) qs = seg_idx(sb + b + (j0 + r) * nb);
-      for (int c0 = 0; c0 < T; c0 += C) {
-        const int cn = min(C, T - c0);
-        const bool act = r < ngc && q < cn;
+      int base = 0;
+      if (seg_ok) {
+        const int s = sb + b + (j0 + r) * nb;
+        qs = seg_idx(s);
+        base = t.seg_scratch[s];
+      }
+      for (int c0 = 0; c0 < T; c0 += span) {
+        const int cn = min(span, T - c0);
+        const int k0 = c0 + tq * R;
+        const int nk = seg_ok ? max(0, min(R, c0 + cn - k0)) : 0;
+        // 1) run map
         double A[NX * NX], bb[NX];
-        if (act) {
+#pragma unroll
+        for (int k = 0; k < NX * NX; ++k) A[k] = (k % (NX + 1)) == 0 ? 1.0 : 0.0;
+#pragma unroll
+        for (int j = 0; j < NX; ++j) bb[j] = 0.0;
+        for (int q = 0; q < nk; ++q) {
           double e[kWE];
-          walk_element(node_at(qs, c0 + q), node_at(qs, c0 + q + 1), e);
-#pragma unroll
-          for (int k = 0; k < NX * NX; ++k) A[k] = e[k];
-#pragma unroll
-          for (int j = 0; j < NX; ++j) bb[j] = e[NX * NX + j] + e[NX * NX + NX + j];
+          load_walk_element(base, fr, k0 + q, e);
+          compose_walk(e, A, bb);
         }
-        for (int off = 1; off < cn; off <<= 1) {
-          if (act) {
+        tick(22);
+        // 2) warp inclusive scan: mine o lane-off's
+        for (int off = 1; off < 32; off <<= 1) {
+          double Ap[NX * NX], bp[NX];
 #pragma unroll
-            for (int k = 0; k < NX * NX; ++k) maps[lr * kFE + k] = A[k];
+          for (int k = 0; k < NX * NX; ++k) Ap[k] = __shfl_up_sync(0xffffffffu, A[k], off);
 #pragma unroll
-            for (int j = 0; j < NX; ++j) maps[lr * kFE + NX * NX + j] = bb[j];
-          }
-          __syncthreads();
-          if (act && q >= off) {  // (A, b) <- (A, b) o (Ap, bp): Ap first
-            const double* pm = maps + (lr - off) * kFE;
+          for (int j = 0; j < NX; ++j) bp[j] = __shfl_up_sync(0xffffffffu, bb[j], off);
+          if (lane >= off) {
             double An[NX * NX], bn[NX];
-            mm<NX, NX, NX>(A, pm, An);
-            mv<NX, NX>(A, pm + NX * NX, bn);
+            mm<NX, NX, NX>(A, Ap, An);
+            mv<NX, NX>(A, bp, bn);
 #pragma unroll
             for (int j = 0; j < NX; ++j) bb[j] = bn[j] + bb[j];
 #pragma unroll
             for (int k = 0; k < NX * NX; ++k) A[k] = An[k];
           }
-          __syncthreads();
         }
-        double dxn[NX];
-        if (act) {
+        // 3) warp totals; the segment's state at this warp's start
+        if (lane == 31) {
+#pragma unroll
+          for (int k = 0; k < NX * NX; ++k) tot[warp * kFE + k] = A[k];
+#pragma unroll
+          for (int j = 0; j < NX; ++j) tot[warp * kFE + NX * NX + j] = bb[j];
+        }
+        __syncthreads();
+        double x[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) x[j] = seg_ok ? carry[r * NX + j] : 0.0;
+        for (int v = 0; v < wg; ++v) {
+          const double* tv = tot + (r * wps + v) * kFE;
           double t1[NX];
-          mv<NX, NX>(A, carry + r * NX, t1);
+          mv<NX, NX>(tv, x, t1);
 #pragma unroll
-          for (int j = 0; j < NX; ++j) dxn[j] = t1[j] + bb[j];
-          const int node = node_at(qs, c0 + q + 1);
-#pragma unroll
-          for (int j = 0; j < NX; ++j) w.dx[node * NX + j] = dxn[j];
+          for (int j = 0; j < NX; ++j) x[j] = t1[j] + tv[NX * NX + j];
         }
-        __syncthreads();
-        if (act && q == cn - 1)
+        // 4) own end state; start state = lane - 1's end state; re-walk
+        double y[NX];
+        {
+          double t1[NX];
+          mv<NX, NX>(A, x, t1);
 #pragma unroll
-          for (int j = 0; j < NX; ++j) carry[r * NX + j] = dxn[j];
+          for (int j = 0; j < NX; ++j) y[j] = t1[j] + bb[j];
+        }
+        double st[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) {
+          const double v = __shfl_up_sync(0xffffffffu, y[j], 1);
+          st[j] = lane == 0 ? x[j] : v;
+        }
+        for (int q = 0; q < nk; ++q) {
+          double e[kWE];
+          load_walk_element(base, fr, k0 + q, e);
+          double t1[NX];
+          mv<NX, NX>(e, st, t1);
+          const int nxt = node_at(qs, k0 + q + 1);
+#pragma unroll
+          for (int j = 0; j < NX; ++j) {
+            st[j] = (t1[j] + e[NX * NX + j]) + e[NX * NX + NX + j];
+            w.dx[nxt * NX + j] = st[j];
+          }
+        }
+        __syncthreads();  // carry / totals consumed
+        if (nk > 0 && k0 + nk == c0 + cn)
+#pragma unroll
+          for (int j = 0; j < NX; ++j) carry[r * NX + j] = st[j];
         __syncthreads();
+        tick(23);
       }
     }
     g.sync();

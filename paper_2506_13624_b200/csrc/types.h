@@ -43,7 +43,7 @@ struct DevOptions {  // SolverOptions (solver.hpp:28-58), device copy
   int keep_values;  // 1: store (P, p) of every node (kernel-level API); 0: segment heads only
   int fwd_scan_min; // segments of >= this length take the forward prefix scan (0: walk everywhere)
   int nonlinear_ls; // 1: ForwardMode::nonlinear_rollout trials (sssilqr, solver.hpp:463-467)
-  int chunk_bwd;    // 1: blocks of >= 256 threads sweep long segments with the chunked scan
+  int chunk_bwd;    // > 0: kChunk kernels sweep segments of >= this many nodes with the chunked scan
   int condensed;    // 1: BackwardStrategy::scan_condensed (hypmsilqr): P2 by condensing + dense solve
   int fwd_block_scan;  // > 0: wide blocks roll segments of >= this many transitions out by a block-local affine-map scan
 };

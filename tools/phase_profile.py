@@ -22,6 +22,8 @@ for name, p in cases:
     passes = r.n_records + r.outer_iterations
     cps = prof.pop("sweep_cycles_per_step", None)
     wk = prof.pop("walk_cycles", (0,) * 6)
+    fs = prof.pop("fwd_scan_cycles", (0,) * 3)
+    print(f"   forward scan cycles/pass: elements+barrier {fs[0] / passes:.0f}, run maps {fs[1] / passes:.0f}, scan+re-walk {fs[2] / passes:.0f}")
     print(f"   effective SM clock during the solve: {prof.pop('sm_mhz', 0):.0f} MHz")
     print(f"   walk cycles/pass: head_dx {wk[0] / passes:.0f}, chunks {wk[1] / passes:.0f}, depth walks {wk[2] / passes:.0f} ({wk[3] / passes:.0f} ns); element phases {wk[4] / passes:.0f}, chain (thread 0) {wk[5] / passes:.0f}")
     tot = sum(prof.values())
