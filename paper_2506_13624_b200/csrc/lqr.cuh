@@ -661,7 +661,7 @@ struct RicFlat {  // offsets into the team's flat shared array
                        qx = ev(Quu + NU * NU), qu = ev(qx + NX), K = ev(qu + NU), k = ev(K + NU * NX),
                        ZERO = ev(k + NU), DUMMY = ZERO + ev(NX), size = DUMMY + 8;
   static constexpr int n1 = NX + NU * NX + NX * NX;                  // psh, B'P, A'P
-  static constexpr int n2 = NX * NX + NU * NX + NU * NU + NX + NU;   // Qxx, Qux, Quu, qx, qu
+  static constexpr int n2 = NX * NX + NU * NX + NX + NU;             // Qxx, Qux, qx, qu (Quu: every lane)
   static constexpr int n3 = NU * NX + NU;                            // K, k
   static constexpr int n4 = NX * NX + NX;                            // P, p
   static constexpr bool kVec = NX % 2 == 0;  // all X / Y operand offsets even
@@ -710,11 +710,6 @@ __device__ __forceinline__ DotSlot ric_slot2(int q) {
     return {short(F::M + q), short(F::BtP + a * NX), short(F::A + j * NX), short(F::Qux + q), false};
   }
   q -= NU * NX;
-  if (q < NU * NU) {  // Quu = R (+reg) + B'P B
-    const int a = q % NU, b = q / NU;
-    return {short(F::R + q), short(F::BtP + a * NX), short(F::B + b * NX), short(F::Quu + q), a == b};
-  }
-  q -= NU * NU;
   if (q < NX) return {short(F::q + q), short(F::A + q * NX), F::psh, short(F::qx + q), false};  // qx
   q -= NX;
   if (q < NU) return {short(F::r + q), short(F::B + q * NX), F::psh, short(F::qu + q), false};  // qu
@@ -773,6 +768,11 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
   }
   __syncwarp(mask);
   stamp(1);
+  // Huu = sym(Quu), Quu = R (+reg) + B'P B formed by every lane (the same
+  // dot-slot arithmetic as a shared slot) and factored here, so the LDLT and
+  // Huu^-1 overlap this stage's slots instead of following them.
+  double inv[NU * NU];
+  bool pos;
   {
     double o[R2];
     short oo[R2];
@@ -782,13 +782,26 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
       o[r] = dot_slot<NX, F::kVec>(Fm, sl, reg);
       oo[r] = sl.oo;
     }
+    double H[NU * NU];
+#pragma unroll
+    for (int q = 0; q < NU * NU; ++q) {
+      const int a = q % NU, b = q / NU;
+      const DotSlot sl{short(F::R + q), short(F::BtP + a * NX), short(F::B + b * NX), F::DUMMY, a == b};
+      H[q] = dot_slot<NX, F::kVec>(Fm, sl, reg);
+    }
 #pragma unroll
     for (int r = 0; r < R2; ++r) Fm[oo[r]] = o[r];
+    symmetrize<NU>(H);
+    Ldlt<NU> f;
+    f.compute(H);
+    pos = f.positive();
+#pragma unroll
+    for (int t = 0; t < NU * NU; ++t) inv[t] = (t % (NU + 1) == 0) ? 1.0 : 0.0;
+    f.template solve<NU>(inv);
   }
   __syncwarp(mask);
   stamp(2);
-  // Operands of this lane's P / p outputs, loaded before the factorisation so
-  // their shared-memory latency overlaps it (same values, same arithmetic).
+  // Operands of this lane's P / p outputs.
   double s4i[R4][NU], s4j[R4][NU], s4a[R4], s4b[R4];
 #pragma unroll
   for (int r = 0; r < R4; ++r) {
@@ -813,20 +826,8 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
       s4b[r] = 0.0;
     }
   }
-  // Huu = sym(Quu); every lane factors it and forms Huu^-1, then builds the
-  // K / k columns its own outputs need (no shared-memory round trip for K):
-  // K(a, j) = -Huu^-1(a, :) Qux(:, j), k(a) = -Huu^-1(a, :) qu.
-  double H[NU * NU];
-#pragma unroll
-  for (int t = 0; t < NU * NU; ++t) H[t] = Fm[F::Quu + t];
-  symmetrize<NU>(H);
-  Ldlt<NU> f;
-  f.compute(H);
-  const bool pos = f.positive();
-  double inv[NU * NU];
-#pragma unroll
-  for (int t = 0; t < NU * NU; ++t) inv[t] = (t % (NU + 1) == 0) ? 1.0 : 0.0;
-  f.template solve<NU>(inv);
+  // Each lane builds the K / k columns its own outputs need (no shared-memory
+  // round trip for K): K(a, j) = -Huu^-1(a, :) Qux(:, j), k(a) = -Huu^-1(a, :) qu.
   auto kcol = [&](const double* v, double* out) {  // out = -Huu^-1 v
 #pragma unroll
     for (int a = 0; a < NU; ++a) {
