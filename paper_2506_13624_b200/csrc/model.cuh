@@ -308,13 +308,32 @@ __device__ __forceinline__ void node_cost(const ModelParams& mp, int node, bool 
       } else {
         *cost = quad_form<4>(mp.Wx, e) + quad_form<2>(mp.Wu, u);
       }
-      double g[kMaxCon];
-      const int nc = ego_constraints<false>(mp, node, leaf, x, u, g, nullptr, nullptr);
-      *penalty = al_penalty(g, eta, nc, rho);
-      double m = -INFINITY;
+      // ego_constraints + al_penalty + max g fused row by row (same rows, same
+      // expressions, same order), so no constraint array is materialised: a
+      // runtime-indexed g[] lives in local memory on the line-search path.
+      double value = 0.0, m = -INFINITY;
+      auto row = [&](double gm, double em) {
+        if (gm >= 0.0 || em > 0.0) value += em * gm + 0.5 * rho * gm * gm;
+        m = fmax(m, gm);
+      };
+      if (!leaf) {
+        row(u[0] - mp.a_max, eta[0]);
+        row(-u[0] - mp.a_max, eta[1]);
+        row(u[1] - mp.w_max, eta[2]);
+        row(-u[1] - mp.w_max, eta[3]);
+      }
+      const int nb = leaf ? 0 : 4;
+      const double* vp = mp.vehicles + static_cast<long long>(node) * mp.nv * 2;
 #pragma unroll
-      for (int i = 0; i < kMaxCon; ++i)
-        if (i < nc) m = fmax(m, g[i]);
+      for (int v = 0; v < kMaxVehicles; ++v) {
+        if (v < mp.nv) {
+          const double dx = x[0] - vp[2 * v + 0];
+          const double dy = x[1] - vp[2 * v + 1];
+          const double dist = sqrt(dx * dx + dy * dy + 1e-6);
+          row(mp.radius - dist, eta[nb + v]);
+        }
+      }
+      *penalty = value;
       *gmax = m;
       return;
     }
