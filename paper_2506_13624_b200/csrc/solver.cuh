@@ -100,6 +100,13 @@ struct CtaGroupT {
   __device__ int nblocks() const { return 1; }
   __device__ bool leader() const { return threadIdx.x == 0; }
   __device__ void sync() const { __syncthreads(); }
+  // Items of a phase over `total` items: this thread's first / end / step,
+  // and the uniform round count with the k-th round's item (see GridGroup).
+  __device__ int item0(int) const { return threadIdx.x; }
+  __device__ int item_end(int total) const { return total; }
+  __device__ int item_step() const { return bdim(); }
+  __device__ int item_rounds(int total) const { return (total + bdim() - 1) / bdim(); }
+  __device__ int item_at(int, int k) const { return k * bdim() + threadIdx.x; }
   // Fold warp partials sm->part[0..nslot) into sm->total (all threads see it).
   __device__ void finish(int nslot, int nsum) const {
     __syncthreads();
@@ -126,6 +133,20 @@ struct GridGroup {
   __device__ int nblocks() const { return gridDim.x; }
   __device__ bool leader() const { return blockIdx.x == 0 && threadIdx.x == 0; }
   __device__ void sync() const { cg::this_grid().sync(); }
+  // Items of a phase: every block takes a contiguous chunk of ceil(total /
+  // blocks) items, so a phase over fewer items than grid threads (cfg1's
+  // 3,971 nodes vs 37,888 threads) spreads over every SM instead of filling
+  // the first blocks, and a warp still reads consecutive nodes.
+  __device__ int item_chunk(int total) const { return (total + gridDim.x - 1) / gridDim.x; }
+  __device__ int item0(int total) const { return blockIdx.x * item_chunk(total) + threadIdx.x; }
+  __device__ int item_end(int total) const { return min(total, (blockIdx.x + 1) * item_chunk(total)); }
+  __device__ int item_step() const { return blockDim.x; }
+  __device__ int item_rounds(int total) const { return (item_chunk(total) + blockDim.x - 1) / blockDim.x; }
+  // Round k's item (>= item_end when this thread has none in that round).
+  __device__ int item_at(int total, int k) const {
+    const int i = blockIdx.x * item_chunk(total) + k * blockDim.x + threadIdx.x;
+    return i < item_end(total) ? i : total;
+  }
   __device__ void finish(int nslot, int nsum) const {
     __syncthreads();
     const int nw = (blockDim.x + 31) >> 5;
@@ -297,7 +318,7 @@ struct Solver {
   // depth levels in order. Returns false on a non-finite state.
   __device__ bool rollout() {
     // Leaves carry no input (TrajectoryTree, tree.hpp:159-173).
-    for (int i = g.rank(); i < t.n; i += g.size()) {
+    for (int i = g.item0(t.n), i_e = g.item_end(t.n); i < i_e; i += g.item_step()) {
       if (is_leaf(i) || o.zero_inputs) {
 #pragma unroll
         for (int j = 0; j < NU; ++j) w.u[i * NU + j] = 0.0;
@@ -392,7 +413,7 @@ struct Solver {
 
   __device__ Eval evaluate_current() {
     double c = 0, cal = 0, dl = 0, vm = -INFINITY;
-    for (int i = g.rank(); i < t.n; i += g.size()) {
+    for (int i = g.item0(t.n), i_e = g.item_end(t.n); i < i_e; i += g.item_step()) {
       double a, b, d, v;
       node_eval(i, 0.0, &a, &b, &d, &v);
       c += a;
@@ -416,7 +437,7 @@ struct Solver {
   // the smallest failing defect node.
   __device__ Eval linearize_evaluate(int* bad_node, int* bad_code) {
     double c = 0, cal = 0, dl = 0, vm = -INFINITY, bad = 0, badd = 0;
-    for (int i = g.rank(); i < t.n; i += g.size()) {
+    for (int i = g.item0(t.n), i_e = g.item_end(t.n); i < i_e; i += g.item_step()) {
       const bool leaf = is_leaf(i);
       const double* eta = w.eta + static_cast<size_t>(i) * t.max_con;
       const bool ok = node_linearize<NX, NU>(mp, i, leaf, t.weight[i], w.x + i * NX, w.u + i * NU, eta, g_rho,
@@ -453,7 +474,7 @@ struct Solver {
   __device__ void for_depth_items(int d, int per_seg, F&& f) const {
     const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
     const int total = (se - sb) * per_seg;
-    for (int q = g.rank(); q < total; q += g.size()) f(sb + q / per_seg, q % per_seg);
+    for (int q = g.item0(total), q_e = g.item_end(total); q < q_e; q += g.item_step()) f(sb + q / per_seg, q % per_seg);
   }
 
   // Backward suffix scan of segments at depth d, elements already in level 0
@@ -1086,7 +1107,7 @@ struct Solver {
     const int D = t.ndepth;
     double* H = cHc();
     double* h = ch();
-    for (int k = g.rank(); k < n * n; k += g.size()) H[k] = 0.0;
+    for (int k = g.item0(n * n), k_e = g.item_end(n * n); k < k_e; k += g.item_step()) H[k] = 0.0;
     // (1) zero-input perturbations z, depth by depth (the boundary: heads of depth D-1).
     for (int d = 0; d < D; ++d) {
       const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
@@ -1219,7 +1240,7 @@ struct Solver {
     // (6) open-loop policies of the shared nodes.
     if (err == kBwdOk) {
       const double* u = cu();
-      for (int i = g.rank(); i < m; i += g.size()) {
+      for (int i = g.item0(m), i_e = g.item_end(m); i < i_e; i += g.item_step()) {
 #pragma unroll
         for (int q = 0; q < NU * NX; ++q) pol(i)[PL::K + q] = 0.0;
 #pragma unroll
@@ -1301,7 +1322,7 @@ struct Solver {
     // Policies of scanned chain nodes from their successor's value
     // (feedback_from_values, lqr_scan.hpp:146); max_feedforward.
     double mff = 0.0;
-    for (int i = g.rank(); i < t.n; i += g.size()) {
+    for (int i = g.item0(t.n), i_e = g.item_end(t.n); i < i_e; i += g.item_step()) {
       if (is_leaf(i)) continue;
       const int s = t.node_seg[i], k = t.node_pos[i];
       if constexpr (!kSeqOnly) {
@@ -1345,7 +1366,7 @@ struct Solver {
   __device__ void for_multi_depth_items(PerSeg&& per_seg, F&& f) const {
     int total = 0;
     for (int d = 0; d < t.ndepth; ++d) total += (t.depth_begin[d + 1] - t.depth_begin[d]) * per_seg(d);
-    for (int q = g.rank(); q < total; q += g.size()) {
+    for (int q = g.item0(total), q_e = g.item_end(total); q < q_e; q += g.item_step()) {
       int r = q, d = 0;
       for (; d < t.ndepth; ++d) {
         const int cnt = (t.depth_begin[d + 1] - t.depth_begin[d]) * per_seg(d);
@@ -1460,7 +1481,7 @@ struct Solver {
     mark(6);
     // EC terms per node (solver.hpp:416-428).
     double a1 = 0.0, a2 = 0.0;
-    for (int i = g.rank(); i < t.n; i += g.size()) {
+    for (int i = g.item0(t.n), i_e = g.item_end(t.n); i < i_e; i += g.item_step()) {
       const double* si = stage(i);
       const double* dxi = w.dx + i * NX;
       if constexpr (NX == 4 && NU == 2) {
@@ -1877,12 +1898,11 @@ struct Solver {
   __device__ int line_search(int levels, double merit0, double a1, double a2, double mu, double dl1_nom,
                              Eval* chosen, double* merit_chosen, double* decrease_chosen, int* evals) {
     const int blk = o.ls_block > 0 ? min(o.ls_block, kMaxAlpha) : levels;
-    const int gsz = g.size();
     for (int l0 = 0; l0 < levels; l0 += blk) {
       const int nl = min(blk, levels - l0);
       *evals += nl;
-      for (int base = 0; base < t.n; base += gsz) {
-        const int i = base + g.rank();
+      for (int rnd = 0, nrnd = g.item_rounds(t.n); rnd < nrnd; ++rnd) {
+        const int i = g.item_at(t.n, rnd);
         const bool valid = i < t.n;
         const bool leaf = valid ? is_leaf(i) : true;
         const int p = valid ? t.parent[i] : -1;
@@ -1931,7 +1951,7 @@ struct Solver {
               dl = sd;
             }
           }
-          const bool first = base == 0;
+          const bool first = rnd == 0;
           red_acc(g, 3 * q + 0, c, true, first);
           red_acc(g, 3 * q + 1, cal, true, first);
           red_acc(g, 3 * q + 2, dl, true, first);
@@ -2049,7 +2069,7 @@ struct Solver {
   // evaluate (problem.hpp:109-146) of the trajectory held in (dx, du).
   __device__ Eval evaluate_trial() {
     double c = 0, cal = 0, dl = 0, vm = -INFINITY;
-    for (int i = g.rank(); i < t.n; i += g.size()) {
+    for (int i = g.item0(t.n), i_e = g.item_end(t.n); i < i_e; i += g.item_step()) {
       const bool leaf = is_leaf(i);
       const double* xi = w.dx + i * NX;
       double u[NU];
@@ -2102,7 +2122,7 @@ struct Solver {
 
   // Accept the trial held in (dx, du).
   __device__ void take_trial() {
-    for (int i = g.rank(); i < t.n; i += g.size()) {
+    for (int i = g.item0(t.n), i_e = g.item_end(t.n); i < i_e; i += g.item_step()) {
 #pragma unroll
       for (int j = 0; j < NX; ++j) w.x[i * NX + j] = w.dx[i * NX + j];
 #pragma unroll
@@ -2112,7 +2132,7 @@ struct Solver {
   }
 
   __device__ void take_step(double alpha) {
-    for (int i = g.rank(); i < t.n; i += g.size()) {
+    for (int i = g.item0(t.n), i_e = g.item_end(t.n); i < i_e; i += g.item_step()) {
 #pragma unroll
       for (int j = 0; j < NX; ++j) w.x[i * NX + j] = fma(alpha, w.dx[i * NX + j], w.x[i * NX + j]);
       if (!is_leaf(i)) {
@@ -2125,7 +2145,7 @@ struct Solver {
 
   // Projected multiplier update (solver.hpp:764-769).
   __device__ void update_multipliers(double rho) {
-    for (int i = g.rank(); i < t.n; i += g.size()) {
+    for (int i = g.item0(t.n), i_e = g.item_end(t.n); i < i_e; i += g.item_step()) {
       double gv[kMaxCon];
       const int nc = node_constraints<NX, NU>(mp, i, is_leaf(i), w.x + i * NX, w.u + i * NU, gv);
       double* eta = w.eta + static_cast<size_t>(i) * t.max_con;
@@ -2212,11 +2232,11 @@ struct Solver {
         return;
       }
       // eta = 0; the caller filled w.u with the initial inputs.
-      for (int i = g.rank(); i < t.n * t.max_con; i += g.size()) w.eta[i] = 0.0;
+      for (int i = g.item0(t.n * t.max_con), i_e = g.item_end(t.n * t.max_con); i < i_e; i += g.item_step()) w.eta[i] = 0.0;
       if constexpr (NX == 4 && NU == 2) {
         if (structured())  // constant part of every stage record, once per solve
           if (!compact())
-            for (int i = g.rank(); i < t.n; i += g.size()) unicycle_stage_constants(mp.dt, is_leaf(i), stage(i));
+            for (int i = g.item0(t.n), i_e = g.item_end(t.n); i < i_e; i += g.item_step()) unicycle_stage_constants(mp.dt, is_leaf(i), stage(i));
       }
       g_rho = o.penalty_init;
       if (!rollout()) {
@@ -2401,7 +2421,7 @@ struct Solver {
     double max_ff = 0.0;
     const int err = backward(reg, &max_ff);
     if (w.value) {
-      for (int i = g.rank(); i < t.n; i += g.size()) {
+      for (int i = g.item0(t.n), i_e = g.item_end(t.n); i < i_e; i += g.item_step()) {
         if (!seq_seg(t.node_seg[i])) {
           const double* v = value_of(i);
           copy<NX * NX>(v + BL::P, w.value + static_cast<size_t>(i) * VL::stride + VL::P);
