@@ -898,9 +898,11 @@ __device__ int team_riccati_step_u(double reg, unsigned mask, double* Fm, int la
     // step's shared-memory loads behind it.
     if (V_g && g4[r] >= 0) __stcg(V_g + g4[r], o4[r]);
   }
-  const unsigned bad = __ballot_sync(mask, !pos);
+  // Every lane factored the same Huu with the same instructions, so `pos`
+  // is uniform across the team: no vote needed (the next step opens with a
+  // __syncwarp).
   stamp(5);
-  return bad ? kIndefinite : kBwdOk;
+  return pos ? kBwdOk : kIndefinite;
 }
 
 }  // namespace bmpc_b200

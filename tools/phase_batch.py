@@ -25,6 +25,7 @@ for inst in (0, cnt // 2):
     passes = r.n_records + r.outer_iterations
     cps = prof.pop("sweep_cycles_per_step", None)
     wk = prof.pop("walk_cycles", (0,) * 6)
+    prof.pop("fwd_scan_cycles", None)
     print(f"   effective SM clock during the solve: {prof.pop('sm_mhz', 0):.0f} MHz")
     print(f"   walk cycles/pass: head_dx {wk[0] / passes:.0f}, chunks {wk[1] / passes:.0f}, depth walks {wk[2] / passes:.0f} ({wk[3] / passes:.0f} ns); element phases {wk[4] / passes:.0f}, chain (thread 0) {wk[5] / passes:.0f}")
     tot = sum(prof.values())
