@@ -464,9 +464,10 @@ __device__ int team_combine_bwd(const double* e1g, const double* e2g, double* ou
     out[E::c + lane] = c_out;
     out[E::p + lane] = p_out;
   }
-  const unsigned bad = __ballot_sync(mask, !ok);
+  // Per-lane status: the callers fold error codes with a max over every
+  // thread, so the team needs no vote here.
   __syncwarp(mask);
-  return bad ? kFactorization : kBwdOk;
+  return ok ? kBwdOk : kFactorization;
 }
 
 // combine_fwd (lqr_scan.hpp:171-173): (A2 A1, A2 c1 + c2).
