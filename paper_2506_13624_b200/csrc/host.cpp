@@ -1445,6 +1445,9 @@ static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_input
   // sweep in the solve kernels (cfg0 alone, 256 threads: 129 vs 80 us per
   // pass; cfg3-spread on the whole GPU: 147 vs 82 ms).
   d.chunk_bwd = 0;
+  // Scanned depths whose elements fit ~2 rounds of the group's teams take the
+  // Hillis-Steele scan (one barrier per level); BMPC_BWD_HS=<rounds> (0: off).
+  d.bwd_hs = std::getenv("BMPC_BWD_HS") ? std::atoi(std::getenv("BMPC_BWD_HS")) : 2;
   // Segments of >= 256 transitions in the wide non-lean kernels: the
   // parallel forward scan (below that the one-thread walk is as fast: cfg3's
   // 99/199-step segments); BMPC_FWD_BLOCK_SCAN=<min transitions> (0: walk).

@@ -496,7 +496,54 @@ struct Solver {
 
   // Backward suffix scan of segments at depth d, elements already in level 0
   // (reversed). f(a, b) = combine_bwd(first = b, second = a).
+  // Hillis-Steele form of the same suffix scan for depths whose elements fit
+  // the group's teams in a couple of rounds (cfg1's 4 x 990 on the whole
+  // grid): ceil(log2 E) levels of S_j = f(S_{j-o}, S_j) ping-ponged between
+  // slots [0, E) and [E, 2E), one barrier per level, instead of the
+  // work-efficient pairing's 2 log2 E barriers.
+  __device__ bool hs_bwd_depth(int d) const {
+    if constexpr (kTS <= 0) return false;
+    const int E = t.depth_len[d], ns = t.depth_begin[d + 1] - t.depth_begin[d];
+    return o.bwd_hs > 0 && E >= 4 && ns * E <= o.bwd_hs * (g.size() / max(kTS, 1));
+  }
+  __device__ int scan_bwd_depth_hs(int d) {
+    const int E = t.depth_len[d];
+    int err = kBwdOk;
+    if constexpr (kTS > 0) {
+      TeamSmem<NX>& my = comb_smem();
+      int src = 0;
+      for (int off = 1; off < E; off <<= 1) {
+        const int dst = E - src;  // the other half
+        for_depth_items_team(d, E, [&](int s, int j, int lane, unsigned mask) {
+          const int base = t.seg_scratch[s];
+          double* out = bwd(base + dst + j);
+          if (j >= off) {
+            const int e = team_combine_bwd<NX, kTS>(bwd(base + src + j), bwd(base + src + j - off), out, lane,
+                                                     mask, my);
+            err = err ? err : e;
+          } else {
+            const double* in = bwd(base + src + j);
+            for (int k = lane; k < BL::size; k += kTS) out[k] = in[k];
+          }
+        });
+        g.sync();
+        src = dst;
+      }
+      if (src != 0) {  // results back to slots [0, E) (value_of reads them there)
+        for_depth_items_team(d, E, [&](int s, int j, int lane, unsigned) {
+          const int base = t.seg_scratch[s];
+          const double* in = bwd(base + src + j);
+          double* out = bwd(base + j);
+          for (int k = lane; k < BL::size; k += kTS) out[k] = in[k];
+        });
+        g.sync();
+      }
+    }
+    return err;
+  }
+
   __device__ int scan_bwd_depth(int d) {
+    if (hs_bwd_depth(d)) return scan_bwd_depth_hs(d);
     const int E = t.depth_len[d];
     const int U = up_steps(E);
     int err = kBwdOk;

@@ -45,6 +45,7 @@ struct DevOptions {  // SolverOptions (solver.hpp:28-58), device copy
   int nonlinear_ls; // 1: ForwardMode::nonlinear_rollout trials (sssilqr, solver.hpp:463-467)
   int chunk_bwd;    // > 0: kChunk kernels sweep segments of >= this many nodes with the chunked scan
   int condensed;    // 1: BackwardStrategy::scan_condensed (hypmsilqr): P2 by condensing + dense solve
+  int bwd_hs;       // > 0: Hillis-Steele backward scan where segments x length <= bwd_hs x teams
   int fwd_block_scan;  // > 0: wide blocks roll segments of >= this many transitions out by a block-local affine-map scan
 };
 
