@@ -299,6 +299,20 @@ struct Solver {
     if (kSeqOnly) return true;
     if (kTS <= 0 || o.seq_max_len <= 0) return false;
     const int L = t.depth_len[d], ns = t.depth_begin[d + 1] - t.depth_begin[d];
+    if constexpr (std::is_same<G, GridGroup>::value) {
+      // Whole-GPU kernel: a depth with few segments leaves most teams idle
+      // under the sweep; the Hillis-Steele scan takes ceil(log2 L) barrier-
+      // separated levels of ceil(ns L / teams) team combines instead of L - 1
+      // dependent steps. Measured costs (cycles): team Riccati step ~1,900 in
+      // this kernel, team combine ~8,000, grid barrier ~3,000, elements ~10,000.
+      if (hs_bwd_depth(d)) {
+        const int teams = g.size() / kTS;
+        const int rounds = (ns * L + teams - 1) / teams;
+        const int levels = 32 - __clz(L - 1);
+        const long long hs = static_cast<long long>(levels) * (rounds * 8000 + 3000) + 10000;
+        if (hs * 5 < static_cast<long long>(L - 1) * 1900 * 4) return false;
+      }
+    }
     return L <= o.seq_max_len || (o.seq_wide_segs > 0 && ns >= o.seq_wide_segs && L <= o.seq_wide_max);
   }
   __device__ bool seq_seg(int s) const { return kSeqOnly || seq_depth(t.seg_depth[s]); }
