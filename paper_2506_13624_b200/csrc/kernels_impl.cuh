@@ -67,7 +67,10 @@ __global__ void __launch_bounds__(256) solve_grid_kernel(const Topo* __restrict_
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   red.part = reinterpret_cast<double*>(dyn_smem);
   __syncthreads();
-  Solver<NX, NU, GridGroup, false, 0, FEAT> s(GridGroup{&red, red_scratch, nullptr}, ctx.topo, ctx.mp, ctx.work, opts);
+  // One warp per team, as in the 256-thread per-instance kernels.
+  constexpr int kTeam = team_size<NX, NU>() == 16 ? 32 : 0;
+  Solver<NX, NU, GridGroup, false, kTeam, FEAT> s(GridGroup{&red, red_scratch, nullptr}, ctx.topo, ctx.mp, ctx.work,
+                                                  opts);
   s.tsm = dyn_smem + red_smem_bytes(blockDim.x);
   s.wbuf = reinterpret_cast<double*>(s.tsm);
   s.wcap = blockDim.x;

@@ -303,14 +303,15 @@ struct Solver {
       // Whole-GPU kernel: a depth with few segments leaves most teams idle
       // under the sweep; the Hillis-Steele scan takes ceil(log2 L) barrier-
       // separated levels of ceil(ns L / teams) team combines instead of L - 1
-      // dependent steps. Measured costs (cycles): team Riccati step ~1,900 in
-      // this kernel, team combine ~8,000, grid barrier ~3,000, elements ~10,000.
+      // dependent steps. Measured costs (cycles): 32-lane team Riccati step
+      // ~1,450 in this kernel, 16-lane team combine ~8,000, grid barrier
+      // ~3,000, elements ~10,000.
       if (hs_bwd_depth(d)) {
-        const int teams = g.size() / kTS;
+        const int teams = g.size() / kTSC;
         const int rounds = (ns * L + teams - 1) / teams;
         const int levels = 32 - __clz(L - 1);
         const long long hs = static_cast<long long>(levels) * (rounds * 8000 + 3000) + 10000;
-        if (hs * 5 < static_cast<long long>(L - 1) * 1900 * 4) return false;
+        if (hs * 5 < static_cast<long long>(L - 1) * 1450 * 4) return false;
       }
     }
     return L <= o.seq_max_len || (o.seq_wide_segs > 0 && ns >= o.seq_wide_segs && L <= o.seq_wide_max);
@@ -495,16 +496,20 @@ struct Solver {
   // (reversed). f(a, b) = combine_bwd(first = b, second = a).
   // Team size of the cooperative combine (0: one thread per combination).
   static constexpr int kTS = kTeam > 0 ? kTeam : team_size<NX, NU>();
+  // Team size of the scan's combines: the 16-lane teams the shared-memory
+  // slots are sized for (twice the teams of the 32-lane sweep in the
+  // 256-thread and whole-GPU kernels; a combine needs only NX*NX lanes).
+  static constexpr int kTSC = team_size<NX, NU>() > 0 ? team_size<NX, NU>() : kTS;
 
-  // Items of a per-segment phase, one kTS-lane team per item.
+  // Items of a per-segment phase, one kTSC-lane team per item.
   template <class F>
   __device__ void for_depth_items_team(int d, int per_seg, F&& f) const {
     const int sb = t.depth_begin[d], se = t.depth_begin[d + 1];
     const int total = (se - sb) * per_seg;
-    const int team = g.rank() / kTS, nteams = g.size() / kTS;
-    const int lane = threadIdx.x % kTS;
+    const int team = g.rank() / kTSC, nteams = g.size() / kTSC;
+    const int lane = threadIdx.x % kTSC;
     const unsigned mask =
-        kTS == 32 ? 0xffffffffu : (((1u << kTS) - 1u) << ((threadIdx.x & 31) / kTS * kTS));
+        kTSC == 32 ? 0xffffffffu : (((1u << kTSC) - 1u) << ((threadIdx.x & 31) / kTSC * kTSC));
     for (int q = team; q < total; q += nteams) f(sb + q / per_seg, q % per_seg, lane, mask);
   }
 
@@ -516,14 +521,14 @@ struct Solver {
   // slots [0, E) and [E, 2E), one barrier per level, instead of the
   // work-efficient pairing's 2 log2 E barriers.
   __device__ bool hs_bwd_depth(int d) const {
-    if constexpr (kTS <= 0) return false;
+    if constexpr (kTSC <= 0) return false;
     const int E = t.depth_len[d], ns = t.depth_begin[d + 1] - t.depth_begin[d];
-    return o.bwd_hs > 0 && E >= 4 && ns * E <= o.bwd_hs * (g.size() / max(kTS, 1));
+    return o.bwd_hs > 0 && E >= 4 && ns * E <= o.bwd_hs * (g.size() / max(kTSC, 1));
   }
   __device__ int scan_bwd_depth_hs(int d) {
     const int E = t.depth_len[d];
     int err = kBwdOk;
-    if constexpr (kTS > 0) {
+    if constexpr (kTSC > 0) {
       TeamSmem<NX>& my = comb_smem();
       int src = 0;
       for (int off = 1; off < E; off <<= 1) {
@@ -532,12 +537,12 @@ struct Solver {
           const int base = t.seg_scratch[s];
           double* out = bwd(base + dst + j);
           if (j >= off) {
-            const int e = team_combine_bwd<NX, kTS>(bwd(base + src + j), bwd(base + src + j - off), out, lane,
+            const int e = team_combine_bwd<NX, kTSC>(bwd(base + src + j), bwd(base + src + j - off), out, lane,
                                                      mask, my);
             err = err ? err : e;
           } else {
             const double* in = bwd(base + src + j);
-            for (int k = lane; k < BL::size; k += kTS) out[k] = in[k];
+            for (int k = lane; k < BL::size; k += kTSC) out[k] = in[k];
           }
         });
         g.sync();
@@ -548,7 +553,7 @@ struct Solver {
           const int base = t.seg_scratch[s];
           const double* in = bwd(base + src + j);
           double* out = bwd(base + j);
-          for (int k = lane; k < BL::size; k += kTS) out[k] = in[k];
+          for (int k = lane; k < BL::size; k += kTSC) out[k] = in[k];
         });
         g.sync();
       }
@@ -561,7 +566,7 @@ struct Solver {
     const int E = t.depth_len[d];
     const int U = up_steps(E);
     int err = kBwdOk;
-    if constexpr (kTS > 0) {
+    if constexpr (kTSC > 0) {
       TeamSmem<NX>& my = comb_smem();
       for (int l = 0; l < U; ++l) {
         const int nl = level_size(E, l), nn = (nl + 1) >> 1;
@@ -570,12 +575,12 @@ struct Solver {
           const int base = t.seg_scratch[s];
           double* dst = bwd(base + on + i);
           if (2 * i + 1 < nl) {
-            const int e = team_combine_bwd<NX, kTS>(bwd(base + ol + 2 * i + 1), bwd(base + ol + 2 * i), dst, lane,
+            const int e = team_combine_bwd<NX, kTSC>(bwd(base + ol + 2 * i + 1), bwd(base + ol + 2 * i), dst, lane,
                                                      mask, my);
             err = err ? err : e;
           } else {
             const double* src = bwd(base + ol + 2 * i);
-            for (int k = lane; k < BL::size; k += kTS) dst[k] = src[k];
+            for (int k = lane; k < BL::size; k += kTSC) dst[k] = src[k];
           }
         });
         g.sync();
@@ -589,11 +594,11 @@ struct Solver {
           if (2 * i + 1 < nl) {
             const double* src = S + static_cast<size_t>(i) * BL::stride;
             double* dst = bwd(base + ol + 2 * i + 1);
-            for (int k = lane; k < BL::size; k += kTS) dst[k] = src[k];
+            for (int k = lane; k < BL::size; k += kTSC) dst[k] = src[k];
           }
           if (i >= 1) {
             double* a = bwd(base + ol + 2 * i);
-            const int e = team_combine_bwd<NX, kTS>(a, S + static_cast<size_t>(i - 1) * BL::stride, a, lane, mask, my);
+            const int e = team_combine_bwd<NX, kTSC>(a, S + static_cast<size_t>(i - 1) * BL::stride, a, lane, mask, my);
             err = err ? err : e;
           }
         });
@@ -646,7 +651,7 @@ struct Solver {
     return *reinterpret_cast<RicSmem<NX, NU>*>(reinterpret_cast<unsigned char*>(tsm) + (threadIdx.x / kTS) * slot_bytes());
   }
   __device__ TeamSmem<NX>& comb_smem() const {
-    return *reinterpret_cast<TeamSmem<NX>*>(reinterpret_cast<unsigned char*>(tsm) + (threadIdx.x / kTS) * slot_bytes());
+    return *reinterpret_cast<TeamSmem<NX>*>(reinterpret_cast<unsigned char*>(tsm) + (threadIdx.x / kTSC) * slot_bytes());
   }
   __host__ __device__ static constexpr size_t slot_bytes() {
     constexpr size_t a = sizeof(TeamSmem<NX>) > sizeof(RicSmem<NX, NU>) ? sizeof(TeamSmem<NX>) : sizeof(RicSmem<NX, NU>);
