@@ -1448,10 +1448,10 @@ static int batch_launch(bmpc_batch* b, const bmpc_options* opts, bool zero_input
   // Scanned depths whose elements fit ~2 rounds of the group's teams take the
   // Hillis-Steele scan (one barrier per level); BMPC_BWD_HS=<rounds> (0: off).
   d.bwd_hs = std::getenv("BMPC_BWD_HS") ? std::atoi(std::getenv("BMPC_BWD_HS")) : 2;
-  // Segments of >= 256 transitions in the wide non-lean kernels: the
-  // parallel forward scan (below that the one-thread walk is as fast: cfg3's
-  // 99/199-step segments); BMPC_FWD_BLOCK_SCAN=<min transitions> (0: walk).
-  d.fwd_block_scan = std::getenv("BMPC_FWD_BLOCK_SCAN") ? std::atoi(std::getenv("BMPC_FWD_BLOCK_SCAN")) : 256;
+  // Segments of >= 64 transitions in the wide non-lean kernels: the parallel
+  // forward scan (cfg3's 99/199-step segments gain ~1 %, cfg1's 990-step ones
+  // halve; shorter segments walk); BMPC_FWD_BLOCK_SCAN=<min transitions> (0: walk).
+  d.fwd_block_scan = std::getenv("BMPC_FWD_BLOCK_SCAN") ? std::atoi(std::getenv("BMPC_FWD_BLOCK_SCAN")) : 64;
   // Strategy enums (solver.hpp:23-26; presets bench.cpp:60-83).
   if (o.backward < 0 || o.backward > 2 || o.forward < 0 || o.forward > 1 || o.line_search < 0 || o.line_search > 1)
     return fail(BMPC_ERR_INVALID, "unknown backward / forward / line_search strategy");
