@@ -16,6 +16,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -1551,10 +1552,26 @@ int bmpc_batch_results(bmpc_batch* b, double* x_out, double* u_out, bmpc_report*
     }
     ck(cudaStreamSynchronize(s), "sync");
     if (x_out || u_out) {
-      for (size_t i = 0; i < C; ++i) {
-        const double* src = b->h_pack + i * per;
-        if (x_out) std::memcpy(x_out + i * n * b->nx, src, n * b->nx * sizeof(double));
-        if (u_out) std::memcpy(u_out + i * n * b->nu, src + n * b->nx, n * b->nu * sizeof(double));
+      // Unpack [x | u] per instance into the caller's arrays; large batches
+      // split over a few host threads (a single core copies ~50 MB, the cfg4
+      // step's trajectories, at a fraction of the link rate).
+      auto unpack = [&](size_t lo, size_t hi) {
+        for (size_t i = lo; i < hi; ++i) {
+          const double* src = b->h_pack + i * per;
+          if (x_out) std::memcpy(x_out + i * n * b->nx, src, n * b->nx * sizeof(double));
+          if (u_out) std::memcpy(u_out + i * n * b->nu, src + n * b->nx, n * b->nu * sizeof(double));
+        }
+      };
+      const size_t total_bytes = C * per * sizeof(double);
+      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+      const size_t nt = total_bytes < (size_t{4} << 20) ? 1 : std::min<size_t>(std::min<size_t>(hw, 8), C);
+      if (nt <= 1) {
+        unpack(0, C);
+      } else {
+        std::vector<std::thread> pool;
+        for (size_t k = 1; k < nt; ++k) pool.emplace_back(unpack, k * C / nt, (k + 1) * C / nt);
+        unpack(0, C / nt);
+        for (auto& th : pool) th.join();
       }
     }
     if (reports)
