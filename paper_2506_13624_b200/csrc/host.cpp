@@ -1147,28 +1147,45 @@ int bmpc_batch_set_models(bmpc_batch* b, const bmpc_model_desc* models, size_t* 
       if (m.kind != b->kind || m.state_dim != b->nx || m.input_dim != b->nu ||
           (b->kind == BMPC_MODEL_UNICYCLE && m.num_vehicles != b->nv))
         return fail(BMPC_ERR_INVALID, "model " + std::to_string(i) + " does not match the batch template");
-      ModelParams& mp = b->h_mps[i];
-      double* md = hs + i * b->node_data_doubles;
-      if (b->kind == BMPC_MODEL_UNICYCLE) {
-        mp.dt = m.dt;
-        std::memcpy(mp.Wx, m.state_weights, sizeof mp.Wx);
-        std::memcpy(mp.Wu, m.input_weights, sizeof mp.Wu);
-        std::memcpy(mp.Wf, m.terminal_weights, sizeof mp.Wf);
-        mp.a_max = m.accel_limit;
-        mp.w_max = m.yaw_rate_limit;
-        mp.radius = m.safety_radius;
-        // BMPC_DENSE_MODEL=1 forces the dense expansion (tests compare both bitwise).
-        mp.w_diag = is_diag(mp.Wx, 4) && is_diag(mp.Wu, 2) && is_diag(mp.Wf, 4) && !std::getenv("BMPC_DENSE_MODEL");
-        std::memcpy(md, m.reference, n * 4 * sizeof(double));
-        if (b->nv > 0) std::memcpy(md + align2(n * 4), m.vehicle_position, n * static_cast<size_t>(b->nv) * 2 * sizeof(double));
-      } else {
-        std::memcpy(md, m.lq_stage, n * lq_stage_size(b->nx, b->nu) * sizeof(double));
-        std::memcpy(md + align2(n * lq_stage_size(b->nx, b->nu)), m.lq_leaf,
-                    n * static_cast<size_t>(b->nx * b->nx + b->nx) * sizeof(double));
-      }
-      std::memcpy(hx0 + i * x0s, m.initial_state, static_cast<size_t>(b->nx) * sizeof(double));
     }
+    const bool dense_env = std::getenv("BMPC_DENSE_MODEL") != nullptr;
+    // Gather split over a few host threads for large batches (cfg4: 67 MB).
+    auto gather = [&](size_t lo, size_t hi) {
+      for (size_t i = lo; i < hi; ++i) {
+        const bmpc_model_desc& m = models[i];
+        ModelParams& mp = b->h_mps[i];
+        double* md = hs + i * b->node_data_doubles;
+        if (b->kind == BMPC_MODEL_UNICYCLE) {
+          mp.dt = m.dt;
+          std::memcpy(mp.Wx, m.state_weights, sizeof mp.Wx);
+          std::memcpy(mp.Wu, m.input_weights, sizeof mp.Wu);
+          std::memcpy(mp.Wf, m.terminal_weights, sizeof mp.Wf);
+          mp.a_max = m.accel_limit;
+          mp.w_max = m.yaw_rate_limit;
+          mp.radius = m.safety_radius;
+          // BMPC_DENSE_MODEL=1 forces the dense expansion (tests compare both bitwise).
+          mp.w_diag = is_diag(mp.Wx, 4) && is_diag(mp.Wu, 2) && is_diag(mp.Wf, 4) && !dense_env;
+          std::memcpy(md, m.reference, n * 4 * sizeof(double));
+          if (b->nv > 0) std::memcpy(md + align2(n * 4), m.vehicle_position, n * static_cast<size_t>(b->nv) * 2 * sizeof(double));
+        } else {
+          std::memcpy(md, m.lq_stage, n * lq_stage_size(b->nx, b->nu) * sizeof(double));
+          std::memcpy(md + align2(n * lq_stage_size(b->nx, b->nu)), m.lq_leaf,
+                      n * static_cast<size_t>(b->nx * b->nx + b->nx) * sizeof(double));
+        }
+        std::memcpy(hx0 + i * x0s, m.initial_state, static_cast<size_t>(b->nx) * sizeof(double));
+      }
+    };
     const size_t bytes_data = C * b->node_data_doubles * sizeof(double);
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nt = bytes_data < (size_t{4} << 20) ? 1 : std::min<size_t>(std::min<size_t>(hw, 8), C);
+    if (nt <= 1) {
+      gather(0, C);
+    } else {
+      std::vector<std::thread> pool;
+      for (size_t k = 1; k < nt; ++k) pool.emplace_back(gather, k * C / nt, (k + 1) * C / nt);
+      gather(0, C / nt);
+      for (auto& th : pool) th.join();
+    }
     ck(cudaMemcpyAsync(b->model_data.p, hs, bytes_data, cudaMemcpyHostToDevice, s), "h2d");
     ck(cudaMemcpyAsync(b->x0.p, hx0, C * x0s * sizeof(double), cudaMemcpyHostToDevice, s), "h2d");
     ck(cudaMemcpyAsync(b->mps.p, b->h_mps.data(), b->h_mps.size() * sizeof(ModelParams), cudaMemcpyHostToDevice, s),
