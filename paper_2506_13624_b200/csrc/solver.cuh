@@ -702,7 +702,9 @@ struct Solver {
       const int e = team_riccati_step_u<NX, NU, TS>(reg, mask, Fm, lane, vi, pbase + static_cast<size_t>(i) * PL::stride);
       err = err ? err : e;
       if (k > k_lo) {
-        __syncwarp(mask);
+        // No barrier needed: every lane passed the step's stage-2 __syncwarp,
+        // after which nothing reads the stage record; the next step opens
+        // with one before it reads what is staged here.
 #pragma unroll
         for (int j = 0; j < PRE; ++j) {
           const int idx = lane + j * TS;
@@ -759,7 +761,9 @@ struct Solver {
       const int e = team_riccati_step_u<NX, NU, TS>(reg, mask, Fm, lane, vi, pbase + static_cast<size_t>(i) * PL::stride);
       err = err ? err : e;
       if (k > k_lo) {
-        __syncwarp(mask);
+        // No barrier needed: every lane passed the step's stage-2 __syncwarp,
+        // after which nothing reads the stage record; the next step opens
+        // with one before it reads what is staged here.
 #pragma unroll
         for (int j = 0; j < PRE; ++j)
           if (lane + j * TS < UniRec::kVar) Fm[F::S + dst[j]] = pre[j];
